@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""QTIP fused trellis-decode GEMV benchmark (BASELINE.json metric: compressed-byte HBM GB/s vs
+peak; us/layer at batch 1).
+
+Step (default workload `llama2-7b`, BASELINE configs[1]): one batch-1 decode token through the
+linear layers of all 32 Llama-2-7B decoder blocks -- q, k, v, o (4096x4096), gate, up
+(11008x4096), down (4096x11008) -- each layer = RHT-in -> fused decode-GEMV -> RHT-out, k=2 3INST,
+L=16, V=1, T=256 tail-biting, every layer its own weights (1.62 GB of packed stream > 126 MB L2,
+so no layer is L2-resident when it is read again next step).  value = compressed bytes / step
+time (GB/s), whole job.  With torchrun (N>1) every layer is row-sharded across ranks and the
+y~ shards are all-gathered over NCCL before the replicated RHT-out (strong scaling).
+
+`--impl reference` times the CPU oracle (the tier's reference arm) on a bounded sample.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+WORKLOADS = {
+    # name: (blocks, [(m, n) per linear in a block], default code, default k)
+    "llama2-7b": (32, [(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)], "3inst", 2),
+    "llama2-70b": (80, [(8192, 8192), (1024, 8192), (1024, 8192), (8192, 8192), (28672, 8192), (28672, 8192),
+                        (8192, 28672)], "hyb", 3),
+    "c4-70b": (8, [(8192, 28672), (28672, 8192)], "3inst", 2),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def oracle_sample(m=2048, n=4096, code="3inst", k=2, reps=1):
+    """Plain oracle (single thread): decode + float64 RHT-in / GEMV / RHT-out of one m x n layer."""
+    from threadpoolctl import threadpool_limits
+    from oracle import gemv
+    tiles = synth.random_tiles(m, n, k, seed=1000)
+    lut = synth.gaussian_lut(9) if code == "hyb" else None
+    x = synth.random_x(1, n).astype(np.float64)
+    sm, sn = synth.random_sign_bytes(m, 3001), synth.random_sign_bytes(n, 3000)
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    times = []
+    with threadpool_limits(1):
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            W = gemv.dense_decode(tiles, p)
+            gemv.matvec(W, x, sn, sm, scale=1.0)
+            times.append(time.perf_counter() - t0)
+    nbytes = m * n * k / 8
+    return nbytes, times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    code = args.code or wl[2]
+    k = args.k or wl[3]
+    m, n = 2048, 4096
+    oracle_sample(256, 256, code, k, reps=1)                       # import / table warm-up
+    for _ in range(args.warmup):
+        oracle_sample(m, n, code, k, reps=1)
+    nbytes, times = oracle_sample(m, n, code, k, reps=args.steps)
+    tot = sum(times)
+    value = nbytes * args.steps / tot / 1e9
+    sample = f"one {m}x{n} {code} k={k} layer per step (decode + float64 RHT-in/GEMV/RHT-out), single thread"
+    line = {"metric": "fused trellis-decode GEMV: compressed-byte HBM GB/s vs peak; us/layer batch=1",
+            "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "code": code, "k": k, "batch": 1, "sample": sample},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_11235_b200 import qtip
+    from paper_2406_11235_b200.layer import QTIPLinear
+    from paper_2406_11235_b200.sharded import ShardedQTIPLinear
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    qtip.load()
+    qtip.set_matvec_impl(args.matvec_impl)
+
+    nblocks, shapes, dcode, dk = WORKLOADS[args.workload]
+    if args.blocks:
+        nblocks = args.blocks
+    code = args.code or dcode
+    k = args.k or dk
+    B = args.batch
+    lut = synth.gaussian_lut(9) if code == "hyb" else None
+
+    # one prototype per distinct shape, copied device-to-device into every layer instance
+    protos = {}
+    for si, (m, n) in enumerate(sorted(set(shapes))):
+        tiles = synth.random_tiles(m, n, k, seed=1000 + si)
+        sm, sn = synth.random_sign_bytes(m, 3001 + si), synth.random_sign_bytes(n, 3000 + si)
+        if world == 1:
+            lay = QTIPLinear(m, n, code=code, k=k, device=dev).load_tiles(tiles, sm, sn, scale=1.0, lut=lut)
+        else:
+            lay = ShardedQTIPLinear(m, n, rank, world, code=code, k=k, device=dev).load_tiles(tiles, sm, sn, lut=lut)
+        protos[(m, n)] = lay
+        del tiles
+    layers = []
+    for b in range(nblocks):
+        for (m, n) in shapes:
+            pr = protos[(m, n)]
+            if world == 1:
+                lay = QTIPLinear(m, n, code=code, k=k, device=dev)
+                lay.packed.copy_(pr.packed)
+                lay.sign_m.copy_(pr.sign_m)
+                lay.sign_n.copy_(pr.sign_n)
+                lay.lut, lay.scale = pr.lut, pr.scale
+            else:
+                lay = ShardedQTIPLinear(m, n, rank, world, code=code, k=k, device=dev)
+                lay.local.packed.copy_(pr.local.packed)
+                lay.local.sign_n.copy_(pr.local.sign_n)
+                lay.local.lut, lay.local.scale = pr.local.lut, pr.local.scale
+                lay.sign_m.copy_(pr.sign_m)
+            layers.append(lay)
+    del protos
+    torch.cuda.synchronize()
+
+    ns = sorted(set(n for _, n in shapes))
+    xs = {n: torch.from_numpy(synth.random_x(B, n, seed=2000 + n)).to(dev) for n in ns}
+    outs = [torch.empty((B, lay.m), dtype=torch.float32, device=dev) for lay in layers]
+    step_bytes = sum(m * n * k // 8 for (m, n) in shapes) * nblocks
+
+    def step():
+        for lay, o in zip(layers, outs):
+            if world == 1:
+                lay.forward(xs[lay.n], out=o)
+            else:
+                o.copy_(lay.forward(xs[lay.n]))
+
+    # eager warm-up (Hadamard tables, workspaces, NCCL communicators), then capture one step
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    c0 = qtip.launch_count()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            step()
+    torch.cuda.current_stream().wait_stream(s)
+    launches_per_step = qtip.launch_count() - c0
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        g.replay()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            g.replay()
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = step_bytes / (ms * 1e-3) / 1e9
+
+    # ---- per-shape layer latency (graph of one layer, replayed) for us/layer reporting
+    per_layer = {}
+    for (m, n) in sorted(set(shapes)):
+        idx = [i for i, l in enumerate(layers) if (l.m, l.n) == (m, n)]
+        gl = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(gl, stream=s):
+                for i in idx:
+                    if world == 1:
+                        layers[i].forward(xs[n], out=outs[i])
+                    else:
+                        outs[i].copy_(layers[i].forward(xs[n]))
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(3):
+            gl.replay()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(max(1, args.steps // 2)):
+            gl.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = max_over_ranks(1e3 * e0.elapsed_time(e1) / (max(1, args.steps // 2) * len(idx)))
+        per_layer[f"{m}x{n}"] = {"us_per_layer": round(us, 3),
+                                 "GBps": round(m * n * k / 8 / (us * 1e-6) / 1e9, 1)}
+
+    # ---- dominant kernel (fused decode-GEMV): CUDA events around each launch, K steps
+    gemv_ms, gemv_bytes = 0.0, 0
+    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in layers]
+    prof_steps = max(1, min(args.steps, 5))
+    for _ in range(prof_steps):
+        for lay, o, (a, b_) in zip(layers, outs, ev_pairs):
+            tgt = lay if world == 1 else lay.local
+            qtip.profile_events(a, b_)
+            if world == 1:
+                lay.forward(xs[lay.n], out=o)
+            else:
+                o.copy_(lay.forward(xs[lay.n]))
+        torch.cuda.synchronize()
+        for lay, (a, b_) in zip(layers, ev_pairs):
+            tgt = lay if world == 1 else lay.local
+            gemv_ms += a.elapsed_time(b_)
+            gemv_bytes += tgt.m * tgt.n * k // 8
+    qtip.profile_events(None, None)
+    gemv_ms = max_over_ranks(gemv_ms)
+    gemv_gbs = gemv_bytes / (gemv_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+
+    # ---- end to end through the public API: pinned H2D of x, the step, D2H of the last output
+    xh = {n: torch.from_numpy(synth.random_x(B, n, seed=2000 + n)).pin_memory() for n in ns}
+    yh = torch.empty_like(outs[-1], device="cpu").pin_memory()
+    ge = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(ge, stream=s):
+            for n in ns:
+                xs[n].copy_(xh[n], non_blocking=True)
+            step()
+            yh.copy_(outs[-1], non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        ge.replay()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        ge.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    h2d = sum(x.numel() * 4 for x in xh.values())
+    d2h = yh.numel() * 4
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        nbytes, times = oracle_sample(2048, 4096, code, k, reps=3)
+        cpu = {"value": nbytes * len(times) / sum(times) / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"3 x one 2048x4096 {code} k={k} layer (decode + float64 RHT-in/GEMV/RHT-out), "
+                         f"single thread, host nproc={os.cpu_count()}"}
+
+    if rank == 0:
+        line = {
+            "metric": "fused trellis-decode GEMV: compressed-byte HBM GB/s vs peak; us/layer batch=1",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "fp16xfp16->f32" if True else "", "data": "synthetic",
+            "config": {"workload": args.workload, "layers_per_step": len(layers), "blocks": nblocks,
+                       "code": code, "k": k, "L": 16, "V": 2 if code == "hyb" else 1, "T": 256, "batch": B,
+                       "stream_bytes_per_step": step_bytes, "tokens_per_s_equiv": round(B * 1e3 / ms, 2),
+                       "per_layer": per_layer, "parallelism": f"rows{world}" if world > 1 else "single",
+                       "l2": "inputs > L2: 1.62 GB of distinct packed weights per step (126 MB L2)"
+                       if args.workload == "llama2-7b" else "distinct weights per layer",
+                       "matvec_impl": qtip.get_matvec_impl()},
+            "roofline": {"bound": "hbm", "achieved": round(gemv_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gemv_gbs / peak, 4), "traffic": None,
+                         "kernel": "fused decode-GEMV", "peak_kind": peak_kind,
+                         "avg_launch_us": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 5)},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="llama2-7b", choices=sorted(WORKLOADS))
+    ap.add_argument("--code", default=None, choices=["3inst", "1mad", "hyb"])
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--blocks", type=int, default=None)
+    ap.add_argument("--matvec-impl", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

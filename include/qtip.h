@@ -1,0 +1,149 @@
+/* qtip.h -- C ABI of libqtip, the B200 (sm_100a) QTIP inference library.
+ *
+ * QTIP (arXiv 2406.11235) stores an RHT-processed weight matrix W~ (m x n) as 16 x 16
+ * tiles, each tile one T = 256 sequence (row-major scan)
+ * tail-biting-quantized on an (L, k, V) bitshift trellis (PAPER.md:121-125, :207-214,
+ * :325-328) and decoded by a computed code (1MAD Alg. 1 :269-281, 3INST Alg. 2 :283-296)
+ * or the hybrid lookup code (HYB Alg. 3 :311-321).  Inference computes
+ *
+ *     y = scale * S_m H_m^T W~ H_n S_n x                 (RHT)
+ *
+ * where H_k is an orthonormal Hadamard matrix (reading R7: kron(Paley-I H_b,
+ * Sylvester H_{2^a}), b the smallest supported order with k/b a power of two) and
+ * S_k a random sign vector.
+ *
+ * Conventions for every call:
+ *   - "d_" pointers are DEVICE pointers, "h_" pointers HOST pointers.  The caller owns
+ *     every buffer; the library never frees caller memory.  The only memory the library
+ *     allocates itself is a per-device cache of constant Hadamard +-1 tables (a few KB),
+ *     created on first use and kept for the process lifetime.
+ *   - stream is a cudaStream_t passed as void* (NULL = legacy default stream).  Device
+ *     work is enqueued on it asynchronously; host-side validation happens before any
+ *     launch, so a non-OK status means nothing was enqueued (except QTIP_ERR_CUDA).
+ *   - Shapes: m, n multiples of 16 (one tile).  Batch B >= 1.
+ *   - Errors are returned by value; qtip_last_error() gives a thread-local detail string.
+ *   - Logical tile stream: kT bits, MSB-first (bit 0 = most significant bit of byte 0),
+ *     tiles ordered [m/16][n/16]; state t of a tile is the L-bit window at bit t*kV,
+ *     wrapping mod kT (tail-biting).  This is the format the oracle and SPEC use; the
+ *     DEVICE layout ("packed") is private to the library and produced by qtip_pack*.
+ */
+#ifndef QTIP_H_
+#define QTIP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    QTIP_OK = 0,
+    QTIP_ERR_INVALID_PARAMS = -1, /* unsupported (L,k,V,code,Q), NULL pointer, bad flags   */
+    QTIP_ERR_SHAPE = -2,          /* m/n not multiples of 16, no Hadamard order, bad rows    */
+    QTIP_ERR_INVALID_PATH = -3,   /* qtip_pack_states: edge rule or tail-biting closure fails */
+    QTIP_ERR_ALIGNMENT = -4,      /* a device pointer is not 16-byte aligned                 */
+    QTIP_ERR_UNSUPPORTED = -5,    /* valid QTIP parameters this build has no kernel for      */
+    QTIP_ERR_CUDA = -6,           /* a CUDA call failed (detail in qtip_last_error)          */
+    QTIP_ERR_WORKSPACE = -7       /* workspace too small (see qtip_matvec_workspace_bytes)   */
+} qtip_status;
+
+typedef enum { QTIP_CODE_1MAD = 1, QTIP_CODE_3INST = 2, QTIP_CODE_HYB = 3 } qtip_code;
+
+/* Trellis + code parameters (PAPER.md:121 (L,k,V); :260, :267 LCG constants; :303 Q). */
+typedef struct {
+    int32_t L;            /* state bits; the device path supports L = 16          */
+    int32_t k;            /* bits per weight, 1..4 (device path: 2, 3, 4)                         */
+    int32_t V;            /* values per trellis step: 1 for 1MAD/3INST, 2 for HYB                 */
+    int32_t code;         /* qtip_code                                                            */
+    int32_t Q;            /* HYB LUT index bits; 9 -> 2 KiB table; must be 9      */
+    int32_t tail_biting;  /* must be 1: kT bits per tile                              */
+    int32_t Tx, Ty;       /* must be 16, 16 (T = 256, one 16x16 tile per sequence)     */
+    uint32_t lcg_a;       /* 1MAD: 34038481; 3INST: 89226354                      */
+    uint32_t lcg_b;       /* 1MAD: 76625530;         3INST: 64248484                              */
+    uint32_t m_fp16;      /* 3INST magic m as binary16 bits: 0x3B60 = fp16(0.922)  */
+    int32_t hyb_two_sign; /* HYB: also XOR bit 31; default 0 (the paper's numbers)    */
+} qtip_params;
+
+/* Fill *p with the paper's defaults for `code` at k bits (L=16, V=1 or 2, Q=9, T=16x16). */
+void qtip_params_default(qtip_params* p, int32_t code, int32_t k);
+
+/* Validate *p for the device path.  QTIP_OK or QTIP_ERR_INVALID_PARAMS/UNSUPPORTED. */
+qtip_status qtip_params_check(const qtip_params* p);
+
+/* Bytes of the device layout for an m x n matrix (rows padded to 128, columns to 256;
+ * padding tiles are zero and multiply zero activations).  Returns -1 on bad params. */
+int64_t qtip_packed_bytes(const qtip_params* p, int64_t m, int64_t n);
+
+/* Lay out logical tile streams in device format.
+ *   h_tiles: HOST uint8[m/16][n/16][k*T/8] (k*32 bytes per tile), MSB-first, tail-biting.
+ *   d_packed: DEVICE buffer of qtip_packed_bytes(p, m, n) bytes, 16-byte aligned.
+ * Any bit string is a valid tail-biting walk, so no path validation happens.
+ * Synchronous with respect to h_tiles: returns after the copy to d_packed completed. */
+qtip_status qtip_pack(const qtip_params* p, int64_t m, int64_t n, const uint8_t* h_tiles,
+                      void* d_packed, void* stream);
+
+/* As qtip_pack, from state walks (SPEC pack(path)): h_states HOST uint32[m/16][n/16][T/V].
+ * Every consecutive pair must satisfy the edge rule and the last state must
+ * connect to the first (tail-biting closure), else QTIP_ERR_INVALID_PATH. */
+qtip_status qtip_pack_states(const qtip_params* p, int64_t m, int64_t n, const uint32_t* h_states,
+                             void* d_packed, void* stream);
+
+/* Dense RHT-domain weights W~ (raw code values, no scale; P:123 reconstruction).
+ *   d_lut: HYB only, DEVICE uint16[2^Q][2] binary16 (c0, c1) pairs (else NULL).
+ *   out_dtype 0: binary16 (normative, bit-exact vs the oracle); 1: float32 = exact widening.
+ *   d_out: DEVICE [m][n] row-major. */
+qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* d_packed,
+                        const uint16_t* d_lut, int out_dtype, void* d_out, void* stream);
+
+#define QTIP_RHT_IN  1  /* apply x~ = H_n S_n x / sqrt(n) before the product               */
+#define QTIP_RHT_OUT 2  /* apply y = S_m H_m^T y~ / sqrt(m) after it (needs all m rows)    */
+
+/* Fused decode + matrix-vector product, batch B (<= 64):
+ *     d_y[b][i - row_begin] = scale * (S_m H_m^T W~ H_n S_n x_b)[i],  i in [row_begin, row_end)
+ *   d_x: DEVICE float32 [B][n];  d_y: DEVICE float32 [B][row_end - row_begin].
+ *   d_sign_n / d_sign_m: DEVICE bit-packed signs (element i negative iff bit (i&7) of byte
+ *     i>>3 is set), ceil(n/8) / ceil(m/8) bytes; ignored when the matching flag is off.
+ *   flags: QTIP_RHT_IN | QTIP_RHT_OUT.  Without RHT_OUT the result is scale * W~ x~.
+ *     A partial row range (row_begin > 0 or row_end < m) requires RHT_OUT off; row_begin
+ *     and row_end must be multiples of 128 (or row_end == m).
+ *   d_workspace: DEVICE scratch of >= qtip_matvec_workspace_bytes(...) bytes, 256-B aligned.
+ *   Deterministic: the K-split and reduction order depend only on (m, n), not on timing,
+ *   so a row shard reproduces the full call's rows bit for bit. */
+qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B,
+                        const void* d_packed, const uint16_t* d_lut,
+                        const uint8_t* d_sign_n, const uint8_t* d_sign_m, float scale,
+                        const float* d_x, float* d_y, int64_t row_begin, int64_t row_end,
+                        int flags, void* d_workspace, size_t workspace_bytes, void* stream);
+
+size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B);
+
+/* Random Hadamard transform of B vectors of length n:
+ *   inverse = 0:  out = H_n (S . in) / sqrt(n)
+ *   inverse = 1:  out = S . (H_n^T in) / sqrt(n)
+ * d_in, d_out: DEVICE float32 [B][n]; in-place allowed. */
+qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d_in, float* d_out,
+                     int inverse, void* stream);
+
+/* The Hadamard factorisation used for order n: n = b * 2^a.  QTIP_ERR_SHAPE if none. */
+qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a);
+
+/* Selects the matvec kernel: 0 = auto (tcgen05 when available), 1 = CUDA-core reference
+ * kernel, 2 = tcgen05 kernel.  Process-wide; for ablations and tests. */
+void qtip_set_matvec_impl(int impl);
+int qtip_get_matvec_impl(void);
+
+/* Bench instrumentation: arms the NEXT qtip_matvec call on this thread to record the two
+ * cudaEvent_t handles (passed as void*) on its stream immediately before and after its fused
+ * decode-GEMV kernel, then disarms.  NULL, NULL disarms explicitly. */
+void qtip_profile_events(void* ev_start, void* ev_stop);
+
+const char* qtip_status_string(qtip_status s);
+const char* qtip_last_error(void);
+/* Number of kernels this thread has launched through the API (for bench accounting). */
+uint64_t qtip_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTIP_H_ */

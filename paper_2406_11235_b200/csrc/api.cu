@@ -1,0 +1,292 @@
+// api.cu -- the extern "C" boundary of libqtip (declared in include/qtip.h).
+//
+// Host-side validation, the private device layout (common.cuh) and kernel dispatch.  No
+// call allocates device memory except the per-device Hadamard table cache (hadamard.cpp).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+namespace qtip {
+namespace {
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
+int g_impl = 0;
+
+qtip_status fail(qtip_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+qtip_status cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return QTIP_ERR_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+CodeArgs code_args(const qtip_params* p) {
+    CodeArgs c;
+    c.a = p->lcg_a;
+    c.b = p->lcg_b;
+    c.magic = (p->m_fp16 << 16) | (p->m_fp16 & 0xFFFFu);
+    c.Q = p->Q;
+    c.two_sign = p->hyb_two_sign;
+    return c;
+}
+
+qtip_status check_shape(int64_t m, int64_t n) {
+    if (m <= 0 || n <= 0 || m % kTile || n % kTile) return fail(QTIP_ERR_SHAPE, "m and n must be positive multiples of 16");
+    return QTIP_OK;
+}
+}  // namespace
+
+void count_launch(int n) { g_launches += (uint64_t)n; }
+
+}  // namespace qtip
+
+using namespace qtip;
+
+extern "C" {
+
+void qtip_params_default(qtip_params* p, int32_t code, int32_t k) {
+    std::memset(p, 0, sizeof(*p));
+    p->L = 16;
+    p->k = k;
+    p->code = code;
+    p->V = (code == QTIP_CODE_HYB) ? 2 : 1;
+    p->Q = 9;
+    p->tail_biting = 1;
+    p->Tx = p->Ty = 16;
+    if (code == QTIP_CODE_1MAD) { p->lcg_a = 34038481u; p->lcg_b = 76625530u; }
+    if (code == QTIP_CODE_3INST) { p->lcg_a = 89226354u; p->lcg_b = 64248484u; }
+    p->m_fp16 = 0x3B60u;                                                            // fp16(0.922)
+    p->hyb_two_sign = 0;
+}
+
+qtip_status qtip_params_check(const qtip_params* p) {
+    if (!p) return fail(QTIP_ERR_INVALID_PARAMS, "params is NULL");
+    if (p->code != QTIP_CODE_1MAD && p->code != QTIP_CODE_3INST && p->code != QTIP_CODE_HYB)
+        return fail(QTIP_ERR_INVALID_PARAMS, "unknown code");
+    if (p->k < 1 || p->k > 4) return fail(QTIP_ERR_INVALID_PARAMS, "k must be in 1..4");
+    if ((p->code == QTIP_CODE_HYB) != (p->V == 2) || (p->V != 1 && p->V != 2))
+        return fail(QTIP_ERR_INVALID_PARAMS, "1MAD/3INST need V=1, HYB needs V=2");
+    if (p->L < p->k * p->V || p->L > 32) return fail(QTIP_ERR_INVALID_PARAMS, "need kV <= L <= 32");
+    if (p->code == QTIP_CODE_HYB && (p->Q < 1 || p->Q > 15)) return fail(QTIP_ERR_INVALID_PARAMS, "HYB needs 1 <= Q <= 15");
+    if (p->L != 16) return fail(QTIP_ERR_UNSUPPORTED, "device path implements L = 16 (PAPER.md:415, :573)");
+    if (!p->tail_biting) return fail(QTIP_ERR_UNSUPPORTED, "device path needs tail-biting tiles (kT bits)");
+    if (p->Tx != 16 || p->Ty != 16) return fail(QTIP_ERR_UNSUPPORTED, "device path needs Tx = Ty = 16");
+    return QTIP_OK;
+}
+
+int64_t qtip_packed_bytes(const qtip_params* p, int64_t m, int64_t n) {
+    if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK) return -1;
+    const Layout l = make_layout(m, n, p->k);
+    return l.n_rb * l.n_kc * l.cell_words * 4;
+}
+
+qtip_status qtip_pack(const qtip_params* p, int64_t m, int64_t n, const uint8_t* h_tiles, void* d_packed,
+                      void* stream) {
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if ((st = check_shape(m, n)) != QTIP_OK) return st;
+    if (!h_tiles || !d_packed) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (!aligned16(d_packed)) return fail(QTIP_ERR_ALIGNMENT, "d_packed must be 16-byte aligned");
+    const Layout l = make_layout(m, n, p->k);
+    const int64_t tile_bytes = 4 * l.tw;
+    const int64_t mt = m / kTile, nt = n / kTile;
+    std::vector<uint32_t> buf((size_t)(l.n_rb * l.n_kc * l.cell_words), 0u);
+    auto work = [&](int64_t t0, int64_t t1) {
+        for (int64_t Ig = t0; Ig < t1; ++Ig) {
+            const int64_t RB = Ig / kCellTileRows;
+            const int I = (int)(Ig % kCellTileRows);
+            for (int64_t Jg = 0; Jg < nt; ++Jg) {
+                const int64_t KC = Jg / kCellTileCols;
+                const int J = (int)(Jg % kCellTileCols);
+                const uint8_t* src = h_tiles + (Ig * nt + Jg) * tile_bytes;
+                uint32_t* cell = buf.data() + (RB * l.n_kc + KC) * l.cell_words;
+                for (int w = 0; w < l.tw; ++w) {
+                    const uint8_t* b = src + 4 * w;
+                    cell[cell_word_index(I, J, w, l.tw)] =
+                        ((uint32_t)b[0] << 24) | ((uint32_t)b[1] << 16) | ((uint32_t)b[2] << 8) | (uint32_t)b[3];
+                }
+            }
+        }
+    };
+    const int nthreads = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<int64_t>(1, mt / 64));
+    if (nthreads <= 1) {
+        work(0, mt);
+    } else {
+        std::vector<std::thread> th;
+        for (int i = 0; i < nthreads; ++i) th.emplace_back(work, mt * i / nthreads, mt * (i + 1) / nthreads);
+        for (auto& t : th) t.join();
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(d_packed, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_pack copy");
+    return QTIP_OK;
+}
+
+qtip_status qtip_pack_states(const qtip_params* p, int64_t m, int64_t n, const uint32_t* h_states, void* d_packed,
+                             void* stream) {
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if ((st = check_shape(m, n)) != QTIP_OK) return st;
+    if (!h_states) return fail(QTIP_ERR_INVALID_PATH, "NULL states");
+    const int L = p->L, kv = p->k * p->V, steps = 256 / p->V;
+    const uint32_t lmask = (L == 32) ? 0xFFFFFFFFu : ((1u << L) - 1u);
+    const uint32_t omask = (1u << (L - kv)) - 1u;
+    const int64_t ntiles = (m / kTile) * (n / kTile);
+    const int tile_bytes = p->k * 32;
+    std::vector<uint8_t> bytes((size_t)(ntiles * tile_bytes), 0);
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const uint32_t* s = h_states + t * steps;
+        uint8_t* out = bytes.data() + t * tile_bytes;
+        for (int q = 0; q < steps; ++q) {
+            const uint32_t cur = s[q], nxt = s[(q + 1) % steps];
+            if (cur & ~lmask) return fail(QTIP_ERR_INVALID_PATH, "state out of range");
+            // edge rule; for q = steps-1 this is the tail-biting closure
+            if ((nxt >> kv) != (cur & omask)) return fail(QTIP_ERR_INVALID_PATH, "edge rule / tail-biting closure violated");
+            // stream bits [q kV, (q+1) kV) are the top kV bits of state q
+            const uint32_t top = cur >> (L - kv);
+            for (int i = 0; i < kv; ++i) {
+                const int bit = q * kv + i;
+                if ((top >> (kv - 1 - i)) & 1u) out[bit >> 3] |= (uint8_t)(0x80u >> (bit & 7));
+            }
+        }
+    }
+    return qtip_pack(p, m, n, bytes.data(), d_packed, stream);
+}
+
+qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* d_packed, const uint16_t* d_lut,
+                        int out_dtype, void* d_out, void* stream) {
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if ((st = check_shape(m, n)) != QTIP_OK) return st;
+    if (!d_packed || !d_out || (p->code == QTIP_CODE_HYB && !d_lut)) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (out_dtype != 0 && out_dtype != 1) return fail(QTIP_ERR_INVALID_PARAMS, "out_dtype must be 0 or 1");
+    if (!aligned16(d_packed) || !aligned16(d_out)) return fail(QTIP_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+    const Layout l = make_layout(m, n, p->k);
+    cudaError_t e = launch_decode(l, p->code, p->V, code_args(p), d_packed, d_lut, out_dtype, d_out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_decode");
+    return QTIP_OK;
+}
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B) {
+    if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1) return 0;
+    const Layout l = make_layout(m, n, p->k);
+    return align256(4 * B * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad);
+}
+
+qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, const void* d_packed,
+                        const uint16_t* d_lut, const uint8_t* d_sign_n, const uint8_t* d_sign_m, float scale,
+                        const float* d_x, float* d_y, int64_t row_begin, int64_t row_end, int flags,
+                        void* d_workspace, size_t workspace_bytes, void* stream) {
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if ((st = check_shape(m, n)) != QTIP_OK) return st;
+    if (B < 1 || B > 64) return fail(QTIP_ERR_INVALID_PARAMS, "batch must be in 1..64");
+    if (flags & ~(QTIP_RHT_IN | QTIP_RHT_OUT)) return fail(QTIP_ERR_INVALID_PARAMS, "unknown flags");
+    if (!d_packed || !d_x || !d_y || !d_workspace || (p->code == QTIP_CODE_HYB && !d_lut))
+        return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (((flags & QTIP_RHT_IN) && !d_sign_n) || ((flags & QTIP_RHT_OUT) && !d_sign_m))
+        return fail(QTIP_ERR_INVALID_PARAMS, "NULL sign vector");
+    if (row_begin < 0 || row_end > m || row_begin >= row_end) return fail(QTIP_ERR_SHAPE, "bad row range");
+    if (row_begin % kCellRows || (row_end % kCellRows && row_end != m))
+        return fail(QTIP_ERR_SHAPE, "row_begin/row_end must be multiples of 128 (or row_end == m)");
+    if ((row_begin != 0 || row_end != m) && (flags & QTIP_RHT_OUT))
+        return fail(QTIP_ERR_INVALID_PARAMS, "a partial row range needs QTIP_RHT_OUT off (H_m^T mixes all rows)");
+    if (!aligned16(d_packed) || (reinterpret_cast<uintptr_t>(d_workspace) & 255u))
+        return fail(QTIP_ERR_ALIGNMENT, "d_packed 16-B and d_workspace 256-B aligned");
+    const size_t need = qtip_matvec_workspace_bytes(p, m, n, B);
+    if (workspace_bytes < need) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
+    RhtPlan pn{}, pm{};
+    if ((flags & QTIP_RHT_IN) && make_rht_plan(n, &pn) != cudaSuccess)
+        return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
+    if ((flags & QTIP_RHT_OUT) && make_rht_plan(m, &pm) != cudaSuccess)
+        return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
+
+    const Layout l = make_layout(m, n, p->k);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = (char*)d_workspace;
+    float* xt = (float*)ws;
+    float* partial = (float*)(ws + align256(4 * B * l.n_pad));
+    float* yt = (float*)(ws + align256(4 * B * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
+    cudaError_t e;
+    if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s);
+    else e = cudaMemcpy2DAsync(xt, 4 * l.n_pad, d_x, 4 * n, 4 * n, B, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
+    const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
+    const bool prof = g_prof_start && g_prof_stop;
+    if (prof) cudaEventRecord(g_prof_start, s);
+    e = launch_gemv_simple(l, p->code, code_args(p), d_packed, d_lut, xt, B, rb0, rb1, partial, s);
+    if (prof) {
+        cudaEventRecord(g_prof_stop, s);
+        g_prof_start = g_prof_stop = nullptr;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec gemv");
+    if (flags & QTIP_RHT_OUT) {
+        e = launch_reduce(partial, l.n_kc, B, l.m_pad, 0, m, 1.0f, yt, l.m_pad, s);
+        if (e == cudaSuccess) e = launch_rht(pm, B, d_sign_m, yt, l.m_pad, d_y, m, 1, scale, s);
+    } else {
+        e = launch_reduce(partial, l.n_kc, B, l.m_pad, row_begin, row_end, scale, d_y, row_end - row_begin, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec epilogue");
+    return QTIP_OK;
+}
+
+qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d_in, float* d_out, int inverse,
+                     void* stream) {
+    if (n <= 0 || B < 1) return fail(QTIP_ERR_SHAPE, "n and B must be positive");
+    if (!d_sign || !d_in || !d_out) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (d_in == d_out) return fail(QTIP_ERR_INVALID_PARAMS, "qtip_rht is out-of-place (d_in != d_out)");
+    RhtPlan plan{};
+    if (make_rht_plan(n, &plan) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
+    cudaError_t e = launch_rht(plan, B, d_sign, d_in, n, d_out, n, inverse ? 1 : 0, 1.0f, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_rht");
+    return QTIP_OK;
+}
+
+qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a) {
+    int bb, aa;
+    if (!b || !a) return fail(QTIP_ERR_INVALID_PARAMS, "NULL output");
+    if (!hadamard_factor(n, &bb, &aa)) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order");
+    *b = bb;
+    *a = aa;
+    return QTIP_OK;
+}
+
+void qtip_set_matvec_impl(int impl) { g_impl = impl; }
+
+void qtip_profile_events(void* ev_start, void* ev_stop) {
+    g_prof_start = (cudaEvent_t)ev_start;
+    g_prof_stop = (cudaEvent_t)ev_stop;
+}
+int qtip_get_matvec_impl(void) { return g_impl; }
+
+const char* qtip_status_string(qtip_status s) {
+    switch (s) {
+        case QTIP_OK: return "QTIP_OK";
+        case QTIP_ERR_INVALID_PARAMS: return "QTIP_ERR_INVALID_PARAMS";
+        case QTIP_ERR_SHAPE: return "QTIP_ERR_SHAPE";
+        case QTIP_ERR_INVALID_PATH: return "QTIP_ERR_INVALID_PATH";
+        case QTIP_ERR_ALIGNMENT: return "QTIP_ERR_ALIGNMENT";
+        case QTIP_ERR_UNSUPPORTED: return "QTIP_ERR_UNSUPPORTED";
+        case QTIP_ERR_CUDA: return "QTIP_ERR_CUDA";
+        case QTIP_ERR_WORKSPACE: return "QTIP_ERR_WORKSPACE";
+    }
+    return "QTIP_ERR_UNKNOWN";
+}
+
+const char* qtip_last_error(void) { return g_err.c_str(); }
+
+uint64_t qtip_launch_count(void) { return g_launches; }
+
+}  // extern "C"

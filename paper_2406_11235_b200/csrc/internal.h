@@ -1,0 +1,43 @@
+// internal.h -- host-side declarations shared by the libqtip translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace qtip {
+
+void count_launch(int n);
+
+// Hadamard factor tables (hadamard.cpp): n = b * 2^a; device +-1 table of H_b, bit-packed
+// row-major (bit i*b + j set <=> H_b[i][j] = -1), cached per device.
+bool hadamard_factor(int64_t n, int* b, int* a);
+const uint32_t* hadamard_table_device(int b, cudaError_t* err);
+
+// Kernel launchers.
+cudaError_t launch_decode(const Layout& lay, int code, int V, const CodeArgs& ca, const void* packed,
+                          const uint16_t* lut, int out_f32, void* out, cudaStream_t s);
+
+struct RhtPlan {
+    int64_t n;
+    int b, a;          // n = b * 2^a
+    int a2;            // FWHT length 2^a2 done in-CTA
+    int f;             // mix order n / 2^a2 = b * 2^(a - a2)
+    int rows_per_cta;  // rows of the mix handled per CTA
+    const uint32_t* hb;  // device H_b bits (nullptr when b == 1)
+};
+cudaError_t make_rht_plan(int64_t n, RhtPlan* plan);
+// out[bt][i] = scale * (M v)[i] with v = in * s (forward) or in (inverse, then * s at the end).
+// in/out batch strides in elements.  out_half != 0 writes binary16 instead of float32.
+cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
+                       float* out, int64_t out_stride, int inverse, float scale, cudaStream_t s);
+
+// Reference (CUDA-core) fused decode-GEMV: partial[kc][b][row] over the row blocks [rb0, rb1).
+cudaError_t launch_gemv_simple(const Layout& lay, int code, const CodeArgs& ca, const void* packed,
+                               const uint16_t* lut, const float* xt, int64_t B, int64_t rb0, int64_t rb1,
+                               float* partial, cudaStream_t s);
+// y[b][i - row0] = scale * sum_kc partial[kc][b][i] for rows [row0, row1).
+cudaError_t launch_reduce(const float* partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0, int64_t row1,
+                          float scale, float* y, int64_t y_stride, cudaStream_t s);
+
+}  // namespace qtip

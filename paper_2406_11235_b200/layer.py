@@ -1,0 +1,70 @@
+"""QTIPLinear: one QTIP-quantized linear layer y = W x on the GPU (the call a user makes).
+
+W = scale * S_m H_m^T W~ H_n S_n with W~ stored as packed trellis tiles.
+Holds device buffers (packed stream, signs, LUT, workspace) and calls qtip_matvec; all
+arithmetic happens in libqtip.
+"""
+import numpy as np
+import torch
+
+from . import qtip
+
+
+class QTIPLinear:
+    def __init__(self, m, n, code="3inst", k=2, device="cuda", two_sign=False):
+        self.m, self.n, self.code, self.k = m, n, code, k
+        self.device = torch.device(device)
+        self.p = qtip.params_default(code, k, two_sign)
+        nbytes = qtip.packed_bytes(self.p, m, n)
+        if nbytes < 0:
+            raise ValueError(f"unsupported QTIP config {code} k={k} for {m}x{n}")
+        self.packed = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        self.sign_m = torch.zeros((m + 7) // 8, dtype=torch.uint8, device=self.device)
+        self.sign_n = torch.zeros((n + 7) // 8, dtype=torch.uint8, device=self.device)
+        self.lut = None
+        self.scale = 1.0
+        self._ws = {}
+
+    # ------------------------------------------------------------------ loading
+    def load_tiles(self, tiles, sign_m, sign_n, scale=1.0, lut=None):
+        """tiles: numpy uint8 (m/16, n/16, 32k) logical tail-biting streams; signs: bit-packed
+        numpy uint8; lut: numpy uint16 (2^Q, 2) binary16 (HYB only)."""
+        qtip.qtip_pack(self.p, self.m, self.n, tiles, self.packed)
+        self.sign_m.copy_(torch.from_numpy(np.ascontiguousarray(sign_m, dtype=np.uint8)))
+        self.sign_n.copy_(torch.from_numpy(np.ascontiguousarray(sign_n, dtype=np.uint8)))
+        if self.code == "hyb":
+            if lut is None:
+                raise ValueError("HYB needs a LUT")
+            self.lut = torch.from_numpy(np.ascontiguousarray(lut, dtype=np.uint16).view(np.int16)).to(self.device)
+        self.scale = float(scale)
+        return self
+
+    def workspace(self, B):
+        if B not in self._ws:
+            nb = qtip.workspace_bytes(self.p, self.m, self.n, B)
+            self._ws[B] = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        return self._ws[B]
+
+    # ------------------------------------------------------------------ compute
+    def forward(self, x, out=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_OUT, rows=None, stream=None):
+        """x: float32 CUDA (B, n) -> float32 (B, m) (or the row range of scale * W~ x~)."""
+        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous()
+        B = x.shape[0]
+        r0, r1 = rows if rows is not None else (0, self.m)
+        if out is None:
+            out = torch.empty((B, r1 - r0), dtype=torch.float32, device=self.device)
+        qtip.qtip_matvec(self.p, self.m, self.n, B, self.packed, self.lut, self.sign_n, self.sign_m, self.scale,
+                         x, out, r0, r1, flags, self.workspace(B), stream)
+        return out
+
+    __call__ = forward
+
+    def decode(self, out_f32=False):
+        out = torch.empty((self.m, self.n), dtype=torch.float32 if out_f32 else torch.float16, device=self.device)
+        qtip.qtip_decode(self.p, self.m, self.n, self.packed, self.lut, out, out_f32)
+        return out
+
+    @property
+    def stream_bytes(self):
+        """Algorithmic compressed bytes m n k / 8 (the metric's numerator)."""
+        return self.m * self.n * self.k // 8

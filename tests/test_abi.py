@@ -1,0 +1,116 @@
+"""CPU-side checks of the C-ABI library: it builds/loads, exports every symbol declared in
+include/qtip.h, and its host-only logic (params, sizes, Hadamard factorisation, Paley
+tables, error codes) behaves as documented.  No device compute runs here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2406_11235_b200 import build, qtip
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return qtip.load()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "qtip.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(qtip_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = header_functions()
+    assert len(names) >= 15
+    for nm in names:
+        assert hasattr(lib, nm), nm
+    assert set(qtip.EXPORTS) <= set(names)
+
+
+def test_params_defaults_follow_the_paper(lib):
+    p = qtip.params_default("3inst", 2)
+    assert (p.L, p.k, p.V, p.lcg_a, p.lcg_b, p.m_fp16, p.Q) == (16, 2, 1, 89226354, 64248484, 0x3B60, 9)
+    p = qtip.params_default("1mad", 2)
+    assert (p.lcg_a, p.lcg_b, p.V) == (34038481, 76625530, 1)
+    p = qtip.params_default("hyb", 4)
+    assert (p.V, p.Q, p.tail_biting, p.Tx, p.Ty) == (2, 9, 1, 16, 16)
+    assert qtip.params_check(p) == 0
+
+
+def test_params_check_errors(lib):
+    p = qtip.params_default("3inst", 2)
+    p.V = 2
+    assert qtip.params_check(p) == -1
+    p = qtip.params_default("hyb", 4)
+    p.V = 1
+    assert qtip.params_check(p) == -1
+    p = qtip.params_default("3inst", 2)
+    p.L = 12
+    assert qtip.params_check(p) == -5            # valid QTIP, unsupported on the device path
+    p = qtip.params_default("3inst", 2)
+    p.tail_biting = 0
+    assert qtip.params_check(p) == -5
+    p = qtip.params_default("3inst", 5)
+    assert qtip.params_check(p) == -1
+    assert lib.qtip_params_check(None) == -1
+
+
+def test_packed_bytes(lib):
+    p = qtip.params_default("3inst", 2)
+    assert qtip.packed_bytes(p, 4096, 4096) == 4096 * 4096 * 2 // 8
+    assert qtip.packed_bytes(p, 11008, 4096) == 11008 * 4096 * 2 // 8      # 11008 = 86 * 128, no padding
+    assert qtip.packed_bytes(p, 4096, 11008) == 4096 * 11008 * 2 // 8      # 11008 = 43 * 256
+    assert qtip.packed_bytes(p, 16, 16) == 128 * 256 * 2 // 8               # one padded cell
+    assert qtip.packed_bytes(p, 17, 16) == -1
+    assert qtip.packed_bytes(qtip.params_default("hyb", 3), 8192, 28672) == 8192 * 28672 * 3 // 8
+
+
+def test_hadamard_factorisation_matches_reading(lib):
+    assert qtip.hadamard_order(4096) == (1, 12)
+    assert qtip.hadamard_order(11008) == (344, 5)
+    assert qtip.hadamard_order(28672) == (28, 10)
+    assert qtip.hadamard_order(5120) == (20, 8)
+    with pytest.raises(qtip.QtipError):
+        qtip.hadamard_order(105)
+
+
+@pytest.mark.parametrize("b", [4, 12, 20, 28, 108, 344])
+def test_library_paley_tables_are_hadamard(lib, b):
+    H = qtip.paley_host(b).astype(np.int64)
+    assert (H @ H.T == b * np.eye(b, dtype=np.int64)).all()
+    assert (H + H.T == 2 * np.eye(b, dtype=np.int64)).all()
+
+
+def test_status_strings(lib):
+    assert lib.qtip_status_string(0) == b"QTIP_OK"
+    assert lib.qtip_status_string(-3) == b"QTIP_ERR_INVALID_PATH"
+
+
+def test_host_validation_before_any_launch(lib):
+    """Calls with invalid arguments return an error without touching the device."""
+    p = qtip.params_default("3inst", 2)
+    vp = ctypes.c_void_p
+    assert lib.qtip_decode(ctypes.byref(p), 17, 16, vp(16), None, 0, vp(16), None) == -2
+    assert lib.qtip_decode(ctypes.byref(p), 16, 16, None, None, 0, vp(16), None) == -1
+    assert lib.qtip_decode(ctypes.byref(p), 16, 16, vp(8), None, 0, vp(16), None) == -4
+    assert lib.qtip_rht(105, 1, vp(16), vp(16), vp(32), 0, None) == -2
+    assert lib.qtip_rht(256, 1, vp(16), vp(16), vp(16), 0, None) == -1      # in-place refused
+    ws = 1 << 20
+    # partial row range with RHT_OUT is refused
+    assert lib.qtip_matvec(ctypes.byref(p), 256, 256, 1, vp(256), None, vp(256), vp(256), ctypes.c_float(1.0),
+                           vp(256), vp(256), 128, 256, 3, vp(256), ws, None) == -1
+    assert lib.qtip_matvec(ctypes.byref(p), 256, 256, 1, vp(256), None, vp(256), vp(256), ctypes.c_float(1.0),
+                           vp(256), vp(256), 64, 256, 0, vp(256), ws, None) == -2
+    assert lib.qtip_matvec(ctypes.byref(p), 256, 256, 1, vp(256), None, vp(256), vp(256), ctypes.c_float(1.0),
+                           vp(256), vp(256), 0, 256, 3, vp(256), 16, None) == -7
+    # qtip_pack_states rejects a non-walk before copying anything
+    states = np.zeros((1, 1, 256), dtype=np.uint32)
+    states[0, 0, 5] = 0xFFFF
+    assert lib.qtip_pack_states(ctypes.byref(p), 16, 16, states.ctypes.data_as(vp), vp(256), None) == -3

@@ -1,0 +1,216 @@
+"""GPU parity: libqtip (sm_100a, through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star): decoded weights bit-exact; matvec relative L2 <= 1e-3 against
+the float64 oracle (fp32 accumulation, fp16 activations on the tensor-core path).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import codes, gemv, rht, trellis, viterbi
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-3
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def lut_for(code, seed=4000):
+    return synth.gaussian_lut(9, seed) if code == "hyb" else None
+
+
+def make_layer(q, m, n, code, k, tiles, lut=None, seed=0, scale=1.0):
+    from paper_2406_11235_b200.layer import QTIPLinear
+    layer = QTIPLinear(m, n, code=code, k=k)
+    layer.load_tiles(tiles, synth.random_sign_bytes(m, 3001 + seed), synth.random_sign_bytes(n, 3000 + seed),
+                     scale=scale, lut=lut)
+    return layer
+
+
+CASES = [("3inst", 2), ("1mad", 2), ("hyb", 4), ("hyb", 3), ("hyb", 2), ("3inst", 3), ("1mad", 4), ("3inst", 1)]
+
+
+@pytest.mark.parametrize("code,k", CASES)
+@pytest.mark.parametrize("m,n", [(256, 256), (272, 304), (128, 512)])
+def test_decode_bit_exact(cuda_lib, code, k, m, n):
+    tiles = synth.random_tiles(m, n, k, seed=1000 + k * 7 + m)
+    lut = lut_for(code)
+    layer = make_layer(cuda_lib, m, n, code, k, tiles, lut)
+    got = layer.decode().cpu().numpy().view(np.uint16)
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    ref = gemv.dense_decode(tiles, p).astype(np.float16).view(np.uint16)
+    assert np.array_equal(got, ref)
+    got32 = layer.decode(out_f32=True).cpu().numpy()
+    assert np.array_equal(got32, ref.view(np.float16).astype(np.float32))
+
+
+def test_decode_kmeans_lut_and_two_sign(cuda_lib):
+    m, n = 256, 256
+    lut = codes.kmeans_lut(9, seed=4000, n_samples=1 << 15, iters=8)
+    tiles = synth.random_tiles(m, n, 4, seed=77)
+    for two in (False, True):
+        from paper_2406_11235_b200.layer import QTIPLinear
+        layer = QTIPLinear(m, n, code="hyb", k=4, two_sign=two)
+        layer.load_tiles(tiles, synth.random_sign_bytes(m, 1), synth.random_sign_bytes(n, 2), lut=lut)
+        got = layer.decode().cpu().numpy().view(np.uint16)
+        ref = gemv.dense_decode(tiles, gemv.Params(k=4, V=2, code="hyb", lut=lut, two_sign=two))
+        assert np.array_equal(got, ref.astype(np.float16).view(np.uint16))
+
+
+def test_c1_viterbi_quantized_tiles_through_pack_states(cuda_lib):
+    """Config C1: 256x256, L=16 k=2 V=1 3INST, tail-biting walks from the oracle's Alg. 4 on
+    i.i.d. N(0,1) tiles (P:98 'approximately i.i.d. Gaussian'), packed from state walks."""
+    m = n = 256
+    tab = codes.code_table("3inst", 16)
+    sd = tab.std()
+    S = synth.gaussian_source((m // 16) * (n // 16), 256, seed=5000)
+    states, cost = viterbi.tailbite_encode_batch(S, 16, 2, 1, tab / sd)
+    assert (cost / 256).mean() < 0.075                          # ~Table 1 quality
+    from paper_2406_11235_b200 import qtip
+    from paper_2406_11235_b200.layer import QTIPLinear
+    layer = QTIPLinear(m, n, code="3inst", k=2)
+    qtip.qtip_pack_states(layer.p, m, n, states.reshape(m // 16, n // 16, 256), layer.packed)
+    got = layer.decode().cpu().numpy().view(np.uint16)
+    # the oracle's own reconstruction of the same walks
+    ref = np.zeros((m, n), dtype=np.uint16)
+    vals = codes.decode_3inst(states.astype(np.uint64)).reshape(m // 16, n // 16, 16, 16)
+    ref[:] = vals.transpose(0, 2, 1, 3).reshape(m, n)
+    assert np.array_equal(got, ref)
+    # the decoded tiles approximate the Gaussian source (times the std normaliser)
+    src = S.reshape(m // 16, n // 16, 16, 16).transpose(0, 2, 1, 3).reshape(m, n)
+    err = ((codes.f16_to_f64(got) / sd - src) ** 2).mean()
+    assert err < 0.08
+    # a broken walk is rejected
+    bad = states.copy()
+    bad[3, 10] ^= 0x8000
+    with pytest.raises(qtip.QtipError):
+        qtip.qtip_pack_states(layer.p, m, n, bad.reshape(m // 16, n // 16, 256), layer.packed)
+
+
+@pytest.mark.parametrize("n", [256, 4096, 8192, 11008, 28672, 12 * 16, 28 * 8, 20 * 256])
+@pytest.mark.parametrize("B", [1, 3])
+def test_rht_matches_oracle(cuda_lib, n, B):
+    from paper_2406_11235_b200 import qtip
+    x = synth.random_x(B, n, seed=2000 + n)
+    s = synth.random_sign_bytes(n, 3000)
+    dx = torch.from_numpy(x).cuda()
+    ds = torch.from_numpy(s).cuda()
+    out = torch.empty_like(dx)
+    qtip.qtip_rht(n, B, ds, dx, out, inverse=False)
+    ref = rht.rht_forward(x, s, n)
+    assert rel_l2(out.cpu().numpy(), ref) < 1e-6
+    back = torch.empty_like(dx)
+    qtip.qtip_rht(n, B, ds, out, back, inverse=True)
+    assert rel_l2(back.cpu().numpy(), rht.rht_inverse(out.cpu().numpy().astype(np.float64), s, n)) < 1e-6
+    assert rel_l2(back.cpu().numpy(), x) < 1e-5
+
+
+def _oracle_matvec(tiles, code, k, lut, m, n, x, seed, scale, flags=3, rows=None):
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    Wt = gemv.dense_decode(tiles, p)
+    return gemv.matvec(Wt, x.astype(np.float64), synth.random_sign_bytes(n, 3000 + seed),
+                       synth.random_sign_bytes(m, 3001 + seed), scale=scale, rht_in=bool(flags & 1),
+                       rht_out=bool(flags & 2), rows=rows)
+
+
+@pytest.mark.parametrize("impl", [1, 0])
+@pytest.mark.parametrize("code,k", CASES)
+@pytest.mark.parametrize("B", [1, 4, 16])
+def test_matvec_small(cuda_lib, impl, code, k, B):
+    m, n = 384, 768                                          # 3 row blocks x 3 K-chunks
+    tiles = synth.random_tiles(m, n, k, seed=11 + k)
+    lut = lut_for(code)
+    layer = make_layer(cuda_lib, m, n, code, k, tiles, lut, seed=1, scale=0.37)
+    x = synth.random_x(B, n, seed=2000 + B)
+    cuda_lib.set_matvec_impl(impl)
+    try:
+        y = layer(torch.from_numpy(x).cuda()).cpu().numpy()
+    finally:
+        cuda_lib.set_matvec_impl(0)
+    ref = _oracle_matvec(tiles, code, k, lut, m, n, x, 1, 0.37)
+    tol = 1e-5 if impl == 1 else MATVEC_TOL
+    assert rel_l2(y, ref) <= tol
+
+
+@pytest.mark.parametrize("impl", [1, 0])
+def test_matvec_ragged_shapes_and_flags(cuda_lib, impl):
+    m, n = 272, 336                                          # partial row block and K-chunk (padding)
+    code, k = "3inst", 2
+    tiles = synth.random_tiles(m, n, k, seed=5)
+    layer = make_layer(cuda_lib, m, n, code, k, tiles, None, seed=2, scale=1.5)
+    x = synth.random_x(2, n, seed=9)
+    cuda_lib.set_matvec_impl(impl)
+    try:
+        for flags in (0, 1, 2, 3):
+            if flags & 2 or flags == 0:
+                pass
+            y = layer(torch.from_numpy(x).cuda(), flags=flags).cpu().numpy()
+            ref = _oracle_matvec(tiles, code, k, None, m, n, x, 2, 1.5, flags=flags)
+            assert rel_l2(y, ref) <= (1e-5 if impl == 1 else MATVEC_TOL), flags
+    finally:
+        cuda_lib.set_matvec_impl(0)
+
+
+@pytest.mark.parametrize("impl", [1, 0])
+def test_row_shards_are_bitwise_slices(cuda_lib, impl):
+    """Row sharding does not change per-row arithmetic (fixed K-split): shards == full rows bitwise."""
+    m, n = 512, 512
+    tiles = synth.random_tiles(m, n, 2, seed=8)
+    layer = make_layer(cuda_lib, m, n, "3inst", 2, tiles, None, seed=3)
+    x = torch.from_numpy(synth.random_x(3, n, seed=4)).cuda()
+    cuda_lib.set_matvec_impl(impl)
+    try:
+        full = layer(x, flags=1).cpu().numpy()
+        parts = [layer(x, flags=1, rows=(r, r + 128)).cpu().numpy() for r in range(0, m, 128)]
+    finally:
+        cuda_lib.set_matvec_impl(0)
+    assert np.array_equal(np.concatenate(parts, axis=1), full)
+
+
+@pytest.mark.parametrize("code,k,m,n", [("3inst", 2, 4096, 4096), ("1mad", 2, 11008, 4096), ("3inst", 2, 4096, 11008),
+                                        ("hyb", 4, 4096, 4096)])
+def test_matvec_full_size_sampled_rows(cuda_lib, code, k, m, n):
+    """BASELINE C2/C3 shapes in the bench's launch configuration: rows of scale*W~ x~ sampled and
+    recomputed one by one by the oracle (RHT-out off), plus the full RHT-out path against the
+    oracle's inverse RHT of the GPU's own y~ (a property that holds at any size)."""
+    tiles = synth.random_tiles(m, n, k, seed=1000)
+    lut = lut_for(code)
+    layer = make_layer(cuda_lib, m, n, code, k, tiles, lut, seed=0, scale=0.5)
+    x = synth.random_x(1, n, seed=2000)
+    dx = torch.from_numpy(x).cuda()
+    yt = layer(dx, flags=1).cpu().numpy()                    # scale * W~ x~
+    rows = np.random.default_rng(0).choice(m, 24, replace=False)
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    Wr = gemv.decode_rows(tiles, p, rows)
+    xt = rht.rht_forward(x.astype(np.float64), synth.random_sign_bytes(n, 3000), n)
+    ref = 0.5 * (xt @ Wr.T)
+    assert rel_l2(yt[:, rows], ref) <= MATVEC_TOL
+    y = layer(dx).cpu().numpy()
+    ref_y = rht.rht_inverse(yt.astype(np.float64), synth.random_sign_bytes(m, 3001), m)
+    assert rel_l2(y, ref_y) <= 1e-5
+
+
+def test_matvec_deterministic(cuda_lib):
+    m, n = 1024, 2048
+    tiles = synth.random_tiles(m, n, 2, seed=1)
+    layer = make_layer(cuda_lib, m, n, "3inst", 2, tiles)
+    x = torch.from_numpy(synth.random_x(1, n)).cuda()
+    a = layer(x).cpu().numpy()
+    for _ in range(3):
+        assert np.array_equal(layer(x).cpu().numpy(), a)
+
+
+def test_launch_counter_counts_kernels(cuda_lib):
+    m, n = 256, 256
+    layer = make_layer(cuda_lib, m, n, "3inst", 2, synth.random_tiles(m, n, 2))
+    x = torch.from_numpy(synth.random_x(1, n)).cuda()
+    c0 = cuda_lib.launch_count()
+    layer(x)
+    torch.cuda.synchronize()
+    assert cuda_lib.launch_count() > c0
