@@ -71,7 +71,7 @@ void qtip_params_default(qtip_params* p, int32_t code, int32_t k);
 /* Validate *p for the device path.  QTIP_OK or QTIP_ERR_INVALID_PARAMS/UNSUPPORTED. */
 qtip_status qtip_params_check(const qtip_params* p);
 
-/* Bytes of the device layout for an m x n matrix (rows padded to 128, columns to 256;
+/* Bytes of the device layout for an m x n matrix (rows and columns padded to 128;
  * padding tiles are zero and multiply zero activations).  Returns -1 on bad params. */
 int64_t qtip_packed_bytes(const qtip_params* p, int64_t m, int64_t n);
 

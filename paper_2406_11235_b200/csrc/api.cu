@@ -214,19 +214,29 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
 
     const Layout l = make_layout(m, n, p->k);
+    const CodeArgs ca = code_args(p);
+    const bool tc_ok = gemv_tc_supported(l, p->code, ca, B);
+    if (g_impl == 2 && !tc_ok) return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 kernel: needs 2 <= k <= 4, B <= 16, HYB Q = 9 one-sign");
+    const bool use_tc = tc_ok && g_impl != 1;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
-    float* xt = (float*)ws;
+    void* xt = ws;
     float* partial = (float*)(ws + align256(4 * B * l.n_pad));
     float* yt = (float*)(ws + align256(4 * B * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
+    const int xmode = use_tc ? gemv_tc_xt_mode(p->code) : 0;
     cudaError_t e;
-    if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s);
-    else e = cudaMemcpy2DAsync(xt, 4 * l.n_pad, d_x, 4 * n, 4 * n, B, cudaMemcpyDeviceToDevice, s);
+    if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad);
+    else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
     const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
     const bool prof = g_prof_start && g_prof_stop;
     if (prof) cudaEventRecord(g_prof_start, s);
-    e = launch_gemv_simple(l, p->code, code_args(p), d_packed, d_lut, xt, B, rb0, rb1, partial, s);
+    if (use_tc) {
+        const int64_t row_bytes = l.n_pad * (xmode == 1 ? 4 : 2);
+        e = launch_gemv_tc(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s);
+    } else {
+        e = launch_gemv_simple(l, p->code, ca, d_packed, d_lut, (const float*)xt, B, rb0, rb1, partial, s);
+    }
     if (prof) {
         cudaEventRecord(g_prof_stop, s);
         g_prof_start = g_prof_stop = nullptr;

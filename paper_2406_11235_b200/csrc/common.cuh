@@ -4,13 +4,14 @@
 //   * tile (16 x 16 weights, one T = 256 trellis sequence) = TW = 8k
 //     32-bit words; word w holds logical stream bits [32w, 32w+32) MSB-first, so bit 31
 //     of word w is stream bit 32w.
-//   * cell = 8 tile-rows x 16 tile-columns (128 output rows x 256 input columns).  Cells
-//     are stored row-block major: cell (RB, KC) at word (RB * NKC + KC) * CELL_WORDS.
+//   * cell = 8 tile-rows x 8 tile-columns (128 output rows x 128 input columns), the unit
+//     of work of the GEMV kernels and one contiguous 2048k-byte block (one bulk copy).
+//     Cells are stored row-block major: cell (RB, KC) at word (RB * NKC + KC) * CELL_WORDS.
 //   * inside a cell the two tiles of a column pair (J = 2p, 2p+1) are word-interleaved:
-//       word(I, J, w) = ((I * 8 + J/2) * TW + w) * 2 + (J & 1)
+//       word(I, J, w) = ((I * 4 + J/2) * TW + w) * 2 + (J & 1)
 //     so the thread that owns output row r of both tiles fetches (tile 2p, tile 2p+1) word
 //     w with one 64-bit load.
-//   * rows are padded to a multiple of 128 and columns to 256 with zero tiles; the padded
+//   * rows and columns are padded to multiples of 128 with zero tiles; the padded
 //     activations are zero, so padding never changes a result.
 #pragma once
 #include <cstdint>
@@ -23,13 +24,13 @@ namespace qtip {
 
 constexpr int kTile = 16;
 constexpr int kCellTileRows = 8;
-constexpr int kCellTileCols = 16;
+constexpr int kCellTileCols = 8;
 constexpr int kCellRows = kTile * kCellTileRows;   // 128
-constexpr int kCellCols = kTile * kCellTileCols;   // 256
+constexpr int kCellCols = kTile * kCellTileCols;   // 128
 
 struct Layout {
     int64_t m, n;          // logical shape
-    int64_t m_pad, n_pad;  // padded to 128 / 256
+    int64_t m_pad, n_pad;  // padded to 128
     int64_t n_rb, n_kc;    // cells along rows / columns
     int k;
     int tw;                // words per tile = 8k
@@ -49,7 +50,7 @@ inline Layout make_layout(int64_t m, int64_t n, int k) {
 }
 
 __host__ __device__ inline int64_t cell_word_index(int I, int J, int w, int tw) {
-    return ((int64_t)(I * 8 + (J >> 1)) * tw + w) * 2 + (J & 1);
+    return ((int64_t)(I * 4 + (J >> 1)) * tw + w) * 2 + (J & 1);
 }
 
 // Code parameters as the kernels see them.

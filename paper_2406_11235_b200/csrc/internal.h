@@ -27,15 +27,27 @@ struct RhtPlan {
     const uint32_t* hb;  // device H_b bits (nullptr when b == 1)
 };
 cudaError_t make_rht_plan(int64_t n, RhtPlan* plan);
-// out[bt][i] = scale * (M v)[i] with v = in * s (forward) or in (inverse, then * s at the end).
-// in/out batch strides in elements.  out_half != 0 writes binary16 instead of float32.
+// out[bt][i] = scale * (M v)[i] / sqrt(n) with v = in * s (forward) or in (inverse, then * s).
+// in/out batch strides in elements.  out_mode 0 float32, 1 binary16 duplicated per 32-bit word,
+// 2 binary16; elements [n, pad_to) of every output row are written as zero.
 cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
-                       float* out, int64_t out_stride, int inverse, float scale, cudaStream_t s);
+                       void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode = 0,
+                       int64_t pad_to = 0);
+// x (float32) -> out_mode encoding, zero padded to pad_to (used when RHT-in is off).
+cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
+                           int out_mode, int64_t pad_to, cudaStream_t s);
 
 // Reference (CUDA-core) fused decode-GEMV: partial[kc][b][row] over the row blocks [rb0, rb1).
 cudaError_t launch_gemv_simple(const Layout& lay, int code, const CodeArgs& ca, const void* packed,
                                const uint16_t* lut, const float* xt, int64_t B, int64_t rb0, int64_t rb1,
                                float* partial, cudaStream_t s);
+// tcgen05 fused decode-GEMM (k_gemv_tc.cu); x~ in the compact binary16 encoding of
+// gemv_tc_xt_mode(code) with row stride xt_row_bytes.
+bool gemv_tc_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B);
+int gemv_tc_xt_mode(int code);
+cudaError_t launch_gemv_tc(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
+                           const void* xt_compact, int64_t xt_row_bytes, int64_t B, int64_t rb0, int64_t rb1,
+                           float* partial, cudaStream_t s);
 // y[b][i - row0] = scale * sum_kc partial[kc][b][i] for rows [row0, row1).
 cudaError_t launch_reduce(const float* partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0, int64_t row1,
                           float scale, float* y, int64_t y_stride, cudaStream_t s);

@@ -1,6 +1,6 @@
 // k_gemv_simple.cu -- reference CUDA-core fused decode + GEMV (impl 1) and the split-K reduce.
 //
-// One CTA per (row block of 128, K-chunk of 256 columns), one thread per output row; the
+// One CTA per (row block of 128, K-chunk of 128 columns), one thread per output row; the
 // thread decodes its row of each tile (decode.cuh, bit-identical to qtip_decode) and
 // accumulates fp16-exact weights times fp32 x~ with FFMA.  Partial sums per K-chunk go to
 // the workspace and are summed in fixed chunk order (deterministic, shard-invariant).
@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(128) gemv_simple_kernel(const uint32_t* __rest
                                                           const uint16_t* __restrict__ lut,
                                                           const float* __restrict__ xt, int B, int64_t rb0,
                                                           float* __restrict__ partial) {
-    extern __shared__ float xs[];                 // [B][256] slice of x~ for this K-chunk
+    extern __shared__ float xs[];                 // [B][128] slice of x~ for this K-chunk
     const int KC = blockIdx.x;
     const int64_t RB = rb0 + blockIdx.y;
     const int t = threadIdx.x, I = t >> 4, r = t & 15;

@@ -6,6 +6,7 @@
 // j-th length-2^a2 slice of the signed input) and then runs an in-shared-memory fast
 // Walsh-Hadamard transform of length 2^a2 on each u_i.  No CTA repeats another's work, and
 // every CTA reads the whole (L2-resident) input once.
+#include <algorithm>
 #include <cmath>
 
 #include "internal.h"
@@ -15,14 +16,26 @@ namespace qtip {
 constexpr int kRhtThreads = 256;
 constexpr int kRhtMaxElems = 4096;   // rows_per_cta * 2^a2 held in shared memory
 
+// out_mode 0: float32; 1: binary16 duplicated into both halves of a 32-bit word (the K-doubled
+// UMMA B operand); 2: binary16.
+__device__ __forceinline__ void store_out(void* out, int mode, int64_t idx, float v) {
+    if (mode == 0) {
+        static_cast<float*>(out)[idx] = v;
+    } else {
+        const uint32_t h = __half_as_ushort(__float2half_rn(v));
+        if (mode == 1) static_cast<uint32_t*>(out)[idx] = h | (h << 16);
+        else static_cast<uint16_t*>(out)[idx] = (uint16_t)h;
+    }
+}
+
 __device__ __forceinline__ float sign_of(const uint8_t* __restrict__ s, int64_t i) {
     return ((s[i >> 3] >> (i & 7)) & 1) ? -1.0f : 1.0f;
 }
 
 __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const uint8_t* __restrict__ sign,
                                                            const float* __restrict__ in, int64_t in_stride,
-                                                           float* __restrict__ out, int64_t out_stride, int inverse,
-                                                           float out_scale) {
+                                                           void* __restrict__ out, int64_t out_stride, int inverse,
+                                                           float out_scale, int out_mode, int64_t pad_to) {
     __shared__ float buf[kRhtMaxElems];
     __shared__ float part[kRhtThreads];
     const int L2 = 1 << plan.a2;
@@ -30,7 +43,6 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const ui
     const int i0 = blockIdx.x * R;
     const int64_t bt = blockIdx.y;
     const float* x = in + bt * in_stride;
-    float* y = out + bt * out_stride;
     const int a1 = plan.a - plan.a2;
     const int n1 = 1 << a1;
     const int outputs = R * L2;
@@ -86,8 +98,17 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const ui
         const int64_t e = (int64_t)i * L2 + (o % L2);
         float v = buf[o] * out_scale;
         if (inverse) v *= sign_of(sign, e);
-        y[e] = v;
+        store_out(out, out_mode, bt * out_stride + e, v);
     }
+    if (blockIdx.x == 0)                                  // zero the padded tail [n, pad_to)
+        for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt * out_stride + e, 0.0f);
+}
+
+__global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t in_stride, void* __restrict__ out,
+                               int64_t out_stride, int out_mode, int64_t pad_to) {
+    const int64_t bt = blockIdx.y;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pad_to; e += (int64_t)gridDim.x * blockDim.x)
+        store_out(out, out_mode, bt * out_stride + e, e < n ? in[bt * in_stride + e] : 0.0f);
 }
 
 cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
@@ -113,10 +134,20 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
 }
 
 cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
-                       float* out, int64_t out_stride, int inverse, float scale, cudaStream_t s) {
+                       void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode,
+                       int64_t pad_to) {
     dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B);
     const float out_scale = (float)(scale / std::sqrt((double)plan.n));
-    rht_kernel<<<grid, kRhtThreads, 0, s>>>(plan, sign, in, in_stride, out, out_stride, inverse, out_scale);
+    rht_kernel<<<grid, kRhtThreads, 0, s>>>(plan, sign, in, in_stride, out, out_stride, inverse, out_scale, out_mode,
+                                            pad_to < plan.n ? plan.n : pad_to);
+    count_launch(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
+                           int out_mode, int64_t pad_to, cudaStream_t s) {
+    dim3 grid((unsigned)std::min<int64_t>((pad_to + 255) / 256, 1024), (unsigned)B);
+    convert_kernel<<<grid, 256, 0, s>>>(in, n, in_stride, out, out_stride, out_mode, pad_to);
     count_launch(1);
     return cudaGetLastError();
 }

@@ -66,8 +66,8 @@ def test_packed_bytes(lib):
     p = qtip.params_default("3inst", 2)
     assert qtip.packed_bytes(p, 4096, 4096) == 4096 * 4096 * 2 // 8
     assert qtip.packed_bytes(p, 11008, 4096) == 11008 * 4096 * 2 // 8      # 11008 = 86 * 128, no padding
-    assert qtip.packed_bytes(p, 4096, 11008) == 4096 * 11008 * 2 // 8      # 11008 = 43 * 256
-    assert qtip.packed_bytes(p, 16, 16) == 128 * 256 * 2 // 8               # one padded cell
+    assert qtip.packed_bytes(p, 4096, 11008) == 4096 * 11008 * 2 // 8      # 11008 = 86 * 128
+    assert qtip.packed_bytes(p, 16, 16) == 128 * 128 * 2 // 8               # one padded cell
     assert qtip.packed_bytes(p, 17, 16) == -1
     assert qtip.packed_bytes(qtip.params_default("hyb", 3), 8192, 28672) == 8192 * 28672 * 3 // 8
 
