@@ -128,8 +128,9 @@ qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d
 /* The Hadamard factorisation used for order n: n = b * 2^a.  QTIP_ERR_SHAPE if none. */
 qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a);
 
-/* Selects the matvec kernel: 0 = auto (tcgen05 when available), 1 = CUDA-core reference
- * kernel, 2 = tcgen05 kernel.  Process-wide; for ablations and tests. */
+/* Selects the matvec kernel: 0 = auto (the measured-fastest supported kernel), 1 = CUDA-core
+ * reference kernel, 2 = tcgen05 kernel (A in TMEM), 3 = register-fed mma.sync kernel.
+ * Process-wide; for ablations and tests. */
 void qtip_set_matvec_impl(int impl);
 int qtip_get_matvec_impl(void);
 
@@ -137,6 +138,10 @@ int qtip_get_matvec_impl(void);
  * cudaEvent_t handles (passed as void*) on its stream immediately before and after its fused
  * decode-GEMV kernel, then disarms.  NULL, NULL disarms explicitly. */
 void qtip_profile_events(void* ev_start, void* ev_stop);
+
+/* Programmatic dependent launch between the library's kernels (default on).  Off isolates
+ * each kernel's duration for measurement. */
+void qtip_set_pdl(int enable);
 
 const char* qtip_status_string(qtip_status s);
 const char* qtip_last_error(void);

@@ -5,7 +5,9 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 #include "internal.h"
@@ -46,6 +48,23 @@ qtip_status check_shape(int64_t m, int64_t n) {
 }  // namespace
 
 void count_launch(int n) { g_launches += (uint64_t)n; }
+
+bool g_pdl = true;
+bool pdl_enabled() { return g_pdl; }
+
+void prefer_max_smem(const void* kern) {
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert(kern).second)
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+
+int num_sms() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
 
 }  // namespace qtip
 
@@ -215,15 +234,21 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
 
     const Layout l = make_layout(m, n, p->k);
     const CodeArgs ca = code_args(p);
+    // kernel choice: 1 CUDA-core reference, 2 tcgen05 (A in TMEM), 3 register-fed mma.sync;
+    // auto picks the measured-fastest supported one
     const bool tc_ok = gemv_tc_supported(l, p->code, ca, B);
+    const bool mma_ok = gemv_mma_supported(l, p->code, ca, B);
     if (g_impl == 2 && !tc_ok) return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 kernel: needs 2 <= k <= 4, B <= 16, HYB Q = 9 one-sign");
-    const bool use_tc = tc_ok && g_impl != 1;
+    if (g_impl == 3 && !mma_ok) return fail(QTIP_ERR_UNSUPPORTED, "mma kernel: needs 2 <= k <= 4, B <= 16, one-sign HYB");
+    int impl = g_impl;
+    if (impl == 0) impl = mma_ok ? 3 : (tc_ok ? 2 : 1);
+    const bool use_tc = impl == 2, use_mma = impl == 3;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
     void* xt = ws;
     float* partial = (float*)(ws + align256(4 * B * l.n_pad));
     float* yt = (float*)(ws + align256(4 * B * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
-    const int xmode = use_tc ? gemv_tc_xt_mode(p->code) : 0;
+    const int xmode = (use_tc || use_mma) ? gemv_tc_xt_mode(p->code) : 0;
     cudaError_t e;
     if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad);
     else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s);
@@ -231,9 +256,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
     const bool prof = g_prof_start && g_prof_stop;
     if (prof) cudaEventRecord(g_prof_start, s);
-    if (use_tc) {
+    if (use_tc || use_mma) {
         const int64_t row_bytes = l.n_pad * (xmode == 1 ? 4 : 2);
-        e = launch_gemv_tc(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s);
+        e = use_tc ? launch_gemv_tc(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s)
+                   : launch_gemv_mma(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s);
     } else {
         e = launch_gemv_simple(l, p->code, ca, d_packed, d_lut, (const float*)xt, B, rb0, rb1, partial, s);
     }
@@ -274,6 +300,8 @@ qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a) {
 }
 
 void qtip_set_matvec_impl(int impl) { g_impl = impl; }
+
+void qtip_set_pdl(int enable) { g_pdl = enable != 0; }
 
 void qtip_profile_events(void* ev_start, void* ev_stop) {
     g_prof_start = (cudaEvent_t)ev_start;

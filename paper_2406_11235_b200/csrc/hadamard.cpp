@@ -110,23 +110,28 @@ bool hadamard_factor(int64_t n, int* b, int* a) {
     return false;
 }
 
-const uint32_t* hadamard_table_device(int b, cudaError_t* err) {
+const uint32_t* hadamard_table_device(int b, bool transpose, cudaError_t* err) {
     int dev = 0;
     *err = cudaGetDevice(&dev);
     if (*err != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_tables.find({dev, b});
+    const int key = transpose ? -b : b;
+    auto it = g_tables.find({dev, key});
     if (it != g_tables.end()) return it->second;
     const std::vector<int8_t> H = paley(b);
-    std::vector<uint32_t> bits(((size_t)b * b + 31) / 32, 0u);
-    for (size_t e = 0; e < H.size(); ++e)
-        if (H[e] < 0) bits[e >> 5] |= 1u << (e & 31);
+    const int wpr = (b + 31) / 32;                                  // words per bit row
+    std::vector<uint32_t> bits((size_t)b * wpr, 0u);
+    for (int i = 0; i < b; ++i)
+        for (int j = 0; j < b; ++j) {
+            const int8_t h = transpose ? H[(size_t)j * b + i] : H[(size_t)i * b + j];
+            if (h < 0) bits[(size_t)i * wpr + (j >> 5)] |= 1u << (j & 31);
+        }
     uint32_t* d = nullptr;
     *err = cudaMalloc(&d, bits.size() * sizeof(uint32_t));
     if (*err != cudaSuccess) return nullptr;
     *err = cudaMemcpy(d, bits.data(), bits.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
     if (*err != cudaSuccess) { cudaFree(d); return nullptr; }
-    g_tables[{dev, b}] = d;
+    g_tables[{dev, key}] = d;
     return d;
 }
 

@@ -8,11 +8,35 @@
 namespace qtip {
 
 void count_launch(int n);
+int num_sms();
 
-// Hadamard factor tables (hadamard.cpp): n = b * 2^a; device +-1 table of H_b, bit-packed
-// row-major (bit i*b + j set <=> H_b[i][j] = -1), cached per device.
+// Launch with programmatic dependent launch enabled (the kernel may start while its predecessor
+// on the stream drains; it must griddepcontrol.wait before reading the predecessor's output).
+// Every libqtip kernel asks for the maximum shared-memory carve-out, so consecutive kernels never
+// force an SM re-partition of L1/shared memory between launches.
+void prefer_max_smem(const void* kern);
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    prefer_max_smem((const void*)kern);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// Hadamard factor tables (hadamard.cpp): n = b * 2^a; device +-1 table of H_b (or H_b^T), one
+// bit row per matrix row padded to 32-bit words (bit j of row i set <=> entry = -1), cached per device.
 bool hadamard_factor(int64_t n, int* b, int* a);
-const uint32_t* hadamard_table_device(int b, cudaError_t* err);
+const uint32_t* hadamard_table_device(int b, bool transpose, cudaError_t* err);
 
 // Kernel launchers.
 cudaError_t launch_decode(const Layout& lay, int code, int V, const CodeArgs& ca, const void* packed,
@@ -24,7 +48,8 @@ struct RhtPlan {
     int a2;            // FWHT length 2^a2 done in-CTA
     int f;             // mix order n / 2^a2 = b * 2^(a - a2)
     int rows_per_cta;  // rows of the mix handled per CTA
-    const uint32_t* hb;  // device H_b bits (nullptr when b == 1)
+    const uint32_t* hb;   // device H_b bit rows (nullptr when b == 1)
+    const uint32_t* hbt;  // device H_b^T bit rows (inverse transform)
 };
 cudaError_t make_rht_plan(int64_t n, RhtPlan* plan);
 // out[bt][i] = scale * (M v)[i] / sqrt(n) with v = in * s (forward) or in (inverse, then * s).
@@ -48,6 +73,11 @@ int gemv_tc_xt_mode(int code);
 cudaError_t launch_gemv_tc(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
                            const void* xt_compact, int64_t xt_row_bytes, int64_t B, int64_t rb0, int64_t rb1,
                            float* partial, cudaStream_t s);
+// Register-fed mma.sync fused decode-GEMV (k_gemv_mma.cu); same x~ encoding as the tcgen05 kernel.
+bool gemv_mma_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B);
+cudaError_t launch_gemv_mma(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
+                            const void* xt_compact, int64_t xt_row_bytes, int64_t B, int64_t rb0, int64_t rb1,
+                            float* partial, cudaStream_t s);
 // y[b][i - row0] = scale * sum_kc partial[kc][b][i] for rows [row0, row1).
 cudaError_t launch_reduce(const float* partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0, int64_t row1,
                           float scale, float* y, int64_t y_stride, cudaStream_t s);

@@ -88,6 +88,7 @@ static void launch_simple_t(const Layout& lay, const CodeArgs& ca, const void* p
     const size_t smem = (size_t)B * kCellCols * sizeof(float);
     auto kern = gemv_simple_kernel<K, V, CODE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    prefer_max_smem((const void*)kern);
     dim3 grid((unsigned)lay.n_kc, (unsigned)(rb1 - rb0));
     kern<<<grid, 128, smem, s>>>((const uint32_t*)packed, lay, ca, lut, xt, (int)B, rb0, partial);
 }
@@ -109,25 +110,6 @@ cudaError_t launch_gemv_simple(const Layout& lay, int code, const CodeArgs& ca, 
         default: return cudaErrorInvalidValue;
     }
 #undef QTIP_SIMPLE_CASE
-    count_launch(1);
-    return cudaGetLastError();
-}
-
-__global__ void reduce_kernel(const float* __restrict__ partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0,
-                              int64_t row1, float scale, float* __restrict__ y, int64_t y_stride) {
-    const int64_t rows = row1 - row0;
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= rows * B) return;
-    const int64_t b = e / rows, i = row0 + e % rows;
-    float s = 0.0f;
-    for (int64_t kc = 0; kc < n_kc; ++kc) s += partial[(kc * B + b) * m_pad + i];
-    y[b * y_stride + (i - row0)] = scale * s;
-}
-
-cudaError_t launch_reduce(const float* partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0, int64_t row1,
-                          float scale, float* y, int64_t y_stride, cudaStream_t s) {
-    const int64_t total = (row1 - row0) * B;
-    reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(partial, n_kc, B, m_pad, row0, row1, scale, y, y_stride);
     count_launch(1);
     return cudaGetLastError();
 }

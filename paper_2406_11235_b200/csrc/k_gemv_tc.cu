@@ -2,17 +2,26 @@
 //
 // Work unit = one 128 x 128 cell (8 x 8 tiles, PAPER.md:389-390 T_x = T_y = 16).  A persistent
 // CTA per SM owns a contiguous range of cells and runs four independent row-block pipelines
-// ("groups") that share one TMA producer warp and one MMA-issuing warp:
+// ("groups") that share one TMA producer warp:
 //
 //   warp 0      producer: cp.async.bulk of each cell's packed stream (2048k bytes) into an
-//               8-slot shared-memory ring (mbarrier complete_tx).
-//   warp 1      allocates 512 TMEM columns; one lane issues tcgen05.mma (kind::f16, M=128,
-//               N=16, K=16, A from TMEM, B from shared memory) and tcgen05.commit.
-//   warps 2-17  decoders, 4 groups x 4 warps.  Thread (quadrant q, lane l) owns output row
+//               8-slot shared-memory ring (mbarrier complete_tx).  The weights do not depend
+//               on the previous kernel, so it starts before griddepcontrol.wait (PDL).
+//   warps 1-16  decoders, 4 groups x 4 warps.  Thread (quadrant q, lane l) owns output row
 //               R = 32q + l of its group's cell: it reads the row's words of two tiles with
 //               64/128-bit LDS, extracts the 16 contiguous trellis windows of each tile row
 //               (PAPER.md:208-212), evaluates the code (1MAD/3INST/HYB, Alg. 1-3) and stores
 //               the A operand straight into its own TMEM lane with tcgen05.st.
+//               Hand-off: every thread arrives on the group's `afull` mbarrier and moves on.
+//   warps 17-20 one UMMA issuer per group: waits on the group's hand-off, one elected lane
+//               issues the tcgen05.mma (kind::f16, M=128, N=16, K=16, A from TMEM, B from
+//               shared memory) and tcgen05.commit.  Measured: a single MMA warp serving all four
+//               groups serialises them (~1000 cycles per hand-off); per-group issuers do not.
+//
+// Per group: A triple-buffered (2 tiles per hand-off), D and the
+// B operand double-buffered so the epilogue of cell j drains while cell j+1 decodes; x~ for the
+// next cell is prefetched into registers.  TMEM columns of group g: D0 128g, D1 128g+16,
+// A_b 128g+32+32b (b < 3).  Within a group the MMA order is fixed, so sums are deterministic.
 //
 // A-operand encodings (one 32-bit TMEM column = two K elements):
 //   3INST  the masked/XORed LCG word (m1, m2) itself; B holds x~ duplicated, so the MMA forms
@@ -21,21 +30,46 @@
 //          MMA forms (s - 510) x exactly; 1/147.8 is applied to the partial sums.
 //   HYB    the looked-up LUT pair (c0, c1) with the sign of Alg. 3 already folded into a
 //          2^(Q+1)-entry, 32-way replicated shared-memory table (conflict-free LDS).
-// Partial sums per (cell column, row) go to the workspace and are reduced in fixed order.
+// B operand: K-major, no swizzle, one 512-byte block per MMA (16 batch rows x 16 K; rows >= B
+// stay zero), so every descriptor differs only in its start address.
+// Partial sums per (cell column, row) go to the workspace; qtip_reduce sums them in a fixed
+// order (deterministic and independent of the grid or of row sharding).
 #include "decode.cuh"
 #include "internal.h"
 #include "tc.cuh"
 
 namespace qtip {
+
+// Debug timeline (CTA 0 only) set by qtip_internal_set_trace; null in normal operation.
+__device__ unsigned long long* g_tc_trace = nullptr;
+#define QTIP_TRACE(idx, field)                                                                   \
+    do {                                                                                         \
+        unsigned long long* _t = g_tc_trace;                                                     \
+        if (_t != nullptr && blockIdx.x == 0 && (idx) < 256) _t[(idx) * 8 + (field)] = clock64(); \
+    } while (0)
+
+#define QTIP_TRACE_NS(idx, field)                                                                \
+    do {                                                                                         \
+        unsigned long long* _t = g_tc_trace;                                                     \
+        if (_t != nullptr && blockIdx.x == 0) {                                                  \
+            unsigned long long _ns;                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_ns));                              \
+            _t[(idx) * 8 + (field)] = _ns;                                                       \
+        }                                                                                        \
+    } while (0)
+
 namespace {
 
 constexpr int kGroups = 4;
 constexpr int kDecWarps = 4 * kGroups;
-constexpr int kThreads = 32 * (2 + kDecWarps);   // 576
+constexpr int kThreads = 32 * (1 + kDecWarps + kGroups);   // 672: producer + 16 decoders + 4 issuers
 constexpr int kSlots = 8;
-constexpr int kHyBLutQ = 9;
-constexpr uint32_t kLutBytes = (1u << (kHyBLutQ + 1)) * 128u;   // 2^(Q+1) entries x 32 replicas x 4 B
+constexpr int kABufs = 3;
+constexpr int kHybLutQ = 9;
+constexpr uint32_t kLutBytes = (1u << (kHybLutQ + 1)) * 128u;   // 2^(Q+1) entries x 32 replicas x 4 B
 constexpr int kN = 16;                                          // UMMA N (batch padded)
+constexpr uint32_t kBlk = 512;                                  // B bytes per MMA: 16 rows x 16 K x 2 B
+constexpr int kMaxXtVecsPerThread = 4;                          // B <= 16, 32 vectors per batch row
 
 struct TcArgs {
     const uint32_t* packed;
@@ -59,34 +93,102 @@ struct Cfg {
     static constexpr int kMmaPerUnit = 8 * kMmaPerTile;
     static constexpr uint32_t kUnitBytes = 2048u * K;
     static constexpr int kXtVecs = kHyb ? 16 : 32;              // 16-byte vectors of x~ per cell per batch row
+    static constexpr uint32_t kBGroup = kMmaPerUnit * kBlk;     // one B buffer
 };
 
-// TMEM column map per group: D at 128 g, A buffers at 128 g + 32 + 32 b.
-__device__ __forceinline__ uint32_t d_col(int g) { return 128u * g; }
-__device__ __forceinline__ uint32_t a_col(int g, int b) { return 128u * g + 32u + 32u * b; }
+// Decode this thread's row of the two tiles of hand-off pw (word w of tile t at pw[2w + t]) and
+// store the A operand into TMEM columns ta .. ta + 2 * kColsPerTile.
+template <int K, int CODE>
+__device__ __forceinline__ void decode_handoff(const uint32_t* __restrict__ pw, int r, const CodeArgs& ca,
+                                               uint32_t lane4, uint32_t lut_base, uint32_t ta) {
+    using C = Cfg<K, CODE>;
+    if constexpr (K == 2 && !C::kHyb) {
+        const uint2 A = *reinterpret_cast<const uint2*>(pw + 2 * r);
+        const uint2 Bw = *reinterpret_cast<const uint2*>(pw + 2 * ((r + 1) & 15));
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            uint32_t x[16], z[16];
+            windows_k2v1(tt ? A.y : A.x, tt ? Bw.y : Bw.x, x);
+#pragma unroll
+            for (int qq = 0; qq < 16; ++qq) {
+                if constexpr (CODE == QTIP_CODE_3INST) z[qq] = inst3_word(x[qq], ca.a, ca.b, ca.magic);
+                else z[qq] = __dp4a(x[qq] * ca.a + ca.b, 0x01010101u, 0xE5FE6400u);
+            }
+            ptx::tmem_st16(ta + tt * 16, z);
+        }
+    } else if constexpr (K == 4 && C::kHyb) {
+        const uint4 AB = *reinterpret_cast<const uint4*>(pw + 4 * r);   // words 2r, 2r+1 of both tiles
+        const uint2 Cw = *reinterpret_cast<const uint2*>(pw + 2 * ((2 * r + 2) & 31));
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            uint32_t x[8], z[8];
+            windows_k4v2_dirty(tt ? AB.y : AB.x, tt ? AB.w : AB.z, tt ? Cw.y : Cw.x, x);
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) {
+                const uint32_t h2 = x[qq] * (x[qq] + x[qq] + 2u);       // 2 (x^2 + x)
+                uint32_t off;
+                asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(off) : "r"(h2), "r"(0x1FF80u), "r"(lane4));
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(z[qq]) : "r"(lut_base + off));
+            }
+            ptx::tmem_st8(ta + tt * 8, z);
+        }
+    } else {
+        // general k (and HYB at k = 2, 3): windows from three words per tile row
+        constexpr int TW = 8 * K;
+        const int start = 16 * K * r, w0 = start >> 5, off = start & 31;
+        const uint2 W0 = *reinterpret_cast<const uint2*>(pw + 2 * (w0 % TW));
+        const uint2 W1 = *reinterpret_cast<const uint2*>(pw + 2 * ((w0 + 1) % TW));
+        const uint2 W2 = *reinterpret_cast<const uint2*>(pw + 2 * ((w0 + 2) % TW));
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            const uint32_t a0 = tt ? W0.y : W0.x, a1 = tt ? W1.y : W1.x, a2 = tt ? W2.y : W2.x;
+            if constexpr (C::kHyb) {
+                uint32_t z[8];
+#pragma unroll
+                for (int qq = 0; qq < 8; ++qq) {
+                    const uint32_t x = window_general(a0, a1, a2, off + qq * 2 * K);
+                    const uint32_t h2 = x * (x + x + 2u);
+                    uint32_t o;
+                    asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(o) : "r"(h2), "r"(0x1FF80u), "r"(lane4));
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(z[qq]) : "r"(lut_base + o));
+                }
+                ptx::tmem_st8(ta + tt * 8, z);
+            } else {
+                uint32_t z[16];
+#pragma unroll
+                for (int qq = 0; qq < 16; ++qq) {
+                    const uint32_t x = window_general(a0, a1, a2, off + qq * K);
+                    if constexpr (CODE == QTIP_CODE_3INST) z[qq] = inst3_word(x, ca.a, ca.b, ca.magic);
+                    else z[qq] = __dp4a(x * ca.a + ca.b, 0x01010101u, 0xE5FE6400u);
+                }
+                ptx::tmem_st16(ta + tt * 16, z);
+            }
+        }
+    }
+}
 
-template <int K, int CODE, int NB8>
+template <int K, int CODE>
 __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args) {
     using C = Cfg<K, CODE>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index and TMEM base made provably warp-uniform (shfl) so UMMA operands stay in
+    // uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) QTIP_TRACE_NS(255, 0);
 
     // ---------------- shared memory carve-up
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 960);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 1008);
     uint8_t* stream = smem + 1024;
     uint8_t* bbuf = stream + kSlots * C::kUnitBytes;
-    constexpr uint32_t kBlk = 256u * NB8;                              // B bytes per MMA
-    constexpr uint32_t kBGroup = C::kMmaPerUnit * kBlk;
-    uint8_t* zero_blk = bbuf + kGroups * kBGroup;
-    uint8_t* lut = zero_blk + 256;
+    uint8_t* lut = bbuf + 2 * kGroups * C::kBGroup;
     const uint32_t bar0 = ptx::smem_u32(bars);
     auto full = [&](int s) { return bar0 + 8u * s; };
     auto empty = [&](int s) { return bar0 + 8u * (kSlots + s); };
-    auto afull = [&](int g, int b) { return bar0 + 8u * (2 * kSlots + 2 * g + b); };
-    auto aempty = [&](int g, int b) { return bar0 + 8u * (2 * kSlots + 8 + 2 * g + b); };
-    auto dfull = [&](int g) { return bar0 + 8u * (2 * kSlots + 16 + g); };
-    auto dempty = [&](int g) { return bar0 + 8u * (2 * kSlots + 20 + g); };
+    auto aempty = [&](int g, int b) { return bar0 + 8u * (2 * kSlots + kABufs * g + b); };
+    auto dfull = [&](int g, int b) { return bar0 + 8u * (2 * kSlots + 12 + 2 * g + b); };
+    auto afull = [&](int g, int b) { return bar0 + 8u * (2 * kSlots + 20 + kABufs * g + b); };
 
     const int64_t G = gridDim.x;
     const int64_t u0 = args.units * blockIdx.x / G, u1 = args.units * (blockIdx.x + 1) / G;
@@ -96,41 +198,45 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
     // ---------------- one-time setup
     {
         uint4* z = reinterpret_cast<uint4*>(bbuf);
-        const int nz = (kGroups * kBGroup + 256) / 16;
+        const int nz = (2 * kGroups * C::kBGroup) / 16;
         for (int i = threadIdx.x; i < nz; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
         if constexpr (C::kHyb) {
             // entry e = idx | sign << Q -> (c0, c1) with c1 negated when sign (Alg. 3), 32 replicas
-            for (int i = threadIdx.x; i < (1 << (kHyBLutQ + 1)) * 8; i += kThreads) {
+            for (int i = threadIdx.x; i < (1 << (kHybLutQ + 1)) * 8; i += kThreads) {
                 const int e = i >> 3, quad = i & 7;
-                uint32_t w = __ldg(args.lut + (e & ((1 << kHyBLutQ) - 1)));
-                if (e >> kHyBLutQ) w ^= 0x80000000u;
+                uint32_t w = __ldg(args.lut + (e & ((1 << kHybLutQ) - 1)));
+                if (e >> kHybLutQ) w ^= 0x80000000u;
                 reinterpret_cast<uint4*>(lut)[(e * 128 + quad * 16) / 16] = make_uint4(w, w, w, w);
             }
         }
     }
-    if (warp == 0 && lane == 0) {
-        for (int s = 0; s < kSlots; ++s) {
-            ptx::mbar_init(full(s), 1);
-            ptx::mbar_init(empty(s), 128);
-        }
-        for (int g = 0; g < kGroups; ++g) {
-            for (int b = 0; b < 2; ++b) {
-                ptx::mbar_init(afull(g, b), 128);
-                ptx::mbar_init(aempty(g, b), 1);
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < kSlots; ++s) {
+                ptx::mbar_init(full(s), 1);
+                ptx::mbar_init(empty(s), 128);
             }
-            ptx::mbar_init(dfull(g), 1);
-            ptx::mbar_init(dempty(g), 128);
+            for (int g = 0; g < kGroups; ++g) {
+                for (int b = 0; b < kABufs; ++b) {
+                    ptx::mbar_init(aempty(g, b), 1);
+                    ptx::mbar_init(afull(g, b), 128);
+                }
+                for (int b = 0; b < 2; ++b) ptx::mbar_init(dfull(g, b), 1);
+            }
+            ptx::fence_mbar_init();
         }
-        ptx::fence_mbar_init();
+        __syncwarp();
+        ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
     }
-    if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_holder;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_holder, 0);
+    ptx::pdl_launch_dependents();
+    if (threadIdx.x == 0) QTIP_TRACE_NS(255, 1);
 
     if (warp == 0) {
-        // ================= producer
+        // ================= producer (packed weights are independent of the previous kernel)
         if (lane == 0) {
             for (int j = 0; j < nunits; ++j) {
                 const int s = j % kSlots, use = j / kSlots;
@@ -142,175 +248,150 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
                 ptx::bulk_g2s(ptx::smem_u32(stream + s * C::kUnitBytes), src, C::kUnitBytes, full(s));
             }
         }
-    } else if (warp == 1) {
-        // ================= MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_f16_f32(128, kN);
-            const uint32_t zaddr = ptx::smem_u32(zero_blk);
-            for (int j = 0; j < nunits; ++j) {
-                // unit j is the lu-th unit of group g; its handoff h is the group's (4 lu + h)-th,
-                // so it uses A buffer h & 1 for the (2 lu + h/2)-th time
-                const int g = j & 3;
-                const uint32_t lu = (uint32_t)j >> 2;
-                if (lu > 0) ptx::mbar_wait(dempty(g), (lu - 1) & 1);
+    } else if (warp > kDecWarps) {
+        // ================= per-group UMMA issuer: waits for the group's hand-off, issues, commits
+        const int g = warp - kDecWarps - 1;
+        const uint32_t tgrp = tmem + 128u * g;
+        constexpr uint32_t idesc = ptx::idesc_f16_f32(128, kN);
+        const uint32_t bdesc_lo0 = (ptx::smem_u32(bbuf + 2 * g * C::kBGroup) >> 4) | ((128u >> 4) << 16);
+        constexpr uint32_t kBDescHi = (256u >> 4) | (1u << 14);
+        const int my_unit_count = (nunits > g) ? (nunits - g + kGroups - 1) / kGroups : 0;
+        for (int lu = 0; lu < my_unit_count; ++lu) {
+            const uint32_t db = lu & 1;
+            const uint32_t bdesc_lo = bdesc_lo0 + db * (C::kBGroup >> 4);
+            const uint32_t dcol = tgrp + 16u * db;
+#pragma unroll 1
+            for (int h = 0; h < 4; ++h) {
+                const uint32_t hc = 4u * lu + h;
+                const int b = (int)(hc % kABufs);
+                ptx::mbar_wait(afull(g, b), (hc / kABufs) & 1);
                 ptx::tc_fence_after();
-                const uint32_t bgrp = ptx::smem_u32(bbuf + g * kBGroup);
-                for (int h = 0; h < 4; ++h) {
-                    const int b = h & 1;
-                    ptx::mbar_wait(afull(g, b), (2 * lu + (h >> 1)) & 1);
-                    ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                    const uint32_t acol = tgrp + 32u + 32u * (uint32_t)b;
 #pragma unroll
                     for (int tt = 0; tt < 2; ++tt) {
 #pragma unroll
                         for (int half = 0; half < C::kMmaPerTile; ++half) {
                             const int mi = (2 * h + tt) * C::kMmaPerTile + half;
-                            const uint32_t start = bgrp + mi * kBlk;
-                            const uint32_t sbo = (NB8 == 2) ? 256u : (zaddr - start);
-                            const uint64_t bdesc = ptx::smem_desc_kmajor_noswizzle(start, 128u, sbo);
-                            const uint32_t a = tmem + a_col(g, b) + tt * C::kColsPerTile + half * 8;
-                            ptx::umma_f16_ts(tmem + d_col(g), a, bdesc, idesc, (h | tt | half) != 0);
+                            const uint64_t bdesc = ((uint64_t)kBDescHi << 32) | (bdesc_lo + mi * (kBlk >> 4));
+                            ptx::umma_f16_ts(dcol, acol + tt * C::kColsPerTile + half * 8, bdesc, idesc,
+                                             (h | tt | half) != 0);
                         }
                     }
                     ptx::umma_commit(aempty(g, b));
+                    if (h == 3) ptx::umma_commit(dfull(g, db));
+                    QTIP_TRACE(g * 64 + hc, 4);
                 }
-                ptx::umma_commit(dfull(g));
+                __syncwarp();
             }
         }
     } else {
-        // ================= decoders
-        const int dw = warp - 2, g = dw >> 2, q = warp & 3;
-        const int tg = (dw & 3) * 32 + lane;                 // thread index within the group
+        // ================= decode groups
+        const int dw = warp - 1, g = dw >> 2, wg = dw & 3, q = warp & 3;
+        const int tg = wg * 32 + lane;                        // thread index within the group
         const int R = 32 * q + lane, I = R >> 4, r = R & 15;
-        const uint32_t taddr_lane = tmem + ((uint32_t)(32 * q) << 16);
+        const uint32_t taddr_lane = tmem + ((uint32_t)(32 * q) << 16) + 128u * g;
         const uint32_t lane4 = (uint32_t)lane * 4u;
         const uint32_t lut_base = ptx::smem_u32(lut);
-        uint8_t* bgrp = bbuf + g * kBGroup;
-        uint32_t lu = 0;
-        for (int j = g; j < nunits; j += kGroups, ++lu) {
+        const int nvec = args.B * C::kXtVecs;
+        const int my_unit_count = (nunits > g) ? (nunits - g + kGroups - 1) / kGroups : 0;
+
+        auto load_xt = [&](int j, uint4 (&xv)[kMaxXtVecsPerThread]) {
+            const int64_t KC = (u0 + j) % n_kc;
+#pragma unroll
+            for (int i = 0; i < kMaxXtVecsPerThread; ++i) {
+                const int e = tg + 128 * i;
+                if (e < nvec) {
+                    const int n = e / C::kXtVecs, v = e % C::kXtVecs;
+                    xv[i] = __ldcg(reinterpret_cast<const uint4*>(args.xt + n * args.xt_row_bytes +
+                                                                  KC * (C::kXtVecs * 16) + v * 16));
+                }
+            }
+        };
+        auto epilogue = [&](int lp) {
+            const int j = g + kGroups * lp;
             const int64_t u = u0 + j;
             const int64_t RB = args.rb0 + u / n_kc, KC = u % n_kc;
+            ptx::mbar_wait(dfull(g, lp & 1), (lp >> 1) & 1);
+            ptx::tc_fence_after();
+            uint32_t d[16];
+            ptx::tmem_ld16(taddr_lane + 16u * (lp & 1), d);
+            ptx::tc_wait_ld();
+            ptx::tc_fence_before();
+            const int64_t row = RB * kCellRows + R;
+#pragma unroll
+            for (int bb = 0; bb < kN; ++bb)
+                if (bb < args.B)
+                    args.partial[(KC * args.B + bb) * args.lay.m_pad + row] = __uint_as_float(d[bb]) * args.code_factor;
+        };
+
+        ptx::pdl_wait();                                      // x~ is written by the previous kernel
+        uint4 xv[kMaxXtVecsPerThread];
+        if (my_unit_count > 0) load_xt(g, xv);
+        for (int lu = 0; lu < my_unit_count; ++lu) {
+            const int j = g + kGroups * lu;
             const int s = j % kSlots;
-            // ---- B operand: this cell's 128 columns of x~ (rows >= B stay zero)
-            for (int e = tg; e < args.B * C::kXtVecs; e += 128) {
-                const int n = e / C::kXtVecs, v = e % C::kXtVecs;
-                const uint4 val = *reinterpret_cast<const uint4*>(args.xt + n * args.xt_row_bytes +
-                                                                  KC * (C::kXtVecs * 16) + v * 16);
-                *reinterpret_cast<uint4*>(bgrp + (v >> 1) * kBlk + (n >> 3) * 256 + (v & 1) * 128 + (n & 7) * 16) = val;
+            const uint32_t db = lu & 1;
+            // ---- B operand of this cell (x~ columns; rows >= B stay zero).  Buffer db was last
+            //      read by the MMAs of cell lu-2, complete since its epilogue waited on dfull.
+            uint8_t* bgrp = bbuf + (2 * g + db) * C::kBGroup;
+#pragma unroll
+            for (int i = 0; i < kMaxXtVecsPerThread; ++i) {
+                const int e = tg + 128 * i;
+                if (e < nvec) {
+                    const int n = e / C::kXtVecs, v = e % C::kXtVecs;
+                    *reinterpret_cast<uint4*>(bgrp + (v >> 1) * kBlk + (n >> 3) * 256 + (v & 1) * 128 + (n & 7) * 16) = xv[i];
+                }
             }
             ptx::fence_proxy_async_smem();
+            if (lu + 1 < my_unit_count) load_xt(j + kGroups, xv);            // prefetch next cell's x~
+            if (lane == 0 && wg == 0) QTIP_TRACE(g * 64 + 4 * lu, 6);
             ptx::mbar_wait(full(s), (j / kSlots) & 1);
+            if (lane == 0 && wg == 0) QTIP_TRACE(g * 64 + 4 * lu, 7);
             const uint32_t* slot = reinterpret_cast<const uint32_t*>(stream + s * C::kUnitBytes);
 #pragma unroll 1
             for (int h = 0; h < 4; ++h) {
-                const int b = h & 1;
-                const uint32_t use = 2 * lu + (h >> 1);                // uses of A buffer b so far
+                const uint32_t hc = 4u * lu + h;                       // hand-off number of this group
+                const int b = (int)(hc % kABufs);
+                const uint32_t use = hc / kABufs;                      // earlier uses of A buffer b
+                const bool tr = (lane == 0 && wg == 0);
+                if (tr) QTIP_TRACE(g * 64 + hc, 0);
                 if (use > 0) ptx::mbar_wait(aempty(g, b), (use - 1) & 1);
+                if (tr) QTIP_TRACE(g * 64 + hc, 1);
                 ptx::tc_fence_after();
-                const uint32_t* pw = slot + (I * 4 + h) * (8 * K) * 2;      // word w of tile t at pw[2w + t]
-                const uint32_t ta = taddr_lane + a_col(g, b);
-                if constexpr (K == 2 && !C::kHyb) {
-                    const uint2 A = *reinterpret_cast<const uint2*>(pw + 2 * r);
-                    const uint2 Bw = *reinterpret_cast<const uint2*>(pw + 2 * ((r + 1) & 15));
-#pragma unroll
-                    for (int tt = 0; tt < 2; ++tt) {
-                        uint32_t x[16], z[16];
-                        windows_k2v1(tt ? A.y : A.x, tt ? Bw.y : Bw.x, x);
-#pragma unroll
-                        for (int qq = 0; qq < 16; ++qq) {
-                            if constexpr (CODE == QTIP_CODE_3INST) z[qq] = inst3_word(x[qq], args.ca.a, args.ca.b, args.ca.magic);
-                            else z[qq] = __dp4a(x[qq] * args.ca.a + args.ca.b, 0x01010101u, 0xE5FE6400u);
-                        }
-                        ptx::tmem_st16(ta + tt * 16, z);
-                    }
-                } else if constexpr (K == 4 && C::kHyb) {
-                    const uint4 AB = *reinterpret_cast<const uint4*>(pw + 4 * r);   // words 2r, 2r+1 of both tiles
-                    const uint2 Cw = *reinterpret_cast<const uint2*>(pw + 2 * ((2 * r + 2) & 31));
-#pragma unroll
-                    for (int tt = 0; tt < 2; ++tt) {
-                        uint32_t x[8], z[8];
-                        windows_k4v2_dirty(tt ? AB.y : AB.x, tt ? AB.w : AB.z, tt ? Cw.y : Cw.x, x);
-#pragma unroll
-                        for (int qq = 0; qq < 8; ++qq) {
-                            const uint32_t h2 = x[qq] * (x[qq] + x[qq] + 2u);       // 2 (x^2 + x)
-                            uint32_t off;
-                            asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(off) : "r"(h2), "r"(0x1FF80u), "r"(lane4));
-                            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(z[qq]) : "r"(lut_base + off));
-                        }
-                        ptx::tmem_st8(ta + tt * 8, z);
-                    }
-                } else {
-                    // general k (and HYB at k = 2, 3): windows from three words per tile row
-                    constexpr int TW = 8 * K;
-                    const int start = 16 * K * r, w0 = start >> 5, off = start & 31;
-                    const uint2 W0 = *reinterpret_cast<const uint2*>(pw + 2 * (w0 % TW));
-                    const uint2 W1 = *reinterpret_cast<const uint2*>(pw + 2 * ((w0 + 1) % TW));
-                    const uint2 W2 = *reinterpret_cast<const uint2*>(pw + 2 * ((w0 + 2) % TW));
-#pragma unroll
-                    for (int tt = 0; tt < 2; ++tt) {
-                        const uint32_t a0 = tt ? W0.y : W0.x, a1 = tt ? W1.y : W1.x, a2 = tt ? W2.y : W2.x;
-                        if constexpr (C::kHyb) {
-                            uint32_t z[8];
-#pragma unroll
-                            for (int qq = 0; qq < 8; ++qq) {
-                                const uint32_t x = window_general(a0, a1, a2, off + qq * 2 * K);
-                                const uint32_t h2 = x * (x + x + 2u);
-                                uint32_t o;
-                                asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(o) : "r"(h2), "r"(0x1FF80u), "r"(lane4));
-                                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(z[qq]) : "r"(lut_base + o));
-                            }
-                            ptx::tmem_st8(ta + tt * 8, z);
-                        } else {
-                            uint32_t z[16];
-#pragma unroll
-                            for (int qq = 0; qq < 16; ++qq) {
-                                const uint32_t x = window_general(a0, a1, a2, off + qq * K);
-                                if constexpr (CODE == QTIP_CODE_3INST) z[qq] = inst3_word(x, args.ca.a, args.ca.b, args.ca.magic);
-                                else z[qq] = __dp4a(x * args.ca.a + args.ca.b, 0x01010101u, 0xE5FE6400u);
-                            }
-                            ptx::tmem_st16(ta + tt * 16, z);
-                        }
-                    }
-                }
+                decode_handoff<K, CODE>(slot + (I * 4 + h) * (8 * K) * 2, r, args.ca, lane4, lut_base,
+                                        taddr_lane + 32u + 32u * b);
                 if (h == 3) ptx::mbar_arrive(empty(s));               // all reads of this slot done
+                if (tr) QTIP_TRACE(g * 64 + hc, 2);
                 ptx::tc_wait_st();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(afull(g, b));
+                ptx::mbar_arrive(afull(g, b));                         // hand-off to the group's issuer
+                if (tr) QTIP_TRACE(g * 64 + hc, 3);
+                if (h == 0 && lu > 0) epilogue(lu - 1);               // drain the previous cell's D
+                if (tr) QTIP_TRACE(g * 64 + hc, 5);
             }
-            // ---- epilogue: D (row R, N columns) -> partial sums of this cell column
-            ptx::mbar_wait(dfull(g), lu & 1);
-            ptx::tc_fence_after();
-            uint32_t d[16];
-            ptx::tmem_ld16(taddr_lane + d_col(g), d);
-            ptx::tc_wait_ld();
-            const int64_t row = RB * kCellRows + R;
-            for (int bb = 0; bb < args.B; ++bb)
-                args.partial[(KC * args.B + bb) * args.lay.m_pad + row] = __uint_as_float(d[bb]) * args.code_factor;
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(dempty(g));
         }
+        if (my_unit_count > 0) epilogue(my_unit_count - 1);
     }
+    if (threadIdx.x == 32) QTIP_TRACE_NS(255, 2);                 // first decoder thread done
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 0) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 512);
     }
+    if (threadIdx.x == 0) QTIP_TRACE_NS(255, 3);
 }
 
-template <int K, int CODE, int NB8>
+template <int K, int CODE>
 cudaError_t launch_tc_t(const TcArgs& a, cudaStream_t s) {
     using C = Cfg<K, CODE>;
-    constexpr uint32_t kBlk = 256u * NB8;
-    const size_t smem = 1024 + kSlots * C::kUnitBytes + kGroups * C::kMmaPerUnit * kBlk + 256 + (C::kHyb ? kLutBytes : 0);
-    auto kern = gemv_tc_kernel<K, CODE, NB8>;
+    const size_t smem = 1024 + kSlots * C::kUnitBytes + 2 * kGroups * C::kBGroup + (C::kHyb ? kLutBytes : 0);
+    auto kern = gemv_tc_kernel<K, CODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::min<int64_t>(sms, a.units);
-    kern<<<grid, kThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    const int grid = (int)std::min<int64_t>(num_sms(), a.units);
+    return launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, a);
 }
 
 }  // namespace
@@ -318,7 +399,7 @@ cudaError_t launch_tc_t(const TcArgs& a, cudaStream_t s) {
 bool gemv_tc_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B) {
     if (B < 1 || B > 16) return false;
     if (lay.k < 2 || lay.k > 4) return false;
-    if (code == QTIP_CODE_HYB && (ca.Q != kHyBLutQ || ca.two_sign)) return false;
+    if (code == QTIP_CODE_HYB && (ca.Q != kHybLutQ || ca.two_sign)) return false;
     return true;
 }
 
@@ -339,10 +420,9 @@ cudaError_t launch_gemv_tc(const Layout& lay, int code, const CodeArgs& ca, cons
     a.units = (rb1 - rb0) * lay.n_kc;
     a.code_factor = (code == QTIP_CODE_1MAD) ? 5.0f / 739.0f : 1.0f;   // 1/147.8 for 1MAD
     a.partial = partial;
-    const bool nb2 = B > 8;
     cudaError_t e = cudaErrorInvalidValue;
-#define QTIP_TC_CASE(KK, CC)                                                         \
-    if (lay.k == KK && code == CC) e = nb2 ? launch_tc_t<KK, CC, 2>(a, s) : launch_tc_t<KK, CC, 1>(a, s);
+#define QTIP_TC_CASE(KK, CC) \
+    if (lay.k == KK && code == CC) e = launch_tc_t<KK, CC>(a, s);
     QTIP_TC_CASE(2, QTIP_CODE_3INST)
     QTIP_TC_CASE(3, QTIP_CODE_3INST)
     QTIP_TC_CASE(4, QTIP_CODE_3INST)
@@ -358,3 +438,8 @@ cudaError_t launch_gemv_tc(const Layout& lay, int code, const CodeArgs& ca, cons
 }
 
 }  // namespace qtip
+
+extern "C" int qtip_internal_set_trace(void* dptr) {
+    unsigned long long* p = (unsigned long long*)dptr;
+    return (int)cudaMemcpyToSymbol(qtip::g_tc_trace, &p, sizeof(p));
+}

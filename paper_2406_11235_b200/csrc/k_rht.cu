@@ -1,20 +1,24 @@
 // k_rht.cu -- random Hadamard transform kernels.
 //
-// H_n = H_b (x) H_{2^a} (reading R7).  Split 2^a = 2^a1 * 2^a2 and write
-// H_n = M_f (x) H_{2^a2} with the "mix" factor M_f = H_b (x) H_{2^a1} of order f = n / 2^a2.
-// A CTA owns `rows_per_cta` rows i of M_f: it forms u_i = sum_j M_f[i][j] v_j (v_j the
-// j-th length-2^a2 slice of the signed input) and then runs an in-shared-memory fast
-// Walsh-Hadamard transform of length 2^a2 on each u_i.  No CTA repeats another's work, and
-// every CTA reads the whole (L2-resident) input once.
+// H_n = H_b (x) H_{2^a} (reading R7).  Split 2^a = 2^a1 * 2^a2 (2^a2 <= 256) and write
+// H_n = M_f (x) H_{2^a2} with the "mix" factor M_f = H_b (x) H_{2^a1} of order f = n / 2^a2,
+// M_f[i][j] = H_b[i_b][j_b] * (-1)^popcount(i_a1 & j_a1).
+// One CTA of 256 threads owns R = 256 / 2^a2 rows i of M_f (one output per thread):
+//   1. stage the whole signed input (n floats, coalesced float4) in shared memory,
+//   2. u_i[c] = sum_j M_f[i][j] v_j[c] from shared memory (sign bits of its H_b row in smem),
+//   3. fast Walsh-Hadamard transform of length 2^a2 across the threads: butterflies with
+//      partner distance < 32 via warp shuffles, the rest through shared memory,
+//   4. scale (and the output signs for the inverse), coalesced store.
+// No CTA repeats another's arithmetic; every CTA reads the (L2-resident) input once.
 #include <algorithm>
 #include <cmath>
 
 #include "internal.h"
+#include "tc.cuh"
 
 namespace qtip {
 
 constexpr int kRhtThreads = 256;
-constexpr int kRhtMaxElems = 4096;   // rows_per_cta * 2^a2 held in shared memory
 
 // out_mode 0: float32; 1: binary16 duplicated into both halves of a 32-bit word (the K-doubled
 // UMMA B operand); 2: binary16.
@@ -28,107 +32,148 @@ __device__ __forceinline__ void store_out(void* out, int mode, int64_t idx, floa
     }
 }
 
-__device__ __forceinline__ float sign_of(const uint8_t* __restrict__ s, int64_t i) {
-    return ((s[i >> 3] >> (i & 7)) & 1) ? -1.0f : 1.0f;
+__device__ __forceinline__ uint32_t sign_bit(const uint8_t* __restrict__ s, int64_t i) {
+    return (s[i >> 3] >> (i & 7)) & 1u;
 }
 
 __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const uint8_t* __restrict__ sign,
                                                            const float* __restrict__ in, int64_t in_stride,
                                                            void* __restrict__ out, int64_t out_stride, int inverse,
                                                            float out_scale, int out_mode, int64_t pad_to) {
-    __shared__ float buf[kRhtMaxElems];
-    __shared__ float part[kRhtThreads];
+    extern __shared__ __align__(16) float xs[];             // [n] staged input, then [256] FWHT exchange
+    __shared__ uint32_t hrow[64][32];                        // H_b (or H_b^T) rows of this CTA's rows, bits
     const int L2 = 1 << plan.a2;
-    const int R = plan.rows_per_cta;
-    const int i0 = blockIdx.x * R;
-    const int64_t bt = blockIdx.y;
-    const float* x = in + bt * in_stride;
-    const int a1 = plan.a - plan.a2;
-    const int n1 = 1 << a1;
-    const int outputs = R * L2;
-    const int slices = max(1, kRhtThreads / outputs);          // threads cooperating on one output
+    const int R = plan.rows_per_cta;                         // rows of M_f per CTA
+    const int RL = R * L2;                                   // outputs per CTA
+    const int S = kRhtThreads / RL;                          // threads (j-slices) per output
     const int tid = threadIdx.x;
+    const int sl = tid / RL, il = (tid % RL) >> plan.a2, c = tid & (L2 - 1);
+    const int i = blockIdx.x * R + il;                       // row of M_f
+    const int64_t bt = blockIdx.y;
+    const int n1 = 1 << (plan.a - plan.a2);
+    const int n = (int)plan.n;
+    const float* x = in + bt * in_stride;
 
-    // ---- mix: u[i][c] = sum_j M_f[i][j] * v[j][c]
-    for (int o0 = 0; o0 < outputs; o0 += kRhtThreads / slices) {
-        const int o = o0 + tid / slices;
-        const int sl = tid % slices;
-        float acc = 0.0f;
-        const int il = o / L2, c = o % L2;
-        const int i = i0 + il;
-        if (o < outputs && tid / slices < kRhtThreads / slices && i < plan.f) {
-            const int ib = i / n1, ia = i % n1;
-            for (int j = sl; j < plan.f; j += slices) {
-                const int jb = j / n1, ja = j % n1;
-                int neg = __popc(ia & ja) & 1;
-                if (plan.b > 1) {
-                    const int64_t bit = inverse ? ((int64_t)jb * plan.b + ib) : ((int64_t)ib * plan.b + jb);
-                    neg ^= (plan.hb[bit >> 5] >> (bit & 31)) & 1;
+    ptx::pdl_wait();                                         // the input may be the previous kernel's output
+    ptx::pdl_launch_dependents();
+
+    // 1. stage v = (S .) x into shared memory (loads batched 8 deep to overlap their latency)
+    for (int e0 = 4 * tid; e0 < n; e0 += 4 * kRhtThreads * 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + 4 * kRhtThreads * u;
+            if (e < n) v[u] = __ldg(reinterpret_cast<const float4*>(x + e));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + 4 * kRhtThreads * u;
+            if (e < n) {
+                if (!inverse) {
+                    const uint32_t sb = (sign[e >> 3] >> (e & 7)) & 0xFu;   // e % 4 == 0: four bits of one byte
+                    v[u].x = (sb & 1u) ? -v[u].x : v[u].x;
+                    v[u].y = (sb & 2u) ? -v[u].y : v[u].y;
+                    v[u].z = (sb & 4u) ? -v[u].z : v[u].z;
+                    v[u].w = (sb & 8u) ? -v[u].w : v[u].w;
                 }
-                const int64_t e = (int64_t)j * L2 + c;
-                float v = x[e];
-                if (!inverse) v *= sign_of(sign, e);
-                acc += neg ? -v : v;
+                *reinterpret_cast<float4*>(xs + e) = v[u];
             }
         }
-        part[tid] = acc;
+    }
+    if (plan.b > 1) {
+        const int wpr = (plan.b + 31) >> 5;
+        for (int e = tid; e < R * wpr; e += kRhtThreads) {
+            const int rl = e / wpr, w = e % wpr;
+            const int ib = min(blockIdx.x * R + rl, plan.f - 1) / n1;
+            hrow[rl][w] = (inverse ? plan.hbt : plan.hb)[ib * wpr + w];
+        }
+    }
+    __syncthreads();
+
+    // 2. mix: u = sum_j M_f[i][j] v[j][c], the j-sum split over S slices (j_b = sl mod S)
+    //    that are added in slice order (a fixed association: deterministic)
+    float acc = 0.0f;
+    if (i < plan.f) {
+        const int ia = i & (n1 - 1);
+        for (int jb = sl; jb < plan.b; jb += S) {
+            const uint32_t sb = (plan.b > 1) ? ((hrow[il][jb >> 5] >> (jb & 31)) & 1u) : 0u;
+#pragma unroll 4
+            for (int ja = 0; ja < n1; ++ja) {
+                const uint32_t neg = sb ^ (__popc(ia & ja) & 1u);
+                const float v = xs[(jb * n1 + ja) * L2 + c];
+                acc += __int_as_float(__float_as_int(v) ^ (neg << 31));
+            }
+        }
+    }
+    __syncthreads();                                         // xs is reused below
+    if (S > 1) {
+        xs[tid] = acc;
         __syncthreads();
-        if (sl == 0 && o < outputs && tid / slices < kRhtThreads / slices) {
-            float s = 0.0f;
-            for (int q = 0; q < slices; ++q) s += part[tid + q];
-            buf[o] = s;
+        if (tid < RL) {
+            acc = 0.0f;
+            for (int q = 0; q < S; ++q) acc += xs[q * RL + tid];
         }
         __syncthreads();
     }
-    // ---- FWHT of length L2 on each row (butterflies (u+v, u-v) = H_2 on one index bit)
+    // 3. FWHT of length L2 along c (threads < R L2 hold the values; all threads run the loop so the
+    //    shuffles and barriers stay uniform): lower index of a pair gets u + v, upper gets u - v
     for (int h = 1; h < L2; h <<= 1) {
-        for (int q = tid; q < outputs / 2; q += kRhtThreads) {
-            const int row = q / (L2 / 2), k = q % (L2 / 2);
-            const int lo = row * L2 + (k / h) * 2 * h + (k % h);
-            const float u = buf[lo], v = buf[lo + h];
-            buf[lo] = u + v;
-            buf[lo + h] = u - v;
+        float other;
+        if (h < 32) {
+            other = __shfl_xor_sync(0xffffffffu, acc, h);
+        } else {
+            xs[tid] = acc;
+            __syncthreads();
+            other = xs[tid ^ h];
+            __syncthreads();
         }
-        __syncthreads();
+        acc = (c & h) ? (other - acc) : (acc + other);
     }
-    // ---- scale (and signs for the inverse), store
-    for (int o = tid; o < outputs; o += kRhtThreads) {
-        const int i = i0 + o / L2;
-        if (i >= plan.f) continue;
-        const int64_t e = (int64_t)i * L2 + (o % L2);
-        float v = buf[o] * out_scale;
-        if (inverse) v *= sign_of(sign, e);
+    // 4. scale (and signs for the inverse), store
+    if (sl == 0 && i < plan.f) {
+        const int64_t e = (int64_t)i * L2 + c;
+        float v = acc * out_scale;
+        if (inverse && sign_bit(sign, e)) v = -v;
         store_out(out, out_mode, bt * out_stride + e, v);
     }
-    if (blockIdx.x == 0)                                  // zero the padded tail [n, pad_to)
+    if (blockIdx.x == 0)                                     // zero the padded tail [n, pad_to)
         for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt * out_stride + e, 0.0f);
 }
 
 __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t in_stride, void* __restrict__ out,
                                int64_t out_stride, int out_mode, int64_t pad_to) {
     const int64_t bt = blockIdx.y;
+    ptx::pdl_wait();
+    ptx::pdl_launch_dependents();
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pad_to; e += (int64_t)gridDim.x * blockDim.x)
         store_out(out, out_mode, bt * out_stride + e, e < n ? in[bt * in_stride + e] : 0.0f);
 }
 
+constexpr int64_t kRhtMaxN = 48 * 1024;                      // staged input <= 192 KB of shared memory
+
 cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
     int b, a;
     if (!hadamard_factor(n, &b, &a)) return cudaErrorInvalidValue;
+    if (n > kRhtMaxN || n % 4) return cudaErrorInvalidValue;
     plan->n = n;
     plan->b = b;
     plan->a = a;
-    plan->a2 = a < 10 ? a : 10;
+    plan->a2 = a < 8 ? a : 8;
     plan->f = (int)(n >> plan->a2);
+    // at least one warp of outputs per CTA, at most ~2 waves of CTAs; the rest of the 256
+    // threads split each output's j-sum
     const int L2 = 1 << plan->a2;
-    int R = (plan->f + 127) / 128;                 // aim for <= 128 CTAs per batch column
-    while (R * L2 > kRhtMaxElems && R > 1) --R;
-    if (R * L2 > kRhtMaxElems) return cudaErrorInvalidValue;
+    int R = std::max(1, 32 / L2);
+    while ((plan->f + R - 1) / R > 296 && R * L2 < kRhtThreads) R *= 2;
     plan->rows_per_cta = R;
-    plan->hb = nullptr;
+    if (R * L2 > kRhtThreads || R > 64 || kRhtThreads % (R * L2)) return cudaErrorInvalidValue;
+    plan->hb = plan->hbt = nullptr;
     if (b > 1) {
         cudaError_t err = cudaSuccess;
-        plan->hb = hadamard_table_device(b, &err);
+        plan->hb = hadamard_table_device(b, false, &err);
         if (!plan->hb) return err == cudaSuccess ? cudaErrorUnknown : err;
+        plan->hbt = hadamard_table_device(b, true, &err);
+        if (!plan->hbt) return err == cudaSuccess ? cudaErrorUnknown : err;
     }
     return cudaSuccess;
 }
@@ -138,18 +183,25 @@ cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, cons
                        int64_t pad_to) {
     dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B);
     const float out_scale = (float)(scale / std::sqrt((double)plan.n));
-    rht_kernel<<<grid, kRhtThreads, 0, s>>>(plan, sign, in, in_stride, out, out_stride, inverse, out_scale, out_mode,
-                                            pad_to < plan.n ? plan.n : pad_to);
+    const int64_t pad = pad_to < plan.n ? plan.n : pad_to;
+    const size_t smem = (size_t)std::max<int64_t>(plan.n, kRhtThreads) * sizeof(float);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(rht_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kRhtMaxN * sizeof(float)));
+        attr_set = true;
+    }
+    cudaError_t e = launch_pdl(rht_kernel, grid, dim3(kRhtThreads), smem, s, plan, sign, in, in_stride, out,
+                               out_stride, inverse, out_scale, out_mode, pad);
     count_launch(1);
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
                            int out_mode, int64_t pad_to, cudaStream_t s) {
     dim3 grid((unsigned)std::min<int64_t>((pad_to + 255) / 256, 1024), (unsigned)B);
-    convert_kernel<<<grid, 256, 0, s>>>(in, n, in_stride, out, out_stride, out_mode, pad_to);
+    cudaError_t e = launch_pdl(convert_kernel, grid, dim3(256), 0, s, in, n, in_stride, out, out_stride, out_mode, pad_to);
     count_launch(1);
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace qtip

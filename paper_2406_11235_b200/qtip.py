@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libqtip.so")
 QTIP_CODE_1MAD, QTIP_CODE_3INST, QTIP_CODE_HYB = 1, 2, 3
 CODES = {"1mad": QTIP_CODE_1MAD, "3inst": QTIP_CODE_3INST, "hyb": QTIP_CODE_HYB}
 QTIP_RHT_IN, QTIP_RHT_OUT = 1, 2
-IMPL_AUTO, IMPL_SIMPLE, IMPL_TC = 0, 1, 2
+IMPL_AUTO, IMPL_SIMPLE, IMPL_TC, IMPL_MMA = 0, 1, 2, 3
 
 STATUS = {0: "QTIP_OK", -1: "QTIP_ERR_INVALID_PARAMS", -2: "QTIP_ERR_SHAPE", -3: "QTIP_ERR_INVALID_PATH",
           -4: "QTIP_ERR_ALIGNMENT", -5: "QTIP_ERR_UNSUPPORTED", -6: "QTIP_ERR_CUDA", -7: "QTIP_ERR_WORKSPACE"}
@@ -25,7 +25,7 @@ STATUS = {0: "QTIP_OK", -1: "QTIP_ERR_INVALID_PARAMS", -2: "QTIP_ERR_SHAPE", -3:
 EXPORTS = ["qtip_params_default", "qtip_params_check", "qtip_packed_bytes", "qtip_pack", "qtip_pack_states",
            "qtip_decode", "qtip_matvec", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
            "qtip_set_matvec_impl", "qtip_get_matvec_impl", "qtip_status_string", "qtip_last_error",
-           "qtip_launch_count", "qtip_profile_events"]
+           "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl"]
 
 
 class QtipParams(ctypes.Structure):
@@ -88,6 +88,8 @@ def load(path=LIB_PATH):
     lib.qtip_launch_count.restype = ctypes.c_uint64
     lib.qtip_profile_events.argtypes = [vp, vp]
     lib.qtip_profile_events.restype = None
+    lib.qtip_set_pdl.argtypes = [ctypes.c_int]
+    lib.qtip_set_pdl.restype = None
     _lib = lib
     return lib
 
@@ -198,6 +200,10 @@ def profile_events(ev_start, ev_stop):
         if not ev.cuda_event:
             ev.record()                       # torch creates the cudaEvent_t lazily
     load().qtip_profile_events(ctypes.c_void_p(ev_start.cuda_event), ctypes.c_void_p(ev_stop.cuda_event))
+
+
+def set_pdl(enable):
+    load().qtip_set_pdl(int(bool(enable)))
 
 
 def paley_host(b):
