@@ -201,7 +201,8 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B) {
     if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1) return 0;
     const Layout l = make_layout(m, n, p->k);
-    return align256(4 * B * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad);
+    const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);       // x~ rows (mma kernel pads the batch)
+    return align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad);
 }
 
 qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, const void* d_packed,
@@ -246,9 +247,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
     void* xt = ws;
-    float* partial = (float*)(ws + align256(4 * B * l.n_pad));
-    float* yt = (float*)(ws + align256(4 * B * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
-    const int xmode = (use_tc || use_mma) ? gemv_tc_xt_mode(p->code) : 0;
+    const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);
+    float* partial = (float*)(ws + align256(4 * Bx * l.n_pad));
+    float* yt = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
+    const int xmode = use_mma ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
     cudaError_t e;
     if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad);
     else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s);
@@ -257,9 +259,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const bool prof = g_prof_start && g_prof_stop;
     if (prof) cudaEventRecord(g_prof_start, s);
     if (use_tc || use_mma) {
-        const int64_t row_bytes = l.n_pad * (xmode == 1 ? 4 : 2);
+        const int64_t row_bytes = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2);
         e = use_tc ? launch_gemv_tc(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s)
-                   : launch_gemv_mma(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s);
+                   : launch_gemv_mma(l, p->code, ca, d_packed, d_lut, xt, row_bytes / 4, B, rb0, rb1, partial, s);
     } else {
         e = launch_gemv_simple(l, p->code, ca, d_packed, d_lut, (const float*)xt, B, rb0, rb1, partial, s);
     }

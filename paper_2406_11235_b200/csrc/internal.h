@@ -74,9 +74,13 @@ cudaError_t launch_gemv_tc(const Layout& lay, int code, const CodeArgs& ca, cons
                            const void* xt_compact, int64_t xt_row_bytes, int64_t B, int64_t rb0, int64_t rb1,
                            float* partial, cudaStream_t s);
 // Register-fed mma.sync fused decode-GEMV (k_gemv_mma.cu); same x~ encoding as the tcgen05 kernel.
+// x~ in fragment order (out_mode gemv_mma_xt_mode(code)), gemv_mma_batch_pad(B) rows of
+// xt_row_words 32-bit words (rows >= B may hold anything: they only feed discarded columns).
 bool gemv_mma_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B);
+int gemv_mma_xt_mode(int code);
+int gemv_mma_batch_pad(int64_t B);
 cudaError_t launch_gemv_mma(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
-                            const void* xt_compact, int64_t xt_row_bytes, int64_t B, int64_t rb0, int64_t rb1,
+                            const void* xt_frag, int64_t xt_row_words, int64_t B, int64_t rb0, int64_t rb1,
                             float* partial, cudaStream_t s);
 // y[b][i - row0] = scale * sum_kc partial[kc][b][i] for rows [row0, row1).
 cudaError_t launch_reduce(const float* partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0, int64_t row1,

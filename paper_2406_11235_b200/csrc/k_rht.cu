@@ -21,14 +21,29 @@ namespace qtip {
 constexpr int kRhtThreads = 256;
 
 // out_mode 0: float32; 1: binary16 duplicated into both halves of a 32-bit word (the K-doubled
-// UMMA B operand); 2: binary16.
-__device__ __forceinline__ void store_out(void* out, int mode, int64_t idx, float v) {
+// UMMA B operand); 2: binary16; 3 / 4: modes 1 / 2 permuted into mma.sync B-fragment order
+// within each 16-column tile (k_gemv_mma.cu): mode 3 puts columns (2t, 2t+8, 2t+1, 2t+9) at
+// words 4t .. 4t+3, mode 4 puts the pairs (t, t+4) at words 2t, 2t+1.  `row` is the element
+// offset of the batch row, e the column.
+__device__ __forceinline__ void store_out(void* out, int mode, int64_t row, int64_t e, float v) {
     if (mode == 0) {
-        static_cast<float*>(out)[idx] = v;
+        static_cast<float*>(out)[row + e] = v;
+        return;
+    }
+    const uint32_t h = __half_as_ushort(__float2half_rn(v));
+    const int64_t tile = e >> 4;
+    const int c = (int)(e & 15);
+    if (mode == 1) {
+        static_cast<uint32_t*>(out)[row + e] = h | (h << 16);
+    } else if (mode == 2) {
+        static_cast<uint16_t*>(out)[row + e] = (uint16_t)h;
+    } else if (mode == 3) {
+        const int t = (c & 7) >> 1, q = ((c & 1) << 1) | (c >> 3);
+        static_cast<uint32_t*>(out)[row + tile * 16 + 4 * t + q] = h | (h << 16);
     } else {
-        const uint32_t h = __half_as_ushort(__float2half_rn(v));
-        if (mode == 1) static_cast<uint32_t*>(out)[idx] = h | (h << 16);
-        else static_cast<uint16_t*>(out)[idx] = (uint16_t)h;
+        const int j = c >> 1;                                  // column pair
+        const int64_t w = tile * 8 + 2 * (j & 3) + (j >> 2);
+        static_cast<uint16_t*>(out)[row + 2 * w + (c & 1)] = (uint16_t)h;
     }
 }
 
@@ -134,10 +149,10 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const ui
         const int64_t e = (int64_t)i * L2 + c;
         float v = acc * out_scale;
         if (inverse && sign_bit(sign, e)) v = -v;
-        store_out(out, out_mode, bt * out_stride + e, v);
+        store_out(out, out_mode, bt * out_stride, e, v);
     }
     if (blockIdx.x == 0)                                     // zero the padded tail [n, pad_to)
-        for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt * out_stride + e, 0.0f);
+        for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt * out_stride, e, 0.0f);
 }
 
 __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t in_stride, void* __restrict__ out,
@@ -146,7 +161,7 @@ __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t 
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pad_to; e += (int64_t)gridDim.x * blockDim.x)
-        store_out(out, out_mode, bt * out_stride + e, e < n ? in[bt * in_stride + e] : 0.0f);
+        store_out(out, out_mode, bt * out_stride, e, e < n ? in[bt * in_stride + e] : 0.0f);
 }
 
 constexpr int64_t kRhtMaxN = 48 * 1024;                      // staged input <= 192 KB of shared memory
