@@ -45,6 +45,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def traffic(workload, code, k, impl):
+    """DRAM bytes (read + write) per GEMV launch from the committed `ncu --set full` capture
+    (profiles/traffic.json, written by scripts/ncu_traffic.py), or None if not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d[f"{workload}/{code}/k{k}"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
@@ -287,6 +298,7 @@ def run_ours(args):
     gemv_ms, gemv_bytes = 0.0, 0
     ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in layers]
     prof_steps = max(1, min(args.steps, 5))
+    qtip.set_pdl(False)              # with PDL the GEMV may start early and wait on its RHT-in
     for _ in range(prof_steps):
         for lay, o, (a, b_) in zip(layers, outs, ev_pairs):
             tgt = lay if world == 1 else lay.local
@@ -301,6 +313,7 @@ def run_ours(args):
             gemv_ms += a.elapsed_time(b_)
             gemv_bytes += tgt.m * tgt.n * k // 8
     qtip.profile_events(None, None)
+    qtip.set_pdl(True)
     gemv_ms = max_over_ranks(gemv_ms)
     gemv_gbs = gemv_bytes / (gemv_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -341,16 +354,17 @@ def run_ours(args):
             "metric": "fused trellis-decode GEMV: compressed-byte HBM GB/s vs peak; us/layer batch=1",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-            "vs_baseline": None, "dtype": "fp16xfp16->f32" if True else "", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": args.workload, "layers_per_step": len(layers), "blocks": nblocks,
                        "code": code, "k": k, "L": 16, "V": 2 if code == "hyb" else 1, "T": 256, "batch": B,
                        "stream_bytes_per_step": step_bytes, "tokens_per_s_equiv": round(B * 1e3 / ms, 2),
                        "per_layer": per_layer, "parallelism": f"rows{world}" if world > 1 else "single",
                        "l2": "inputs > L2: 1.62 GB of distinct packed weights per step (126 MB L2)"
                        if args.workload == "llama2-7b" else "distinct weights per layer",
-                       "matvec_impl": qtip.get_matvec_impl()},
+                       "matvec_impl": qtip.get_matvec_impl(),
+                       "arith": "decoded weights and RHT'd x in binary16, fp32 accumulation"},
             "roofline": {"bound": "hbm", "achieved": round(gemv_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(gemv_gbs / peak, 4), "traffic": None,
+                         "frac": round(gemv_gbs / peak, 4), "traffic": traffic(args.workload, code, k, qtip.get_matvec_impl()),
                          "kernel": "fused decode-GEMV", "peak_kind": peak_kind,
                          "avg_launch_us": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3)},
             "cpu_baseline": cpu,

@@ -129,7 +129,8 @@ qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d
 qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a);
 
 /* Selects the matvec kernel: 0 = auto (the measured-fastest supported kernel), 1 = CUDA-core
- * reference kernel, 2 = tcgen05 kernel (A in TMEM), 3 = register-fed mma.sync kernel.
+ * reference kernel, 2 = tcgen05 kernel (A in TMEM), 3 = register-fed mma.sync kernel with
+ * split-K over 128-column cells, 4 = row-tile mma.sync kernel (one CTA per 16 rows, B <= 4).
  * Process-wide; for ablations and tests. */
 void qtip_set_matvec_impl(int impl);
 int qtip_get_matvec_impl(void);

@@ -50,6 +50,7 @@ qtip_status check_shape(int64_t m, int64_t n) {
 void count_launch(int n) { g_launches += (uint64_t)n; }
 
 bool g_pdl = true;
+bool g_fused_reduce = false;
 bool pdl_enabled() { return g_pdl; }
 
 void prefer_max_smem(const void* kern) {
@@ -202,7 +203,8 @@ size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, i
     if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1) return 0;
     const Layout l = make_layout(m, n, p->k);
     const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);       // x~ rows (mma kernel pads the batch)
-    return align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad);
+    return align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad) +
+           align256(4 * (l.m_pad / kCellRows + 1));
 }
 
 qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, const void* d_packed,
@@ -239,29 +241,53 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     // auto picks the measured-fastest supported one
     const bool tc_ok = gemv_tc_supported(l, p->code, ca, B);
     const bool mma_ok = gemv_mma_supported(l, p->code, ca, B);
+    const bool row_ok = gemv_row_supported(l, p->code, ca, B);
     if (g_impl == 2 && !tc_ok) return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 kernel: needs 2 <= k <= 4, B <= 16, HYB Q = 9 one-sign");
     if (g_impl == 3 && !mma_ok) return fail(QTIP_ERR_UNSUPPORTED, "mma kernel: needs 2 <= k <= 4, B <= 16, one-sign HYB");
+    if (g_impl == 4 && !row_ok) return fail(QTIP_ERR_UNSUPPORTED, "row kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB");
     int impl = g_impl;
     if (impl == 0) impl = mma_ok ? 3 : (tc_ok ? 2 : 1);
-    const bool use_tc = impl == 2, use_mma = impl == 3;
+    const bool use_tc = impl == 2, use_mma = impl == 3, use_row = impl == 4;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
     void* xt = ws;
     const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);
     float* partial = (float*)(ws + align256(4 * Bx * l.n_pad));
     float* yt = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
-    const int xmode = use_mma ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
+    int* cnt = (int*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad));
+    const int n_rb = (int)(l.m_pad / kCellRows);
+    const int xmode = (use_mma || use_row) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
     cudaError_t e;
-    if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad);
-    else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s);
+    // the input kernel also clears the GEMV's split-K arrival counters (workspace is caller memory)
+    if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 1);
+    else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s, cnt, n_rb + 1);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
     const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
     const bool prof = g_prof_start && g_prof_stop;
     if (prof) cudaEventRecord(g_prof_start, s);
-    if (use_tc || use_mma) {
+    const bool rht_out = (flags & QTIP_RHT_OUT) != 0;
+    const bool fused_reduce = use_row || (use_mma && g_fused_reduce);
+    if (use_row) {
+        const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
+        e = launch_gemv_row(l, p->code, ca, d_packed, d_lut, xt, row_words, B, row_begin, row_end,
+                            rht_out ? yt : d_y, rht_out ? l.m_pad : row_end - row_begin, rht_out ? 0 : row_begin,
+                            rht_out ? m : row_end, rht_out ? 1.0f : scale, s);
+    } else if (use_mma) {
+        // split-K reduction fused into the GEMV: straight to y (no RHT-out) or to y~
+        MmaEpilogue ep;
+        ep.cnt = cnt;
+        ep.n_rb = n_rb;
+        ep.y = rht_out ? yt : d_y;
+        ep.y_stride = rht_out ? l.m_pad : row_end - row_begin;
+        ep.row_lo = rht_out ? 0 : row_begin;
+        ep.row_hi = rht_out ? m : row_end;
+        ep.scale = rht_out ? 1.0f : scale;
+        if (!fused_reduce) ep.y = nullptr;
+        const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
+        e = launch_gemv_mma(l, p->code, ca, d_packed, d_lut, xt, row_words, B, rb0, rb1, partial, ep, s);
+    } else if (use_tc) {
         const int64_t row_bytes = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2);
-        e = use_tc ? launch_gemv_tc(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s)
-                   : launch_gemv_mma(l, p->code, ca, d_packed, d_lut, xt, row_bytes / 4, B, rb0, rb1, partial, s);
+        e = launch_gemv_tc(l, p->code, ca, d_packed, d_lut, xt, row_bytes, B, rb0, rb1, partial, s);
     } else {
         e = launch_gemv_simple(l, p->code, ca, d_packed, d_lut, (const float*)xt, B, rb0, rb1, partial, s);
     }
@@ -270,10 +296,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         g_prof_start = g_prof_stop = nullptr;
     }
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec gemv");
-    if (flags & QTIP_RHT_OUT) {
-        e = launch_reduce(partial, l.n_kc, B, l.m_pad, 0, m, 1.0f, yt, l.m_pad, s);
+    if (rht_out) {
+        if (!fused_reduce) e = launch_reduce(partial, l.n_kc, B, l.m_pad, 0, m, 1.0f, yt, l.m_pad, s);
         if (e == cudaSuccess) e = launch_rht(pm, B, d_sign_m, yt, l.m_pad, d_y, m, 1, scale, s);
-    } else {
+    } else if (!fused_reduce) {
         e = launch_reduce(partial, l.n_kc, B, l.m_pad, row_begin, row_end, scale, d_y, row_end - row_begin, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec epilogue");
@@ -330,3 +356,18 @@ const char* qtip_last_error(void) { return g_err.c_str(); }
 uint64_t qtip_launch_count(void) { return g_launches; }
 
 }  // extern "C"
+
+// Test / profiling hook: per-CTA timelines of the RHT and mma GEMV kernels into buf (u64, see
+// trace.cuh; cap records); buf = NULL turns tracing off.
+// Test / tuning knobs: 1 = fused split-K reduction in the mma GEMV (default 0: measured slower,
+// DESIGN.md).
+extern "C" int qtip_internal_set_knob(int key, int value) {
+    if (key == 1) { g_fused_reduce = value != 0; return 0; }
+    return -1;
+}
+
+extern "C" int qtip_internal_set_cta_trace(void* buf, int cap) {
+    cudaError_t e = qtip::set_cta_trace_rht((unsigned long long*)buf, cap);
+    if (e == cudaSuccess) e = qtip::set_cta_trace_mma((unsigned long long*)buf, cap);
+    return (int)e;
+}

@@ -45,9 +45,11 @@ cudaError_t launch_decode(const Layout& lay, int code, int V, const CodeArgs& ca
 struct RhtPlan {
     int64_t n;
     int b, a;          // n = b * 2^a
-    int a2;            // FWHT length 2^a2 done in-CTA
-    int f;             // mix order n / 2^a2 = b * 2^(a - a2)
-    int rows_per_cta;  // rows of the mix handled per CTA
+    int a2;            // Walsh-Hadamard length L2 = 2^a2 done in registers / shuffles
+    int f;             // order of the dense factor D = H_b (x) H_{2^(a - a2)}, f = n / L2
+    int E;             // columns per lane (L2 / 32, at least 1)
+    int RA;            // rows of D accumulated per lane
+    int rows_per_cta;  // rows of D per CTA (RA * 32 / min(L2, 32))
     const uint32_t* hb;   // device H_b bit rows (nullptr when b == 1)
     const uint32_t* hbt;  // device H_b^T bit rows (inverse transform)
 };
@@ -55,12 +57,13 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan);
 // out[bt][i] = scale * (M v)[i] / sqrt(n) with v = in * s (forward) or in (inverse, then * s).
 // in/out batch strides in elements.  out_mode 0 float32, 1 binary16 duplicated per 32-bit word,
 // 2 binary16; elements [n, pad_to) of every output row are written as zero.
+// zero_ptr[0 .. zero_n) is cleared after the kernel's PDL wait (the GEMV's split-K arrival counters).
 cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
                        void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode = 0,
-                       int64_t pad_to = 0);
+                       int64_t pad_to = 0, int* zero_ptr = nullptr, int zero_n = 0);
 // x (float32) -> out_mode encoding, zero padded to pad_to (used when RHT-in is off).
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
-                           int out_mode, int64_t pad_to, cudaStream_t s);
+                           int out_mode, int64_t pad_to, cudaStream_t s, int* zero_ptr = nullptr, int zero_n = 0);
 
 // Reference (CUDA-core) fused decode-GEMV: partial[kc][b][row] over the row blocks [rb0, rb1).
 cudaError_t launch_gemv_simple(const Layout& lay, int code, const CodeArgs& ca, const void* packed,
@@ -79,11 +82,33 @@ cudaError_t launch_gemv_tc(const Layout& lay, int code, const CodeArgs& ca, cons
 bool gemv_mma_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B);
 int gemv_mma_xt_mode(int code);
 int gemv_mma_batch_pad(int64_t B);
+// Split-K reduction fused in: the last CTA to finish a row block (arrival counter cnt[RB], zero
+// on entry and left zero) writes y[b][i - row_lo] = scale * sum_kc partial[kc][b][i] for the
+// block's rows i in [row_lo, row_hi), in launch_reduce's association (bitwise equal to it).
+struct MmaEpilogue {
+    int* cnt;          // n_rb arrival counters, then the work counter (all zero on entry)
+    int64_t n_rb;
+    float* y;
+    int64_t y_stride;
+    int64_t row_lo, row_hi;
+    float scale;
+};
 cudaError_t launch_gemv_mma(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
                             const void* xt_frag, int64_t xt_row_words, int64_t B, int64_t rb0, int64_t rb1,
-                            float* partial, cudaStream_t s);
+                            float* partial, const MmaEpilogue& ep, cudaStream_t s);
 // y[b][i - row0] = scale * sum_kc partial[kc][b][i] for rows [row0, row1).
 cudaError_t launch_reduce(const float* partial, int64_t n_kc, int64_t B, int64_t m_pad, int64_t row0, int64_t row1,
                           float scale, float* y, int64_t y_stride, cudaStream_t s);
+
+// Row-tile fused decode-GEMV (k_gemv_row.cu, impl 4): one CTA per tile row, no split-K; writes
+// y[b * y_stride + (i - row_lo)] = scale * (W~ x~)[i] for rows i in [row_lo, row_hi).
+bool gemv_row_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B);
+cudaError_t launch_gemv_row(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
+                            const void* xt_frag, int64_t xt_row_words, int64_t B, int64_t row_begin, int64_t row_end,
+                            float* y, int64_t y_stride, int64_t row_lo, int64_t row_hi, float scale, cudaStream_t s);
+
+// Debug CTA timelines (trace.cuh), per translation unit.
+cudaError_t set_cta_trace_rht(unsigned long long* buf, int cap);
+cudaError_t set_cta_trace_mma(unsigned long long* buf, int cap);
 
 }  // namespace qtip

@@ -1,20 +1,24 @@
 // k_rht.cu -- random Hadamard transform kernels.
 //
-// H_n = H_b (x) H_{2^a} (reading R7).  Split 2^a = 2^a1 * 2^a2 (2^a2 <= 256) and write
-// H_n = M_f (x) H_{2^a2} with the "mix" factor M_f = H_b (x) H_{2^a1} of order f = n / 2^a2,
-// M_f[i][j] = H_b[i_b][j_b] * (-1)^popcount(i_a1 & j_a1).
-// One CTA of 256 threads owns R = 256 / 2^a2 rows i of M_f (one output per thread):
-//   1. stage the whole signed input (n floats, coalesced float4) in shared memory,
-//   2. u_i[c] = sum_j M_f[i][j] v_j[c] from shared memory (sign bits of its H_b row in smem),
-//   3. fast Walsh-Hadamard transform of length 2^a2 across the threads: butterflies with
-//      partner distance < 32 via warp shuffles, the rest through shared memory,
-//   4. scale (and the output signs for the inverse), coalesced store.
-// No CTA repeats another's arithmetic; every CTA reads the (L2-resident) input once.
+// H_n = H_b (x) H_{2^a} (reading R7).  With L2 = 2^a2 (a2 = min(a, 8)) write
+// H_n = D (x) H_{L2}, D = H_b (x) H_{2^(a-a2)} the dense factor of order f = n / L2,
+// D[i][j] = H_b[i_b][j_b] * (-1)^popcount(i_1 & j_1).  Viewing v (n) as V[f][L2]:
+//     (H_n v)[i L2 + c] = FWHT_{L2}( sum_j D[i][j] V[j][.] )[c],
+// so a CTA owning rows i of D needs every V[j] once and no other CTA's result.
+// CTA = 8 warps; a lane owns columns c = lane + 32 e (e < E, L2 = 32 E; for L2 < 32 a warp
+// holds 32 / L2 rows side by side) and RA rows of D, and accumulates over its warp's slice of
+// j with FFMA against the CTA's rows of D (+-1.0f, built once in shared memory).  The 8 slices are
+// added in slice order through shared memory (fixed association: deterministic), then the
+// length-L2 Walsh-Hadamard transform runs in registers (bits of e) and warp shuffles (bits of
+// the lane) -- no barrier inside the transform.  The input is read straight from global
+// memory (L2-resident: the previous kernel just wrote it), coalesced 128 B per row segment.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "internal.h"
 #include "tc.cuh"
+#include "trace.cuh"
 
 namespace qtip {
 
@@ -51,137 +55,201 @@ __device__ __forceinline__ uint32_t sign_bit(const uint8_t* __restrict__ s, int6
     return (s[i >> 3] >> (i & 7)) & 1u;
 }
 
+constexpr int kRhtWarps = kRhtThreads / 32;
+
+__device__ unsigned long long* g_rht_trace = nullptr;
+__device__ int g_rht_trace_cap = 0;
+
+template <int E, int RA>
 __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const uint8_t* __restrict__ sign,
                                                            const float* __restrict__ in, int64_t in_stride,
                                                            void* __restrict__ out, int64_t out_stride, int inverse,
-                                                           float out_scale, int out_mode, int64_t pad_to) {
-    extern __shared__ __align__(16) float xs[];             // [n] staged input, then [256] FWHT exchange
-    __shared__ uint32_t hrow[64][32];                        // H_b (or H_b^T) rows of this CTA's rows, bits
+                                                           float out_scale, int out_mode, int64_t pad_to,
+                                                           int* __restrict__ zero_ptr, int zero_n) {
+    extern __shared__ __align__(16) float sm[];
     const int L2 = 1 << plan.a2;
-    const int R = plan.rows_per_cta;                         // rows of M_f per CTA
-    const int RL = R * L2;                                   // outputs per CTA
-    const int S = kRhtThreads / RL;                          // threads (j-slices) per output
-    const int tid = threadIdx.x;
-    const int sl = tid / RL, il = (tid % RL) >> plan.a2, c = tid & (L2 - 1);
-    const int i = blockIdx.x * R + il;                       // row of M_f
+    const int CL = L2 < 32 ? L2 : 32;                        // lanes per row
+    const int rpw = 32 / CL;                                 // rows side by side in a warp
+    const int R = plan.rows_per_cta;                         // = RA * rpw
+    const int f = plan.f;
+    float* Dsm = sm;                                         // [f][R] +-1.0f (row r0 + rl of D, column j)
+    float* red = sm + ((f * R + 3) & ~3);                    // [8][R][L2] slice partial sums
+    uint32_t* ssm = reinterpret_cast<uint32_t*>(red + kRhtWarps * R * L2);   // forward: sign bits, n / 32 words
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int c = lane & (CL - 1), ro = lane / CL;
+    const int r0 = blockIdx.x * R;
     const int64_t bt = blockIdx.y;
-    const int n1 = 1 << (plan.a - plan.a2);
-    const int n = (int)plan.n;
-    const float* x = in + bt * in_stride;
+    const int a1 = plan.a - plan.a2, m1 = (1 << a1) - 1;
+    __shared__ unsigned long long trace_ts[4];
+    CtaTrace trace{trace_ts};
+    trace.entry(g_rht_trace);
 
+    // D rows of this CTA (static tables only: overlaps the previous kernel under PDL)
+    {
+        const uint32_t* hb = inverse ? plan.hbt : plan.hb;
+        const int wpr = (plan.b + 31) >> 5;
+        for (int e = tid; e < f * R; e += kRhtThreads) {
+            const int j = e / R, rl = e % R, r = r0 + rl;
+            float d = 0.0f;
+            if (r < f) {
+                const int ib = r >> a1, jb = j >> a1;
+                uint32_t neg = __popc((r & m1) & (j & m1)) & 1u;
+                if (plan.b > 1) neg ^= (__ldg(hb + ib * wpr + (jb >> 5)) >> (jb & 31)) & 1u;
+                d = neg ? -1.0f : 1.0f;
+            }
+            Dsm[e] = d;
+        }
+    }
+    const bool sign_words = !inverse && CL == 32 && (reinterpret_cast<uintptr_t>(sign) & 3u) == 0;
+    if (sign_words)                                          // n % 32 == 0 here
+        for (int w = tid; w < (int)(plan.n >> 5); w += kRhtThreads) ssm[w] = __ldg(reinterpret_cast<const uint32_t*>(sign) + w);
     ptx::pdl_wait();                                         // the input may be the previous kernel's output
     ptx::pdl_launch_dependents();
-
-    // 1. stage v = (S .) x into shared memory (loads batched 8 deep to overlap their latency)
-    for (int e0 = 4 * tid; e0 < n; e0 += 4 * kRhtThreads * 8) {
-        float4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = e0 + 4 * kRhtThreads * u;
-            if (e < n) v[u] = __ldg(reinterpret_cast<const float4*>(x + e));
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = e0 + 4 * kRhtThreads * u;
-            if (e < n) {
-                if (!inverse) {
-                    const uint32_t sb = (sign[e >> 3] >> (e & 7)) & 0xFu;   // e % 4 == 0: four bits of one byte
-                    v[u].x = (sb & 1u) ? -v[u].x : v[u].x;
-                    v[u].y = (sb & 2u) ? -v[u].y : v[u].y;
-                    v[u].z = (sb & 4u) ? -v[u].z : v[u].z;
-                    v[u].w = (sb & 8u) ? -v[u].w : v[u].w;
-                }
-                *reinterpret_cast<float4*>(xs + e) = v[u];
-            }
-        }
-    }
-    if (plan.b > 1) {
-        const int wpr = (plan.b + 31) >> 5;
-        for (int e = tid; e < R * wpr; e += kRhtThreads) {
-            const int rl = e / wpr, w = e % wpr;
-            const int ib = min(blockIdx.x * R + rl, plan.f - 1) / n1;
-            hrow[rl][w] = (inverse ? plan.hbt : plan.hb)[ib * wpr + w];
-        }
-    }
+    trace.waited(g_rht_trace);
+    if (blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = tid; i < zero_n; i += kRhtThreads) zero_ptr[i] = 0;
     __syncthreads();
 
-    // 2. mix: u = sum_j M_f[i][j] v[j][c], the j-sum split over S slices (j_b = sl mod S)
-    //    that are added in slice order (a fixed association: deterministic)
-    float acc = 0.0f;
-    if (i < plan.f) {
-        const int ia = i & (n1 - 1);
-        for (int jb = sl; jb < plan.b; jb += S) {
-            const uint32_t sb = (plan.b > 1) ? ((hrow[il][jb >> 5] >> (jb & 31)) & 1u) : 0u;
-#pragma unroll 4
-            for (int ja = 0; ja < n1; ++ja) {
-                const uint32_t neg = sb ^ (__popc(ia & ja) & 1u);
-                const float v = xs[(jb * n1 + ja) * L2 + c];
-                acc += __int_as_float(__float_as_int(v) ^ (neg << 31));
+    // slice sums: acc[q][e] = sum_{j in slice} D[r0 + ro RA + q][j] V[j][c + 32 e]
+    float acc[RA][E];
+#pragma unroll
+    for (int q = 0; q < RA; ++q)
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[q][e] = 0.0f;
+    const float* x = in + bt * in_stride;
+    const int j_lo = f * warp / kRhtWarps, j_hi = f * (warp + 1) / kRhtWarps;
+    // loads of U rows are issued together before their FMAs (the latency is L2's, ~U x fewer round trips)
+    constexpr int U = E >= 4 ? 2 : 8;
+    auto slice = [&](auto kind) {
+        constexpr int K = decltype(kind)::value;             // 0 plain, 1 sign words, 2 sign bytes
+        const float* xp = x + (int64_t)j_lo * L2 + c;
+        int j = j_lo;
+        auto step = [&](const float (&v)[E], int jj) {
+            const float* d = Dsm + jj * R + ro * RA;
+#pragma unroll
+            for (int q = 0; q < RA; ++q) {
+                const float dq = d[q];
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc[q][e] = fmaf(dq, v[e], acc[q][e]);
+            }
+        };
+        auto load = [&](float (&v)[E], int jj) {
+            const float* p = xp + (int64_t)(jj - j_lo) * L2;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                v[e] = __ldg(p + 32 * e);
+                if constexpr (K == 1) {
+                    const uint32_t w = ssm[((jj * L2) >> 5) + e];
+                    v[e] = __int_as_float(__float_as_int(v[e]) ^ ((w << (31 - lane)) & 0x80000000u));
+                } else if constexpr (K == 2) {
+                    if (sign_bit(sign, (int64_t)jj * L2 + c + 32 * e)) v[e] = -v[e];
+                }
+            }
+        };
+        for (; j + U <= j_hi; j += U) {
+            float v[U][E];
+#pragma unroll
+            for (int u = 0; u < U; ++u) load(v[u], j + u);
+#pragma unroll
+            for (int u = 0; u < U; ++u) step(v[u], j + u);
+        }
+        for (; j < j_hi; ++j) {
+            float v[E];
+            load(v, j);
+            step(v, j);
+        }
+    };
+    if (inverse) slice(std::integral_constant<int, 0>{});
+    else if (sign_words) slice(std::integral_constant<int, 1>{});
+    else slice(std::integral_constant<int, 2>{});
+#pragma unroll
+    for (int q = 0; q < RA; ++q)
+#pragma unroll
+        for (int e = 0; e < E; ++e) red[(warp * R + ro * RA + q) * L2 + c + 32 * e] = acc[q][e];
+    __syncthreads();
+
+    // rows ro RA + q of pass `warp` (RA passes): sum the 8 slices in order, FWHT, store
+    if (warp < RA) {
+        const int q = warp;
+        const int rl = ro * RA + q, r = r0 + rl;
+        float u[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            float t = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kRhtWarps; ++w) t += red[(w * R + rl) * L2 + c + 32 * e];
+            u[e] = t;
+        }
+        // butterflies on the column bits held by the lane (distance < CL): shuffles
+        for (int h = 1; h < CL; h <<= 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const float o = __shfl_xor_sync(0xffffffffu, u[e], h);
+                u[e] = (c & h) ? (o - u[e]) : (u[e] + o);
             }
         }
-    }
-    __syncthreads();                                         // xs is reused below
-    if (S > 1) {
-        xs[tid] = acc;
-        __syncthreads();
-        if (tid < RL) {
-            acc = 0.0f;
-            for (int q = 0; q < S; ++q) acc += xs[q * RL + tid];
+        // butterflies on the bits of e (distance 32, 64, ...): in registers
+#pragma unroll
+        for (int h = 1; h < E; h <<= 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (!(e & h)) {
+                    const float lo = u[e], hi = u[e | h];
+                    u[e] = lo + hi;
+                    u[e | h] = lo - hi;
+                }
         }
-        __syncthreads();
-    }
-    // 3. FWHT of length L2 along c (threads < R L2 hold the values; all threads run the loop so the
-    //    shuffles and barriers stay uniform): lower index of a pair gets u + v, upper gets u - v
-    for (int h = 1; h < L2; h <<= 1) {
-        float other;
-        if (h < 32) {
-            other = __shfl_xor_sync(0xffffffffu, acc, h);
-        } else {
-            xs[tid] = acc;
-            __syncthreads();
-            other = xs[tid ^ h];
-            __syncthreads();
+        if (r < f) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int64_t idx = (int64_t)r * L2 + c + 32 * e;
+                float o = u[e] * out_scale;
+                if (inverse && sign_bit(sign, idx)) o = -o;
+                store_out(out, out_mode, bt * out_stride, idx, o);
+            }
         }
-        acc = (c & h) ? (other - acc) : (acc + other);
-    }
-    // 4. scale (and signs for the inverse), store
-    if (sl == 0 && i < plan.f) {
-        const int64_t e = (int64_t)i * L2 + c;
-        float v = acc * out_scale;
-        if (inverse && sign_bit(sign, e)) v = -v;
-        store_out(out, out_mode, bt * out_stride, e, v);
     }
     if (blockIdx.x == 0)                                     // zero the padded tail [n, pad_to)
         for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt * out_stride, e, 0.0f);
+    trace.exit(g_rht_trace, inverse ? 2 : 1, g_rht_trace_cap);
 }
 
 __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t in_stride, void* __restrict__ out,
-                               int64_t out_stride, int out_mode, int64_t pad_to) {
+                               int64_t out_stride, int out_mode, int64_t pad_to, int* __restrict__ zero_ptr, int zero_n) {
     const int64_t bt = blockIdx.y;
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
+    if (blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = threadIdx.x; i < zero_n; i += blockDim.x) zero_ptr[i] = 0;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pad_to; e += (int64_t)gridDim.x * blockDim.x)
         store_out(out, out_mode, bt * out_stride, e, e < n ? in[bt * in_stride + e] : 0.0f);
 }
 
-constexpr int64_t kRhtMaxN = 48 * 1024;                      // staged input <= 192 KB of shared memory
+constexpr int64_t kRhtMaxN = 48 * 1024;
 
 cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
     int b, a;
     if (!hadamard_factor(n, &b, &a)) return cudaErrorInvalidValue;
-    if (n > kRhtMaxN || n % 4) return cudaErrorInvalidValue;
+    if (n > kRhtMaxN) return cudaErrorInvalidValue;
     plan->n = n;
     plan->b = b;
     plan->a = a;
+    // a2 = 5 (one column per lane, the whole transform tail in 5 shuffles, 4 rows per lane) while
+    // the dense factor stays small; longer Walsh-Hadamard factors otherwise (less L2 re-reading)
     plan->a2 = a < 8 ? a : 8;
-    plan->f = (int)(n >> plan->a2);
-    // at least one warp of outputs per CTA, at most ~2 waves of CTAs; the rest of the 256
-    // threads split each output's j-sum
+    if (a >= 5 && (n >> 5) <= 512) plan->a2 = 5;
     const int L2 = 1 << plan->a2;
-    int R = std::max(1, 32 / L2);
-    while ((plan->f + R - 1) / R > 296 && R * L2 < kRhtThreads) R *= 2;
-    plan->rows_per_cta = R;
-    if (R * L2 > kRhtThreads || R > 64 || kRhtThreads % (R * L2)) return cudaErrorInvalidValue;
+    plan->f = (int)(n >> plan->a2);
+    plan->E = L2 >= 32 ? L2 / 32 : 1;
+    const int rpw = L2 >= 32 ? 1 : 32 / L2;
+    // rows per lane: amortise the D loads, but keep at least ~one CTA per SM when f allows
+    int RA = 1;
+    if (plan->E <= 2) {
+        RA = 4;
+        while (RA > 1 && (plan->f + RA * rpw - 1) / (RA * rpw) < 128) RA /= 2;
+    }
+    plan->RA = RA;
+    plan->rows_per_cta = RA * rpw;
     plan->hb = plan->hbt = nullptr;
     if (b > 1) {
         cudaError_t err = cudaSuccess;
@@ -193,29 +261,52 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
     return cudaSuccess;
 }
 
-cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
-                       void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode,
-                       int64_t pad_to) {
-    dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B);
-    const float out_scale = (float)(scale / std::sqrt((double)plan.n));
-    const int64_t pad = pad_to < plan.n ? plan.n : pad_to;
-    const size_t smem = (size_t)std::max<int64_t>(plan.n, kRhtThreads) * sizeof(float);
+template <int E, int RA>
+static cudaError_t launch_rht_t(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in,
+                                int64_t in_stride, void* out, int64_t out_stride, int inverse, float out_scale,
+                                cudaStream_t s, int out_mode, int64_t pad, int* zero_ptr, int zero_n) {
+    const int L2 = 1 << plan.a2;
+    const size_t smem = sizeof(float) * ((size_t)((plan.f * plan.rows_per_cta + 3) & ~3) +
+                                         (size_t)kRhtWarps * plan.rows_per_cta * L2 + (size_t)(plan.n >> 5));
+    auto kern = rht_kernel<E, RA>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(rht_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kRhtMaxN * sizeof(float)));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    cudaError_t e = launch_pdl(rht_kernel, grid, dim3(kRhtThreads), smem, s, plan, sign, in, in_stride, out,
-                               out_stride, inverse, out_scale, out_mode, pad);
+    dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B);
+    return launch_pdl(kern, grid, dim3(kRhtThreads), smem, s, plan, sign, in, in_stride, out, out_stride, inverse,
+                      out_scale, out_mode, pad, zero_ptr, zero_n);
+}
+
+cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
+                       void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode,
+                       int64_t pad_to, int* zero_ptr, int zero_n) {
+    const float out_scale = (float)(scale / std::sqrt((double)plan.n));
+    const int64_t pad = pad_to < plan.n ? plan.n : pad_to;
+    cudaError_t e = cudaErrorInvalidValue;
+#define QTIP_RHT_CASE(EE, RR) \
+    if (plan.E == EE && plan.RA == RR) e = launch_rht_t<EE, RR>(plan, B, sign, in, in_stride, out, out_stride, inverse, out_scale, s, out_mode, pad, zero_ptr, zero_n);
+    QTIP_RHT_CASE(1, 1) QTIP_RHT_CASE(1, 2) QTIP_RHT_CASE(1, 4) QTIP_RHT_CASE(2, 1) QTIP_RHT_CASE(2, 2)
+    QTIP_RHT_CASE(2, 4) QTIP_RHT_CASE(4, 1) QTIP_RHT_CASE(8, 1)
+#undef QTIP_RHT_CASE
     count_launch(1);
     return e;
 }
 
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
-                           int out_mode, int64_t pad_to, cudaStream_t s) {
+                           int out_mode, int64_t pad_to, cudaStream_t s, int* zero_ptr, int zero_n) {
     dim3 grid((unsigned)std::min<int64_t>((pad_to + 255) / 256, 1024), (unsigned)B);
-    cudaError_t e = launch_pdl(convert_kernel, grid, dim3(256), 0, s, in, n, in_stride, out, out_stride, out_mode, pad_to);
+    cudaError_t e = launch_pdl(convert_kernel, grid, dim3(256), 0, s, in, n, in_stride, out, out_stride, out_mode, pad_to,
+                               zero_ptr, zero_n);
     count_launch(1);
+    return e;
+}
+
+cudaError_t set_cta_trace_rht(unsigned long long* buf, int cap) {
+    cudaError_t e = cudaMemcpyToSymbol(g_rht_trace, &buf, sizeof(buf));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_rht_trace_cap, &cap, sizeof(cap));
     return e;
 }
 

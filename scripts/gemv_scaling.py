@@ -9,6 +9,8 @@ code = sys.argv[1] if len(sys.argv) > 1 else "3inst"
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 impl = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 qtip.set_matvec_impl(impl)
+fused = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+qtip.load().qtip_internal_set_knob(1, fused)
 qtip.set_pdl(False)                   # isolate the GEMV kernel in the event timing
 n = 4096
 for m in [128, 1024, 4736, 9472, 18944, 37888]:
@@ -25,4 +27,4 @@ for m in [128, 1024, 4736, 9472, 18944, 37888]:
         ts.append(a.elapsed_time(b) * 1e3)
     units = (m // 128) * (n // 128)
     t = float(np.median(ts))
-    print(f"impl={impl} {code} k={k} m={m:6d} units={units:5d} per_cta={units/148:6.2f} gemv_us={t:8.2f} GB/s={m*n*k/8/t/1e3:8.1f}", flush=True)
+    print(f"impl={impl} fused={fused} {code} k={k} m={m:6d} units={units:5d} per_cta={units/148:6.2f} gemv_us={t:8.2f} GB/s={m*n*k/8/t/1e3:8.1f}", flush=True)
