@@ -98,13 +98,17 @@ qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* 
 
 #define QTIP_RHT_IN  1  /* apply x~ = H_n S_n x / sqrt(n) before the product               */
 #define QTIP_RHT_OUT 2  /* apply y = S_m H_m^T y~ / sqrt(m) after it (needs all m rows)    */
+#define QTIP_XT_READY 4 /* kernel benchmarking: reuse the x~ left in d_workspace by the previous
+                           call with the same (p, m, n, B, workspace) instead of transforming
+                           d_x again (d_x and d_sign_n are then ignored)                     */
 
 /* Fused decode + matrix-vector product, batch B (<= 64):
  *     d_y[b][i - row_begin] = scale * (S_m H_m^T W~ H_n S_n x_b)[i],  i in [row_begin, row_end)
  *   d_x: DEVICE float32 [B][n];  d_y: DEVICE float32 [B][row_end - row_begin].
  *   d_sign_n / d_sign_m: DEVICE bit-packed signs (element i negative iff bit (i&7) of byte
  *     i>>3 is set), ceil(n/8) / ceil(m/8) bytes; ignored when the matching flag is off.
- *   flags: QTIP_RHT_IN | QTIP_RHT_OUT.  Without RHT_OUT the result is scale * W~ x~.
+ *   flags: QTIP_RHT_IN | QTIP_RHT_OUT (| QTIP_XT_READY).  Without RHT_OUT the result is
+ *     scale * W~ x~.
  *     A partial row range (row_begin > 0 or row_end < m) requires RHT_OUT off; row_begin
  *     and row_end must be multiples of 128 (or row_end == m).
  *   d_workspace: DEVICE scratch of >= qtip_matvec_workspace_bytes(...) bytes, 256-B aligned.
@@ -121,7 +125,8 @@ size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, i
 /* Random Hadamard transform of B vectors of length n:
  *   inverse = 0:  out = H_n (S . in) / sqrt(n)
  *   inverse = 1:  out = S . (H_n^T in) / sqrt(n)
- * d_in, d_out: DEVICE float32 [B][n]; in-place allowed. */
+ * d_in, d_out: DEVICE float32 [B][n], distinct buffers (out-of-place; d_in == d_out is
+ * QTIP_ERR_INVALID_PARAMS). */
 qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d_in, float* d_out,
                      int inverse, void* stream);
 

@@ -199,12 +199,21 @@ qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* 
 
 static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
+// Profile events also work inside CUDA-graph capture (as external event-record nodes).
+static void record_event(cudaEvent_t ev, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(ev, s);
+}
+
 size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B) {
     if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1) return 0;
     const Layout l = make_layout(m, n, p->k);
     const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);       // x~ rows (mma kernel pads the batch)
     return align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad) +
-           align256(4 * (l.m_pad / kCellRows + 1));
+           align256(4 * (l.m_pad / kCellRows + 2));
 }
 
 qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, const void* d_packed,
@@ -215,10 +224,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if (st != QTIP_OK) return st;
     if ((st = check_shape(m, n)) != QTIP_OK) return st;
     if (B < 1 || B > 64) return fail(QTIP_ERR_INVALID_PARAMS, "batch must be in 1..64");
-    if (flags & ~(QTIP_RHT_IN | QTIP_RHT_OUT)) return fail(QTIP_ERR_INVALID_PARAMS, "unknown flags");
+    if (flags & ~(QTIP_RHT_IN | QTIP_RHT_OUT | QTIP_XT_READY)) return fail(QTIP_ERR_INVALID_PARAMS, "unknown flags");
     if (!d_packed || !d_x || !d_y || !d_workspace || (p->code == QTIP_CODE_HYB && !d_lut))
         return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
-    if (((flags & QTIP_RHT_IN) && !d_sign_n) || ((flags & QTIP_RHT_OUT) && !d_sign_m))
+    if (((flags & QTIP_RHT_IN) && !(flags & QTIP_XT_READY) && !d_sign_n) || ((flags & QTIP_RHT_OUT) && !d_sign_m))
         return fail(QTIP_ERR_INVALID_PARAMS, "NULL sign vector");
     if (row_begin < 0 || row_end > m || row_begin >= row_end) return fail(QTIP_ERR_SHAPE, "bad row range");
     if (row_begin % kCellRows || (row_end % kCellRows && row_end != m))
@@ -230,7 +239,7 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const size_t need = qtip_matvec_workspace_bytes(p, m, n, B);
     if (workspace_bytes < need) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
     RhtPlan pn{}, pm{};
-    if ((flags & QTIP_RHT_IN) && make_rht_plan(n, &pn) != cudaSuccess)
+    if ((flags & QTIP_RHT_IN) && !(flags & QTIP_XT_READY) && make_rht_plan(n, &pn) != cudaSuccess)
         return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
     if ((flags & QTIP_RHT_OUT) && make_rht_plan(m, &pm) != cudaSuccess)
         return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
@@ -246,7 +255,13 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if (g_impl == 3 && !mma_ok) return fail(QTIP_ERR_UNSUPPORTED, "mma kernel: needs 2 <= k <= 4, B <= 16, one-sign HYB");
     if (g_impl == 4 && !row_ok) return fail(QTIP_ERR_UNSUPPORTED, "row kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB");
     int impl = g_impl;
-    if (impl == 0) impl = mma_ok ? 3 : (tc_ok ? 2 : 1);
+    if (impl == 0) {
+        // measured: the row-tile kernel wins while its CTAs (one per 16 rows,
+        // 8-16 warps each) fill the GPU in one wave; beyond that the split-K kernel balances better
+        const int64_t tile_rows = (row_end - row_begin + kTile - 1) / kTile;
+        if (row_ok && tile_rows <= 4 * (int64_t)num_sms()) impl = 4;
+        else impl = mma_ok ? 3 : (tc_ok ? 2 : 1);
+    }
     const bool use_tc = impl == 2, use_mma = impl == 3, use_row = impl == 4;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
@@ -259,12 +274,13 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const int xmode = (use_mma || use_row) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
     cudaError_t e;
     // the input kernel also clears the GEMV's split-K arrival counters (workspace is caller memory)
-    if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 1);
-    else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s, cnt, n_rb + 1);
+    if (flags & QTIP_XT_READY) e = cudaSuccess;          // counters are left zero by every GEMV
+    else if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 2);
+    else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s, cnt, n_rb + 2);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
     const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
     const bool prof = g_prof_start && g_prof_stop;
-    if (prof) cudaEventRecord(g_prof_start, s);
+    if (prof) record_event(g_prof_start, s);
     const bool rht_out = (flags & QTIP_RHT_OUT) != 0;
     const bool fused_reduce = use_row || (use_mma && g_fused_reduce);
     if (use_row) {
@@ -292,7 +308,7 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         e = launch_gemv_simple(l, p->code, ca, d_packed, d_lut, (const float*)xt, B, rb0, rb1, partial, s);
     }
     if (prof) {
-        cudaEventRecord(g_prof_stop, s);
+        record_event(g_prof_stop, s);
         g_prof_start = g_prof_stop = nullptr;
     }
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec gemv");
@@ -369,5 +385,6 @@ extern "C" int qtip_internal_set_knob(int key, int value) {
 extern "C" int qtip_internal_set_cta_trace(void* buf, int cap) {
     cudaError_t e = qtip::set_cta_trace_rht((unsigned long long*)buf, cap);
     if (e == cudaSuccess) e = qtip::set_cta_trace_mma((unsigned long long*)buf, cap);
+    if (e == cudaSuccess) e = qtip::set_cta_trace_row((unsigned long long*)buf, cap);
     return (int)e;
 }

@@ -110,5 +110,6 @@ cudaError_t launch_gemv_row(const Layout& lay, int code, const CodeArgs& ca, con
 // Debug CTA timelines (trace.cuh), per translation unit.
 cudaError_t set_cta_trace_rht(unsigned long long* buf, int cap);
 cudaError_t set_cta_trace_mma(unsigned long long* buf, int cap);
+cudaError_t set_cta_trace_row(unsigned long long* buf, int cap);
 
 }  // namespace qtip

@@ -217,6 +217,17 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : 6) g
             if (threadIdx.x == 0) args.ep.cnt[RB] = 0;                // left zero for the next call
         }
     }
+    // the last CTA to leave resets the work counter and the exit counter: every launch (and the
+    // next one, which reads them only after its PDL wait) starts from zero
+    if (threadIdx.x == 0) {
+        int* work = args.ep.cnt + args.ep.n_rb;
+        int old;
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(work + 1) : "memory");
+        if (old == (int)G - 1) {
+            work[0] = 0;
+            work[1] = 0;
+        }
+    }
     trace.exit(g_mma_trace, 3 | (j << 8), g_mma_trace_cap);
 }
 

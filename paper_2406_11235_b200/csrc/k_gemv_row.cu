@@ -12,17 +12,23 @@
 // no CTA-wide barrier until the final sum.  The packed weights do not depend on the previous
 // kernel, so the first stages are requested before the PDL wait and stream in while the RHT-in
 // still runs; only the x~ copies wait for it.
+#include <algorithm>
+
 #include "internal.h"
 #include "mma_tile.cuh"
 #include "tc.cuh"
+#include "trace.cuh"
 
 namespace qtip {
 namespace {
 
 using namespace mma;
 
-constexpr int kRowWarps = 8;
+constexpr int kRowMaxWarps = 16;
 constexpr int kRowMaxStages = 4;
+
+__device__ unsigned long long* g_row_trace = nullptr;
+__device__ int g_row_trace_cap = 0;
 
 struct RowArgs {
     const uint32_t* packed;
@@ -41,8 +47,10 @@ struct RowArgs {
     float scale;
 };
 
+// W = blockDim.x / 32 warps per tile row (16, 8 or 4: the launcher picks the widest that keeps
+// every CTA resident in one wave); registers are capped at 64 so two 16-warp CTAs fit an SM.
 template <int K, int CODE, bool kImm>
-__global__ void __launch_bounds__(32 * kRowWarps, 3) gemv_row_kernel(const RowArgs args) {
+__global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const RowArgs args) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
     constexpr int TW = 8 * K;
@@ -51,17 +59,21 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) gemv_row_kernel(const RowAr
     const int S = args.stages;
     const uint32_t stage_bytes = kChunkBytes + kXRowBytes * (uint32_t)args.B;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = blockDim.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
     const int64_t n_kc = args.lay.n_kc;
     const int64_t I = args.tile_row0 + blockIdx.x;                  // tile row
     const int64_t RB = I / kCellTileRows, Il = I % kCellTileRows;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem) + warp * kRowMaxStages;
-    float* red = reinterpret_cast<float*>(smem + 8 * kRowWarps * kRowMaxStages);   // [W][16][B]
-    uint8_t* ring = smem + 8 * kRowWarps * kRowMaxStages + 4 * kRowWarps * kTile * args.B;
+    float* red = reinterpret_cast<float*>(smem + 8 * kRowMaxWarps * kRowMaxStages);   // [W][16][B]
+    uint8_t* ring = smem + 8 * kRowMaxWarps * kRowMaxStages + 4 * kRowMaxWarps * kTile * args.B;
     ring += (size_t)warp * S * stage_bytes;
     const CodeArgs ca = args.ca;
     const Lcg<CODE, kImm> lcg(ca);
-    const int ncells = (int)((n_kc - warp + kRowWarps - 1) / kRowWarps);   // cells warp, warp + W, ...
+    const int ncells = (int)((n_kc - warp + W - 1) / W);                   // cells warp, warp + W, ...
+    __shared__ unsigned long long trace_ts[4];
+    CtaTrace trace{trace_ts};
+    trace.entry(g_row_trace);
 
     if (lane == 0) {
         for (int st = 0; st < S; ++st) ptx::mbar_init(ptx::smem_u32(full + st), 1);
@@ -70,7 +82,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) gemv_row_kernel(const RowAr
     __syncwarp();
     auto issue_w = [&](int j) {                                      // lane 0: packed chunk of cell j
         const int st = j % S;
-        const int64_t kc = warp + (int64_t)j * kRowWarps;
+        const int64_t kc = warp + (int64_t)j * W;
         const uint32_t bar = ptx::smem_u32(full + st);
         ptx::mbar_arrive_expect_tx(bar, stage_bytes);
         ptx::bulk_g2s(ptx::smem_u32(ring + st * stage_bytes),
@@ -78,7 +90,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) gemv_row_kernel(const RowAr
     };
     auto issue_x = [&](int j) {                                      // lane 0: x~ columns of cell j
         const int st = j % S;
-        const int64_t kc = warp + (int64_t)j * kRowWarps;
+        const int64_t kc = warp + (int64_t)j * W;
         for (int n = 0; n < args.B; ++n)
             ptx::bulk_g2s(ptx::smem_u32(ring + st * stage_bytes + kChunkBytes + n * kXRowBytes),
                           reinterpret_cast<const uint8_t*>(args.xt) + n * args.xt_row_words * 4 + kc * kXRowBytes,
@@ -88,6 +100,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) gemv_row_kernel(const RowAr
         for (int j = 0; j < min(ncells, S); ++j) issue_w(j);
     ptx::pdl_wait();
     ptx::pdl_launch_dependents();
+    trace.waited(g_row_trace);
     if (lane == 0)
         for (int j = 0; j < min(ncells, S); ++j) issue_x(j);
 
@@ -118,34 +131,53 @@ __global__ void __launch_bounds__(32 * kRowWarps, 3) gemv_row_kernel(const RowAr
         if (b < args.B) red[(warp * kTile + r) * args.B + b] = acc[0][e];
     }
     __syncthreads();
+    trace.aux(g_row_trace, 1);
     for (int t = threadIdx.x; t < kTile * args.B; t += blockDim.x) {
         const int r = t % kTile, b = t / kTile;
         const int64_t i = I * kTile + r;
         if (i < args.row_lo || i >= args.row_hi) continue;
         float s = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kRowWarps; ++w) s += red[(w * kTile + r) * args.B + b];
+        for (int w = 0; w < W; ++w) s += red[(w * kTile + r) * args.B + b];
         args.y[b * args.y_stride + (i - args.row_lo)] = args.scale * (s * args.code_factor);
     }
+    trace.exit(g_row_trace, 4, g_row_trace_cap);
 }
 
 template <int K, int CODE, bool kImm>
 cudaError_t launch_row_t(RowArgs a, int64_t tile_rows, cudaStream_t s) {
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
+    auto kern = gemv_row_kernel<K, CODE, kImm>;
     const size_t stage = 256u * K + (kHyb ? 256u : 512u) * (size_t)a.B;
-    const size_t fixed = 8 * kRowWarps * kRowMaxStages + 4 * kRowWarps * kTile * (size_t)a.B;
-    // ring depth: as deep as fits ~72 KB per CTA (three CTAs per SM), at least 2
-    int S = (int)((72 * 1024 - fixed) / (kRowWarps * stage));
+    const size_t fixed = 8 * kRowMaxWarps * kRowMaxStages + 4 * kRowMaxWarps * kTile * (size_t)a.B;
+    // widest W whose CTAs all fit in one wave (per-SM CTA count from registers / threads, and a
+    // shared-memory share of 227 KB / CTAs); ring depth as deep as that share allows (2..4)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    const int regs = fa.numRegs > 0 ? fa.numRegs : 64;
+    int W = 4, per_sm = 1;
+    for (int w : {16, 8, 4}) {
+        per_sm = std::min(65536 / (regs * 32 * w), 2048 / (32 * w));
+        W = w;
+        if ((int64_t)per_sm * num_sms() >= tile_rows) break;
+    }
+    const size_t share = std::min<size_t>(227 * 1024 / std::max(per_sm, 1), 200 * 1024);
+    int S = (int)((share - fixed) / (W * stage));
     S = S < 2 ? 2 : (S > kRowMaxStages ? kRowMaxStages : S);
     a.stages = S;
-    const size_t smem = fixed + (size_t)kRowWarps * S * stage;
-    auto kern = gemv_row_kernel<K, CODE, kImm>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = fixed + (size_t)W * S * stage;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(kern, dim3((unsigned)tile_rows), dim3(32 * kRowWarps), smem, s, a);
+    return launch_pdl(kern, dim3((unsigned)tile_rows), dim3(32 * W), smem, s, a);
 }
 
 }  // namespace
+
+cudaError_t set_cta_trace_row(unsigned long long* buf, int cap) {
+    cudaError_t e = cudaMemcpyToSymbol(g_row_trace, &buf, sizeof(buf));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_row_trace_cap, &cap, sizeof(cap));
+    return e;
+}
 
 bool gemv_row_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B) {
     if (B < 1 || B > 4) return false;

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libqtip.so")
 QTIP_CODE_1MAD, QTIP_CODE_3INST, QTIP_CODE_HYB = 1, 2, 3
 CODES = {"1mad": QTIP_CODE_1MAD, "3inst": QTIP_CODE_3INST, "hyb": QTIP_CODE_HYB}
 QTIP_RHT_IN, QTIP_RHT_OUT = 1, 2
+QTIP_XT_READY = 4          # kernel benchmarking: reuse the x~ already in the workspace
 IMPL_AUTO, IMPL_SIMPLE, IMPL_TC, IMPL_MMA = 0, 1, 2, 3
 
 STATUS = {0: "QTIP_OK", -1: "QTIP_ERR_INVALID_PARAMS", -2: "QTIP_ERR_SHAPE", -3: "QTIP_ERR_INVALID_PATH",

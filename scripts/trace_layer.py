@@ -59,7 +59,7 @@ b = buf.cpu().numpy()
 cnt = min(int(b[0]), CAP)
 r = b[1:1 + 8 * cnt].reshape(cnt, 8).astype(np.int64)
 t_ref = r[:, 3].min()
-names = {1: "rht_in", 2: "rht_out", 3: "gemv"}
+names = {1: "rht_in", 2: "rht_out", 3: "gemv", 4: "gemv_row"}
 units = r[:, 0] >> 8                        # gemv: cells processed by the CTA
 r[:, 0] &= 0xFF
 # split each kind's records into launches at gaps between sorted entry times
@@ -76,8 +76,8 @@ for t0, tag, p in sorted(out, key=lambda z: z[0]):
     print(f"  {names.get(int(tag), tag):8s} ctas={len(p):5d} entry {e.min():7.2f}..{e.max():7.2f}  "
           f"wait-release {w.min():7.2f}/{np.median(w):7.2f}/{w.max():7.2f}  "
           f"exit {x_.min():7.2f}/{np.median(x_):7.2f}/{x_.max():7.2f}  sms={len(set(p[:, 2]))}"
-          + (f"  cells/cta {p[:, 8].min()}..{p[:, 8].max()} (sum {p[:, 8].sum()})" if tag == 3 else ""))
-    if tag == 3:
+          + (f"  cells/cta {p[:, 8].min()}..{p[:, 8].max()} (sum {p[:, 8].sum()})" if tag in (3, 4) else ""))
+    if tag in (3, 4):
         late = p[np.argsort(p[:, 5])[-5:]]
         for z in late:
             red = f" last reduce RB {z[7]-1} at {(z[6]-t_ref)/1e3:7.2f}" if z[7] else ""
