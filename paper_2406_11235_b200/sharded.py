@@ -39,6 +39,24 @@ def gather_order(slots, m, world):
     return np.array(idx, dtype=np.int64)
 
 
+def gather_rows(send, recv, world, m, group=None, out=None):
+    """The exchange step: every rank's padded y~ slice send [B, slot] -> y~ [B, m] in row order on
+    every rank (one all_gather_into_tensor; NCCL on GPUs, gloo in the CPU tests).  recv is the
+    [world, B, slot] staging buffer; out (optional) receives the reordered rows."""
+    import torch
+    import torch.distributed as dist
+    B, slot = send.shape
+    dist.all_gather_into_tensor(recv.view(-1), send.reshape(-1), group=group)
+    if B == 1 and slot * world == m:
+        return recv.view(1, m)                                           # already in row order
+    idx = torch.from_numpy(gather_order(slot, m, world)).to(send.device)
+    rows = recv.permute(1, 0, 2).reshape(B, -1).index_select(1, idx)    # drop padding, reorder
+    if out is None:
+        return rows
+    out.copy_(rows)
+    return out
+
+
 class ShardedQTIPLinear:
     """One rank's part of a row-sharded layer.  `group` is a torch.distributed process group."""
 
@@ -76,7 +94,6 @@ class ShardedQTIPLinear:
         return self._bufs[B]
 
     def forward(self, x):
-        import torch.distributed as dist
         from . import qtip
         B = x.shape[0]
         send, recv, yt, y, idx, tmp = self._buffers(B)
@@ -86,12 +103,7 @@ class ShardedQTIPLinear:
         else:
             self.local.forward(x, out=tmp, flags=qtip.QTIP_RHT_IN)
             send[:, :rows].copy_(tmp)
-        dist.all_gather_into_tensor(recv.view(-1), send.view(-1), group=self.group)
-        if B == 1 and self.slot * self.world == self.m:
-            src = recv.view(1, self.m)                                       # already in row order
-        else:
-            yt.copy_(recv.permute(1, 0, 2).reshape(B, -1).index_select(1, idx))   # drop padding, reorder
-            src = yt
+        src = gather_rows(send, recv, self.world, self.m, group=self.group, out=yt)
         qtip.qtip_rht(self.m, B, self.sign_m, src, y, inverse=True)          # S_m H_m^T y~ / sqrt(m)
         return y
 

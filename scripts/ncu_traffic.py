@@ -16,7 +16,7 @@ import subprocess
 import sys
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
-         "second": 1.0, "%": 1.0, "": 1.0}
+         "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "%": 1.0, "": 1.0}
 
 
 def raw(report):
@@ -69,9 +69,19 @@ def main():
     report, key = sys.argv[1], sys.argv[2]
     path = sys.argv[3] if len(sys.argv) > 3 else os.path.join(os.path.dirname(__file__), "..", "profiles",
                                                               "traffic.json")
-    summ = summarise(raw(report))
+    recs = raw(report)
+    summ = summarise(recs)
+    # all GEMV launches of the capture together (the bench's per-launch average runs over the
+    # step's mix of kernels)
+    g = [d for d in recs if "gemv" in d["Kernel Name"]]
+    if g:
+        tot = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0) for d in g)
+        dur = sum(d["gpu__time_duration.sum"] for d in g)
+        summ["all_gemv"] = {"launches": len(g), "dram_bytes_per_launch": tot / len(g),
+                            "duration_us": dur / len(g) * 1e6, "dram_GBps": tot / dur / 1e9,
+                            "kernels": sorted(set(d["Kernel Name"].split("(")[0] for d in g))}
     print(json.dumps(summ, indent=1))
-    gemv = [v for k, v in summ.items() if "gemv" in k]
+    gemv = [summ["all_gemv"]] if g else []
     if gemv:
         try:
             with open(path) as f:

@@ -224,3 +224,33 @@ def test_launch_counter_counts_kernels(cuda_lib):
     layer(x)
     torch.cuda.synchronize()
     assert cuda_lib.launch_count() > c0
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_sharded_layer_world1_nccl_equals_unsharded(cuda_lib, B):
+    """ShardedQTIPLinear through a real NCCL process group (world size 1 on this GPU): the
+    all-gather + reorder + replicated RHT-out path returns the unsharded layer's y bit for bit."""
+    import socket
+    import torch.distributed as dist
+    from paper_2406_11235_b200.sharded import ShardedQTIPLinear
+    m, n = 640, 512
+    tiles = synth.random_tiles(m, n, 2, seed=31)
+    full = make_layer(cuda_lib, m, n, "3inst", 2, tiles, None, seed=4, scale=0.5)   # power of 2: exact either side of the RHT
+    x = torch.from_numpy(synth.random_x(B, n, seed=32)).cuda()
+    created = False
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+        created = True
+    try:
+        sh = ShardedQTIPLinear(m, n, 0, 1, code="3inst", k=2).load_tiles(
+            tiles, synth.random_sign_bytes(m, 3001 + 4), synth.random_sign_bytes(n, 3000 + 4), scale=0.5)
+        y_sh = sh(x).cpu().numpy()
+    finally:
+        if created:
+            dist.destroy_process_group()
+    y = full(x).cpu().numpy()
+    assert np.array_equal(y_sh, y)
