@@ -51,6 +51,7 @@ void count_launch(int n) { g_launches += (uint64_t)n; }
 
 bool g_pdl = true;
 bool g_fused_reduce = false;
+bool g_layer_auto = false;     // auto-pick the fused layer kernel (knob 3)
 bool pdl_enabled() { return g_pdl; }
 
 void prefer_max_smem(const void* kern) {
@@ -213,7 +214,7 @@ size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, i
     const Layout l = make_layout(m, n, p->k);
     const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);       // x~ rows (mma kernel pads the batch)
     return align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad) +
-           align256(4 * (l.m_pad / kCellRows + 2));
+           align256(4 * (l.m_pad / kCellRows + 2)) + align256(4 * layer_workspace_floats(l, B, 0)) + 1024;
 }
 
 qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, const void* d_packed,
@@ -254,7 +255,13 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if (g_impl == 2 && !tc_ok) return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 kernel: needs 2 <= k <= 4, B <= 16, HYB Q = 9 one-sign");
     if (g_impl == 3 && !mma_ok) return fail(QTIP_ERR_UNSUPPORTED, "mma kernel: needs 2 <= k <= 4, B <= 16, one-sign HYB");
     if (g_impl == 4 && !row_ok) return fail(QTIP_ERR_UNSUPPORTED, "row kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB");
+    const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
+    const int64_t launch_tile_rows = (row_end - row_begin + kTile - 1) / kTile;
+    const bool layer_ok = layer_supported(l, p->code, ca, B, launch_tile_rows, rin && !(flags & QTIP_XT_READY), rout);
+    if (g_impl == 5 && !layer_ok)
+        return fail(QTIP_ERR_UNSUPPORTED, "fused layer kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB, shared memory fit");
     int impl = g_impl;
+    if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
     if (impl == 0) {
         // measured: the row-tile kernel wins while its CTAs (one per 16 rows,
         // 8-16 warps each) fill the GPU in one wave; beyond that the split-K kernel balances better
@@ -271,8 +278,25 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     float* yt = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
     int* cnt = (int*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad));
     const int n_rb = (int)(l.m_pad / kCellRows);
-    const int xmode = (use_mma || use_row) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
+    const int xmode = (use_mma || use_row || impl == 5) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
     cudaError_t e;
+    if (impl == 5) {
+        // one persistent launch: RHT-in, decode-GEMV, reduction, RHT-out (k_layer.cu)
+        float* lws = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) +
+                              align256(4 * B * l.m_pad) + align256(4 * (l.m_pad / kCellRows + 2)));
+        unsigned* bar = (unsigned*)((char*)lws + align256(4 * layer_workspace_floats(l, B, 0)));
+        const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
+        const bool prof = g_prof_start && g_prof_stop;
+        if (prof) record_event(g_prof_start, s);
+        e = launch_layer(l, p->code, ca, d_packed, d_lut, d_x, d_sign_n, d_sign_m, scale, d_y, B, row_begin, row_end,
+                         rin, rout, (flags & QTIP_XT_READY) != 0, (uint32_t*)xt, row_words, lws, bar, s);
+        if (prof) {
+            record_event(g_prof_stop, s);
+            g_prof_start = g_prof_stop = nullptr;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec layer");
+        return QTIP_OK;
+    }
     // the input kernel also clears the GEMV's split-K arrival counters (workspace is caller memory)
     if (flags & QTIP_XT_READY) e = cudaSuccess;          // counters are left zero by every GEMV
     else if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 2);
@@ -379,6 +403,8 @@ uint64_t qtip_launch_count(void) { return g_launches; }
 // DESIGN.md).
 extern "C" int qtip_internal_set_knob(int key, int value) {
     if (key == 1) { g_fused_reduce = value != 0; return 0; }
+    if (key == 2) { qtip::g_layer_debug = value; return 0; }
+    if (key == 3) { g_layer_auto = value != 0; return 0; }
     return -1;
 }
 
@@ -386,5 +412,6 @@ extern "C" int qtip_internal_set_cta_trace(void* buf, int cap) {
     cudaError_t e = qtip::set_cta_trace_rht((unsigned long long*)buf, cap);
     if (e == cudaSuccess) e = qtip::set_cta_trace_mma((unsigned long long*)buf, cap);
     if (e == cudaSuccess) e = qtip::set_cta_trace_row((unsigned long long*)buf, cap);
+    if (e == cudaSuccess) e = qtip::set_cta_trace_layer((unsigned long long*)buf, cap);
     return (int)e;
 }

@@ -107,9 +107,22 @@ cudaError_t launch_gemv_row(const Layout& lay, int code, const CodeArgs& ca, con
                             const void* xt_frag, int64_t xt_row_words, int64_t B, int64_t row_begin, int64_t row_end,
                             float* y, int64_t y_stride, int64_t row_lo, int64_t row_hi, float scale, cudaStream_t s);
 
+// Fused single-launch layer (k_layer.cu, impl 5): RHT-in, decode-GEMV, reduction and RHT-out with
+// in-kernel grid barriers (one CTA per SM).  ws_f: layer_workspace_floats() floats; bar: 256
+// per-CTA epoch flags that must be zero before the first call (every call leaves them equal).
+bool layer_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int64_t tile_rows, bool rht_in,
+                     bool rht_out);
+size_t layer_workspace_floats(const Layout& lay, int64_t B, int64_t tile_rows);
+cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
+                         const float* x, const uint8_t* sign_n, const uint8_t* sign_m, float scale, float* y,
+                         int64_t B, int64_t row_begin, int64_t row_end, bool rht_in, bool rht_out, bool xt_ready,
+                         uint32_t* xt_g, int64_t row_words, float* ws_f, unsigned* bar, cudaStream_t s);
+
 // Debug CTA timelines (trace.cuh), per translation unit.
 cudaError_t set_cta_trace_rht(unsigned long long* buf, int cap);
 cudaError_t set_cta_trace_mma(unsigned long long* buf, int cap);
 cudaError_t set_cta_trace_row(unsigned long long* buf, int cap);
+cudaError_t set_cta_trace_layer(unsigned long long* buf, int cap);
+extern int g_layer_debug;   // k_layer.cu debug bits (qtip_internal_set_knob(2, bits))
 
 }  // namespace qtip

@@ -1,0 +1,1040 @@
+// k_layer.cu -- the whole QTIP layer y = scale * S_m H_m^T W~ H_n S_n x in ONE
+// persistent launch (impl 5): RHT-in, fused trellis-decode GEMV, split reduction and RHT-out,
+// separated by in-kernel grid barriers instead of kernel boundaries.
+//
+// Grid: one 512-thread CTA per SM (all co-resident; grid barriers are self-resetting counters in
+// the caller's zero-initialised workspace, with a 4 s watchdog that traps instead of hanging).
+//
+//   prologue   every warp requests its first S weight chunks (cp.async.bulk into a private ring);
+//              the packed stream does not depend on the previous kernel, so this runs before the
+//              PDL wait and overlaps the previous layer's tail.
+//   x~         n = 2^a: every CTA computes the whole x~ = H_n S_n x / sqrt(n) itself (fp32 FWHT in
+//              shared memory, register radix-8 passes) and keeps it resident in shared memory as
+//              binary16 in mma.sync B-fragment order -- no barrier.  n = b 2^a, b > 1 (Paley
+//              factor): every CTA does the Sylvester part, computes its slice of the dense H_b
+//              mixing, publishes it, grid barrier, then loads all of x~.
+//   GEMV       the launch's tile rows are cut into fixed "units" of U tile pairs (32 columns each)
+//              along a row; unit partial sums (16 rows x B) come from one warp's register MMA
+//              accumulation in a fixed order.  CTA c owns the contiguous unit range
+//              [c T / P, (c+1) T / P) in row-major order, its warps take units round-robin.
+//              Row sums are always (((p_0 + p_1) + p_2) + ...) over the row's units, so every
+//              row's arithmetic depends on n only (a row shard equals the full call bit for bit).
+//   reduce     rows whose units all lie in this CTA are summed in shared memory -> y~ (global);
+//              rows shared with a neighbour CTA publish their unit partials; grid barrier.
+//   RHT-out    every CTA assembles all of y~, runs the Sylvester FWHT, and writes its slice of
+//              y = scale * S_m (H_m^T y~) / sqrt(m) (dense H_b^T mixing of its slice for b > 1).
+//              Without RHT-out the owner of a row's last unit finishes the shared rows.
+#include <algorithm>
+#include <cmath>
+
+#include "internal.h"
+#include "mma_tile.cuh"
+#include "tc.cuh"
+
+namespace qtip {
+namespace {
+
+using namespace mma;
+
+constexpr int kLWarps = 16;
+constexpr int kLThreads = 32 * kLWarps;
+constexpr int kLMaxStages = 8;
+constexpr int kMixChunk = 256;               // outputs per dense-mixing round
+
+struct LayerArgs {
+    const uint32_t* packed;
+    Layout lay;
+    CodeArgs ca;
+    const uint32_t* lut;
+    const float* x;                          // [B][n]
+    const uint8_t* sign_n;
+    const uint8_t* sign_m;
+    float scale, code_factor;
+    float* y;                                // y[b * y_stride + (i - row_lo)]
+    int64_t y_stride, row_lo, row_hi;
+    int B;
+    int rht_in, rht_out, xt_ready, coop;     // coop: x~ through global memory + a grid barrier
+    int nb, na, mb, ma;                      // n = nb 2^na, m = mb 2^ma
+    const uint32_t* hb_n;                    // H_nb bit rows (nb > 1)
+    const uint32_t* hbt_m;                   // H_mb^T bit rows (mb > 1)
+    uint32_t* xt_g;                          // x~ in fragment order, [B][row_words] words
+    int64_t row_words;                       // n_pad (K-doubled codes) or n_pad / 2 (HYB)
+    float* ybuf;                             // [B][m_pad] completed y~ rows
+    float* gpart;                            // [B][m_pad][n_units] unit partials of shared rows
+    unsigned* bar;                           // grid barrier {count at [0], generation at [32]}
+    int64_t tile_row0;                       // first tile row of the launch
+    int64_t T;                               // units in the launch
+    int n_units, U, CP;                      // units per tile row, tile pairs per unit / chunk
+    int stages;
+    int max_units_cta;
+    int part_smem;                           // unit partials in shared memory (else in gpart)
+    uint32_t off_ring, off_x, off_v, off_red, off_out, off_outred, off_scr;
+    int finishers;                           // rows mode: CTAs (last arrivals) that run the RHT-out
+    int debug;                               // knob 2: bit 0 = run the fast x~ phase twice (cold/warm probe)
+};
+
+__device__ unsigned long long* g_layer_trace = nullptr;
+__device__ int g_layer_trace_cap = 0;
+
+// Phase timeline (debug): per CTA %globaltimer marks [0] entry, [1] PDL wait released, [2] input
+// staged, [3] FWHT-in, [4] x~ ready, [5] GEMV done, [6] in-CTA reduction (+ barrier 1), [7] shared
+// rows, [8] barrier 2, [9] y~ staged, [10] FWHT-out, [11] exit; records of 14 words
+// {tag 5, blockIdx, t0..t11} after a u64 record counter.
+constexpr int kMarks = 12;
+__shared__ unsigned long long g_trs[kMarks];
+__device__ __forceinline__ void trace_mark(bool on, int i) {
+    if (on && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trs[i] = t;
+    }
+}
+
+__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 6) & 3) << 3); }
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Grid barrier: arrival counter and generation word on different 128-B lines (bar[0], bar[32]);
+// the last arrival resets the counter and bumps the generation, the others poll the generation
+// with relaxed loads and fence once.  The counter is 0 between barriers (zero-initialised
+// workspace); a 4 s watchdog traps instead of hanging if a CTA is missing.
+// Measured variants: scripts/gridbar_microbench.cu.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* cnt = bar;
+        unsigned* gen = bar + 32;
+        unsigned g, old;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(cnt) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+        } else {
+            const uint64_t t0 = gtimer();
+            while (true) {
+                unsigned v;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+                if (v != g) break;
+                if (gtimer() - t0 > 4000000000ull) __trap();
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+    }
+    __syncthreads();
+}
+
+// The canonical sum of a row's unit partials p_u (u < nu, element stride st): lane l adds
+// p_l, p_{l+32}, ... in order, then a fixed xor butterfly over the lanes (every lane ends with
+// the same bits).  Used for every row, in-CTA or shared, so a row's value depends on n only.
+template <bool kGlobal>
+__device__ __forceinline__ float warp_row_sum(const float* p, int64_t st, int nu) {
+    const int lane = threadIdx.x & 31;
+    float t = 0.0f;
+    for (int u = lane; u < nu; u += 32) t += kGlobal ? __ldcg(p + u * st) : p[u * st];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
+// Register/shuffle Walsh-Hadamard transform of one length-n = 2^a vector held by T = n / E threads
+// (layout A: thread t owns elements t E + e).  Butterflies on the E register bits and the 5 lane
+// bits run without memory traffic; if warps hold further bits, one swizzled shared-memory
+// transpose (scr: n floats) swaps the warp field into the lanes and those bits run as shuffles.
+// Every thread of the CTA must call it (it synchronises); threads >= T carry don't-care values.
+// Returns the index of the thread's first element afterwards (E contiguous elements).
+template <int E>
+__device__ __forceinline__ int fwht_fast(float (&v)[E], int a, float* scr) {
+    constexpr int s = E == 4 ? 2 : (E == 8 ? 3 : 4);
+    const int t = threadIdx.x, lane = t & 31;
+    const int T = (1 << a) >> s;
+#pragma unroll
+    for (int h = 1; h < E; h <<= 1)
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (!(e & h)) {
+                const float x0 = v[e], x1 = v[e | h];
+                v[e] = x0 + x1;
+                v[e | h] = x0 - x1;
+            }
+    const int lb = a - s < 5 ? a - s : 5;
+    for (int j = 0; j < lb; ++j) {
+        const int h = 1 << j;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const float o = __shfl_xor_sync(0xffffffffu, v[e], h);
+            v[e] = (lane & h) ? o - v[e] : v[e] + o;
+        }
+    }
+    const int wb = a - s - 5;
+    if (wb <= 0) return t * E;
+    // transpose: float4 slot q = i >> 2 stored at q ^ (warp field & 7)
+    auto slot = [&](int i) { return ((i >> 2) ^ ((i >> (s + 5)) & 7)) << 2; };
+    if (t < T) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4)
+            *reinterpret_cast<float4*>(scr + slot(t * E + e)) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+    }
+    __syncthreads();
+    const int w2 = t >> 5;                                          // = the old lane's high wb bits
+    const int wo = lane >> (5 - wb), llo = lane & ((1 << (5 - wb)) - 1);
+    const int i0 = (wo << (s + 5)) | (w2 << (s + 5 - wb)) | (llo << s);
+    if (t < T) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const float4 q = *reinterpret_cast<const float4*>(scr + slot(i0 + e));
+            v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
+        }
+    }
+    for (int j = 0; j < wb; ++j) {
+        const int h = 1 << (5 - wb + j);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const float o = __shfl_xor_sync(0xffffffffu, v[e], h);
+            v[e] = (lane & h) ? o - v[e] : v[e] + o;
+        }
+    }
+    __syncthreads();                                                // scr may be reused
+    return i0;
+}
+
+// After fwht_fast: park the thread's E values (first index i0) in scr with the transpose swizzle,
+// so that whole 16-element tiles can be read back conflict-free by one thread each (tile_read).
+template <int E>
+__device__ __forceinline__ void park_tiles(const float (&v)[E], int i0, int a, float* scr) {
+    constexpr int s = E == 4 ? 2 : (E == 8 ? 3 : 4);
+    const int T = (1 << a) >> s;
+    if ((int)threadIdx.x < T) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const int i = i0 + e;
+            *reinterpret_cast<float4*>(scr + (((i >> 2) ^ ((i >> (s + 5)) & 7)) << 2)) =
+                make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+    }
+    __syncthreads();
+}
+// the 16 values of tile `tile` (elements 16 tile .. 16 tile + 15) parked by park_tiles<E>; with
+// consecutive tiles on consecutive lanes the swizzle spreads each 16-B read over the bank groups
+template <int E>
+__device__ __forceinline__ void tile_read(const float* scr, int tile, float (&o)[16]) {
+    constexpr int s = E == 4 ? 2 : (E == 8 ? 3 : 4);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int i = 16 * tile + 4 * j;
+        const float4 q = *reinterpret_cast<const float4*>(scr + (((i >> 2) ^ ((i >> (s + 5)) & 7)) << 2));
+        o[4 * j] = q.x; o[4 * j + 1] = q.y; o[4 * j + 2] = q.z; o[4 * j + 3] = q.w;
+    }
+}
+// one tile of x~ (16 values, already scaled) -> binary16 B-fragment words at dst (16 words
+// K-doubled, 8 words HYB); the 16-B chunks go out in a lane-rotated order (consecutive lanes write
+// consecutive tiles, 64 B apart: rotation spreads a store instruction over 8 bank groups)
+template <bool kHyb>
+__device__ __forceinline__ void put_tile(uint32_t* dst, const float (&v)[16]) {
+    auto h = [&](int c) { return (uint32_t)__half_as_ushort(__float2half_rn(v[c])); };
+    if constexpr (!kHyb) {
+        uint4 w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {                               // words 4j..4j+3 = cols 2j, 2j+8, 2j+1, 2j+9
+            const uint32_t a = h(2 * j), b = h(2 * j + 8), c = h(2 * j + 1), d = h(2 * j + 9);
+            w[j] = make_uint4(a | (a << 16), b | (b << 16), c | (c << 16), d | (d << 16));
+        }
+        const int r = (threadIdx.x >> 1) & 3;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int j = (jj + r) & 3;
+            const uint4 x = j == 0 ? w[0] : (j == 1 ? w[1] : (j == 2 ? w[2] : w[3]));
+            *reinterpret_cast<uint4*>(dst + 4 * j) = x;
+        }
+    } else {
+        uint4 w[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {                               // word ww holds pair 4 (ww & 1) + (ww >> 1)
+            uint32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int ww = 4 * j + k, pr = 4 * (ww & 1) + (ww >> 1);
+                u[k] = h(2 * pr) | (h(2 * pr + 1) << 16);
+            }
+            w[j] = make_uint4(u[0], u[1], u[2], u[3]);
+        }
+        const int r = (threadIdx.x >> 2) & 1;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = jj ^ r;
+            *reinterpret_cast<uint4*>(dst + 4 * j) = j ? w[1] : w[0];
+        }
+    }
+}
+
+// fast-path element count per thread for a power-of-two length n (0: not supported)
+__host__ __device__ inline int fwht_fast_E(int64_t n, int a, int threads) {
+    if (n != ((int64_t)1 << a) || n < 128) return 0;
+    const int64_t E = n / threads < 4 ? 4 : n / threads;
+    return (E == 4 || E == 8 || E == 16) ? (int)E : 0;
+}
+
+// One radix-2^R pass of the Walsh-Hadamard butterflies on index bits [p, p + R) of v (swizzled).
+template <int R>
+__device__ __forceinline__ void fwht_pass(float* v, int len, int p) {
+    constexpr int G = 1 << R;
+    const int ng = len >> R;
+    const int pm = (1 << p) - 1;
+    for (int gi = threadIdx.x; gi < ng; gi += kLThreads) {
+        const int base = (gi & pm) | ((gi >> p) << (p + R));
+        float u[G];
+        bool vec = false;
+        if constexpr (R == 3) {
+            if (p == 0) {                                            // 8 contiguous floats: 2 x LDS.128
+                const float4* q = reinterpret_cast<const float4*>(v + swz(base));
+                const float4 a = q[0], b = q[1];
+                u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w; u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
+                vec = true;
+            }
+        }
+        if (!vec) {
+#pragma unroll
+            for (int j = 0; j < G; ++j) u[j] = v[swz(base + (j << p))];
+        }
+#pragma unroll
+        for (int h = 1; h < G; h <<= 1)
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+                if (!(j & h)) {
+                    const float a = u[j], b = u[j | h];
+                    u[j] = a + b;
+                    u[j | h] = a - b;
+                }
+        if constexpr (R == 3) {
+            if (vec) {
+                float4* q = reinterpret_cast<float4*>(v + swz(base));
+                q[0] = make_float4(u[0], u[1], u[2], u[3]);
+                q[1] = make_float4(u[4], u[5], u[6], u[7]);
+            }
+        }
+        if (!vec) {
+#pragma unroll
+            for (int j = 0; j < G; ++j) v[swz(base + (j << p))] = u[j];
+        }
+    }
+}
+
+// Sylvester transform along index bits [0, a) of every 2^a block of v[0, len) (no scaling).
+__device__ __noinline__ void cta_fwht(float* v, int len, int a) {
+    for (int p = 0; p < a;) {
+        const int r = min(3, a - p);
+        if (r == 3) fwht_pass<3>(v, len, p);
+        else if (r == 2) fwht_pass<2>(v, len, p);
+        else fwht_pass<1>(v, len, p);
+        __syncthreads();
+        p += r;
+    }
+}
+
+// Dense Paley-factor mixing of flat outputs [f0, f1) (f = bt * len + i_b 2^a + i_a):
+// out = sum_jb Hbits[i_b][jb] v[bt][jb][i_a]; warps split jb, partials added in warp order.
+// emit(f, value) is called once per output by threads 0 .. kMixChunk-1.
+template <typename Emit>
+__device__ __noinline__ void dense_mix(const float* v, int len, int b, int a, const uint32_t* __restrict__ hbits,
+                                       int f0, int f1, float* red, Emit emit) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpr = (b + 31) >> 5;
+    const int jlo = b * warp / kLWarps, jhi = b * (warp + 1) / kLWarps;
+    const int am = (1 << a) - 1;
+    for (int c0 = f0; c0 < f1; c0 += kMixChunk) {
+        const int cnt = f1 - c0 < kMixChunk ? f1 - c0 : kMixChunk;
+#pragma unroll 1
+        for (int e = 0; e < kMixChunk / 32; ++e) {
+            const int fl = lane + 32 * e;
+            float s = 0.0f;
+            if (fl < cnt) {
+                const int f = c0 + fl;
+                const int bt = f / len, i = f - bt * len;
+                const int ib = i >> a, ia = i & am;
+                const uint32_t* hr = hbits + ib * wpr;
+                for (int jb = jlo; jb < jhi; ++jb) {
+                    const float x = v[swz(bt * len + (jb << a) + ia)];
+                    const uint32_t neg = (__ldg(hr + (jb >> 5)) >> (jb & 31)) & 1u;
+                    s += neg ? -x : x;
+                }
+            }
+            red[warp * kMixChunk + fl] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            float s = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kLWarps; ++w) s += red[w * kMixChunk + threadIdx.x];
+            emit(c0 + threadIdx.x, s);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ uint32_t sgn(const uint8_t* __restrict__ s, int64_t i) {
+    return (__ldg(s + (i >> 3)) >> (i & 7)) & 1u;
+}
+
+// vb[swz(bt * dst_stride + e)] = S[e] src[bt * src_stride + e] for bt < B, e < len (fp32 in global
+// memory, possibly the previous kernel's output: L2 loads); e in [len, dst_stride) is zero-filled.
+// Four 16-B loads in flight per thread.
+__device__ __noinline__ void stage_input(float* vb, int dst_stride, const float* src, int64_t src_stride,
+                                         const uint8_t* __restrict__ sign, int B, int len) {
+    const int qpr = dst_stride >> 2, nq = B * qpr;                  // len, dst_stride multiples of 4
+    for (int q0 = threadIdx.x; q0 < nq; q0 += 4 * kLThreads) {
+        float4 v[4];
+        uint32_t sb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int q = q0 + j * kLThreads;
+            v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            sb[j] = 0u;
+            if (q < nq) {
+                const int bt = q / qpr, e = 4 * (q - bt * qpr);
+                if (e < len) {
+                    v[j] = __ldcg(reinterpret_cast<const float4*>(src + bt * src_stride + e));
+                    if (sign) sb[j] = (uint32_t)__ldg(sign + (e >> 3)) >> (e & 7);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int q = q0 + j * kLThreads;
+            if (q < nq) {
+                float4 w = v[j];
+                if (sb[j] & 1u) w.x = -w.x;
+                if (sb[j] & 2u) w.y = -w.y;
+                if (sb[j] & 4u) w.z = -w.z;
+                if (sb[j] & 8u) w.w = -w.w;
+                *reinterpret_cast<float4*>(vb + swz(4 * q)) = w;
+            }
+        }
+    }
+}
+
+// x~ element (bt, e) -> binary16 in B-fragment order (the RHT kernel's out_mode 3 / 4).
+template <bool kHyb>
+__device__ __forceinline__ void put_xt(uint32_t* xs, int64_t row_words, int bt, int64_t e, float v) {
+    const uint32_t h = __half_as_ushort(__float2half_rn(v));
+    const int64_t tile = e >> 4;
+    const int c = (int)(e & 15);
+    if constexpr (!kHyb) {
+        const int t = (c & 7) >> 1, q = ((c & 1) << 1) | (c >> 3);
+        xs[bt * row_words + tile * 16 + 4 * t + q] = h | (h << 16);
+    } else {
+        const int j = c >> 1;
+        const int64_t w = tile * 8 + 2 * (j & 3) + (j >> 2);
+        reinterpret_cast<uint16_t*>(xs + bt * row_words)[2 * w + (c & 1)] = (uint16_t)h;
+    }
+}
+
+__device__ __noinline__ void rht_out_phase(const LayerArgs& args, uint8_t* smem, int64_t c, int64_t P, bool tr);
+
+// 16 warps x 64 registers: half the register file, so the next layer's CTA can become resident
+// under PDL while this one runs (its parameter fetch, prologue and weight requests then overlap
+// this launch instead of following it).
+template <int K, int CODE, bool kImm>
+__global__ void __launch_bounds__(kLThreads, 2) layer_kernel(const __grid_constant__ LayerArgs args) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr bool kHyb = CODE == QTIP_CODE_HYB;
+    constexpr int TW = 8 * K;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tig = lane & 3;
+    const int B = args.B, S = args.stages;
+    const int64_t P = gridDim.x, c = blockIdx.x;
+    const int64_t n = args.lay.n, m = args.lay.m, n_kc = args.lay.n_kc, m_pad = args.lay.m_pad;
+    const int n_units = args.n_units, U = args.U, CP = args.CP;
+    const int64_t T = args.T;
+    // rows mode (launch tile rows >= CTAs): CTA c owns whole tile rows [c R / P, (c+1) R / P), no row
+    // is shared; else CTA c owns units [c T / P, (c+1) T / P) and rows may straddle CTAs
+    const int64_t R = T / n_units;
+    const bool rows_mode = R >= P;
+    const int64_t L0 = rows_mode ? (c * R / P) * n_units : c * T / P;
+    const int64_t L1 = rows_mode ? ((c + 1) * R / P) * n_units : (c + 1) * T / P;
+    const uint32_t chunk_bytes = 256u * K;                          // one cell's tile row
+    const int n_pairs = (int)(n_kc * 4);
+
+    const bool tr = g_layer_trace != nullptr;
+    if (tr && threadIdx.x == 0)
+        for (int q = 0; q < kMarks; ++q) g_trs[q] = 0;
+    trace_mark(tr, 0);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem) + warp * kLMaxStages;
+    float* part = reinterpret_cast<float*>(smem + 8 * kLWarps * kLMaxStages);   // [unit - L0][16][B]
+    uint8_t* ring = smem + args.off_ring + (size_t)warp * S * chunk_bytes;
+    uint32_t* xs = reinterpret_cast<uint32_t*>(smem + args.off_x);
+    float* vb = reinterpret_cast<float*>(smem + args.off_v);
+    float* red = reinterpret_cast<float*>(smem + args.off_red);
+
+    // ---- warp's units L = L0 + warp + j W (one unit = one ring chunk = one cell's tile row: 4 tile
+    //      pairs, 128 columns, 256 k bytes); 32-bit incremental (row, unit-in-row) iterators
+    struct UnitIt {
+        int L, Ir, u;                                               // launch unit, tile row, unit in row
+        __device__ __forceinline__ void step(int n_units) {
+            L += kLWarps;
+            u += kLWarps;
+            while (u >= n_units) { u -= n_units; ++Ir; }
+        }
+    };
+    const int L0i = (int)L0, L1i = (int)L1;
+    UnitIt first{L0i + warp, (L0i + warp) / n_units, (L0i + warp) % n_units};
+    auto issue = [&](const UnitIt& it, int st) {
+        const int I = (int)args.tile_row0 + it.Ir;
+        const uint32_t bar = ptx::smem_u32(full + st);
+        ptx::mbar_arrive_expect_tx(bar, chunk_bytes);
+        ptx::bulk_g2s(ptx::smem_u32(ring + (size_t)st * chunk_bytes),
+                      args.packed + ((int64_t)(I >> 3) * n_kc + it.u) * (512 * K) + (I & 7) * (64 * K), chunk_bytes, bar);
+    };
+    UnitIt iit = first;                                             // issue-side iterator (lane 0)
+    int ist = 0;
+    auto issue_next = [&]() {
+        if (iit.L >= L1i) return;
+        issue(iit, ist);
+        if (++ist == S) ist = 0;
+        iit.step(n_units);
+    };
+    if (lane == 0) {
+        for (int st = 0; st < S; ++st) ptx::mbar_init(ptx::smem_u32(full + st), 1);
+        ptx::fence_mbar_init();
+        for (int st = 0; st < S; ++st) issue_next();
+    }
+    __syncwarp();
+    trace_mark(tr, 7);
+
+    ptx::pdl_wait();                                                // x may be the previous kernel's output
+    trace_mark(tr, 1);
+
+    // ---------------------------------------------------------------- x~
+    const int64_t rw = args.row_words;
+    const int64_t n_pad = args.lay.n_pad;
+    if (args.xt_ready || args.coop) {
+        if (args.coop && !args.xt_ready) {
+            // Sylvester part of every block (redundant), then this CTA's slice of the H_b mixing
+            const int len = (int)n;
+            stage_input(vb, len, args.x, n, args.rht_in ? args.sign_n : nullptr, B, len);
+            __syncthreads();
+            cta_fwht(vb, B * len, args.na);
+            const float rs = rsqrtf((float)n);
+            const int64_t F = (int64_t)B * len;
+            uint32_t* xg = args.xt_g;
+            dense_mix(vb, len, args.nb, args.na, args.hb_n, (int)(c * F / P), (int)((c + 1) * F / P), red,
+                      [=](int f, float s) { put_xt<kHyb>(xg, rw, f / len, f % len, s * rs); });
+            if (c == 0) {                                           // zero padding columns [n, n_pad)
+                const int pad = (int)(n_pad - n);
+                for (int i = threadIdx.x; i < B * pad; i += kLThreads)
+                    put_xt<kHyb>(args.xt_g, rw, i / pad, n + i % pad, 0.0f);
+            }
+            grid_sync(args.bar);
+        }
+        const int words = (int)(B * rw);
+        for (int i = threadIdx.x; i < words / 4; i += kLThreads)
+            reinterpret_cast<uint4*>(xs)[i] = __ldcg(reinterpret_cast<const uint4*>(args.xt_g) + i);
+    } else {
+        const int len = (int)n, np = (int)n_pad;
+        const int Ef = args.rht_in ? fwht_fast_E(n, args.na, kLThreads) : 0;
+        if (Ef) {
+            // register / shuffle FWHT per batch row straight from global x; fragment-order x~ out
+            float* scr = reinterpret_cast<float*>(smem + args.off_scr);
+            const float rs = rsqrtf((float)n);
+            for (int rep = 0; rep < 1 + (args.debug & 1); ++rep) {
+            for (int bt = 0; bt < B; ++bt) {
+                auto run = [&](auto EE) {
+                    constexpr int E = decltype(EE)::value;
+                    float v[E];
+                    const int T = len / E;
+                    uint32_t sb = 0;
+                    if ((int)threadIdx.x < T) {
+                        const int e0 = threadIdx.x * E;
+                        sb = (uint32_t)__ldg(reinterpret_cast<const uint16_t*>(args.sign_n) + (e0 >> 4)) >> (e0 & 15);
+#pragma unroll
+                        for (int e = 0; e < E; e += 4) {
+                            const float4 q = __ldcg(reinterpret_cast<const float4*>(args.x + bt * n + e0 + e));
+                            v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
+                        }
+#pragma unroll
+                        for (int e = 0; e < E; ++e)
+                            if ((sb >> e) & 1u) v[e] = -v[e];
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) v[e] = 0.0f;
+                    }
+                    trace_mark(tr, 2);
+                    const int i0 = fwht_fast<E>(v, args.na, scr);
+                    trace_mark(tr, 3);
+                    park_tiles<E>(v, i0, args.na, scr);
+                    const int wpt = kHyb ? 8 : 16;                  // x~ words per tile
+                    for (int tile = threadIdx.x; tile < (len >> 4); tile += kLThreads) {
+                        float o[16];
+                        tile_read<E>(scr, tile, o);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) o[q] *= rs;
+                        put_tile<kHyb>(xs + bt * rw + tile * wpt, o);
+                        if (c == 0 && args.xt_g) put_tile<kHyb>(args.xt_g + bt * rw + tile * wpt, o);
+                    }
+                    __syncthreads();                                // scr reused by the next batch row
+                };
+                if (Ef == 4) run(std::integral_constant<int, 4>{});
+                else if (Ef == 8) run(std::integral_constant<int, 8>{});
+                else run(std::integral_constant<int, 16>{});
+            }
+            __syncthreads();
+            }
+            for (int i = threadIdx.x; i < B * (np - len); i += kLThreads) {   // zero padding columns
+                const int bt = i / (np - len);
+                put_xt<kHyb>(xs, rw, bt, len + i - bt * (np - len), 0.0f);
+            }
+        } else {
+        // x~ in place: vb (fp32, batch stride n_pad, zero padded) and xs share memory; each thread
+        // converts one 16-column tile, all reads of a chunk of tiles precede its writes (a tile's
+        // data and its fragment words stay inside one 32-element swizzle block)
+        stage_input(vb, np, args.x, n, args.rht_in ? args.sign_n : nullptr, B, len);
+        __syncthreads();
+        trace_mark(tr, 2);
+        float rs = 1.0f;
+        if (args.rht_in) {
+            cta_fwht(vb, B * np, args.na);
+            rs = rsqrtf((float)n);
+        }
+        trace_mark(tr, 3);
+        const int tpr = np >> 4, ntiles = B * tpr;
+        for (int t0 = 0; t0 < ntiles; t0 += kLThreads) {
+            const int t = t0 + threadIdx.x;
+            float v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = t < ntiles ? vb[swz(16 * t + q)] * rs : 0.0f;
+            __syncthreads();
+            if (t < ntiles) {
+                const int bt = t / tpr, e0 = 16 * (t - bt * tpr);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    put_xt<kHyb>(xs, rw, bt, e0 + q, v[q]);
+                    if (c == 0 && args.xt_g) put_xt<kHyb>(args.xt_g, rw, bt, e0 + q, v[q]);   // QTIP_XT_READY reuse
+                }
+            }
+            __syncthreads();
+        }
+        }
+    }
+    __syncthreads();
+    trace_mark(tr, 4);
+    ptx::pdl_launch_dependents();
+
+    // ---------------------------------------------------------------- GEMV over the warp's units
+    const CodeArgs ca = args.ca;
+    const Lcg<CODE, kImm> lcg(ca);
+    int st = 0;
+    uint32_t phase = 0;
+    for (UnitIt it = first; it.L < L1i; it.step(n_units)) {
+        float acc[2][1][4] = {{{0.f, 0.f, 0.f, 0.f}}, {{0.f, 0.f, 0.f, 0.f}}};
+        ptx::mbar_wait(ptx::smem_u32(full + st), phase);
+        const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + (size_t)st * chunk_bytes);
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int J = 8 * it.u + 2 * pp;                        // tile columns J, J + 1
+            uint32_t bf[2][1][4];
+            load_bfrag<1, kHyb>(xs, (int)rw, J, g, tig, B, bf[0]);
+            load_bfrag<1, kHyb>(xs, (int)rw, J + 1, g, tig, B, bf[1]);
+            tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf, acc[pp & 1], g, tig, lcg, ca, args.lut);
+        }
+        __syncwarp();
+        if (lane == 0) issue_next();
+        if (++st == S) { st = 0; phase ^= 1u; }
+        // acc[e] = D[MMA row g + 8 (e >> 1)][batch 2 tig + (e & 1)] <-> tile row 2g + (e >> 1)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int b = 2 * tig + (e & 1), r = 2 * g + (e >> 1);
+            if (b < B) {
+                const float v = acc[0][0][e] + acc[1][0][e];
+                if (args.part_smem) part[((it.L - L0i) * kTile + r) * B + b] = v;
+                else args.gpart[(b * m_pad + (args.tile_row0 + it.Ir) * kTile + r) * n_units + it.u] = v;
+            }
+        }
+    }
+    __syncthreads();
+    trace_mark(tr, 5);
+
+    // ---------------------------------------------------------------- reduction (warp per row)
+    const bool rht_out = args.rht_out != 0;
+    auto owner = [&](int64_t L) { return ((L + 1) * P - 1) / T; };    // unit mode: CTA whose range holds unit L
+    auto finish = [&](int b, int64_t i, float s) {                    // s = the row's canonical sum
+        s *= args.code_factor;
+        if (rht_out) args.ybuf[b * m_pad + i] = s;
+        else if (i >= args.row_lo && i < args.row_hi) args.y[b * args.y_stride + (i - args.row_lo)] = args.scale * s;
+    };
+    int Ia = 0, nrow_items = 0;
+    if (L1 > L0) {
+        Ia = L0i / n_units;
+        nrow_items = ((L1i - 1) / n_units - Ia + 1) * kTile * B;
+    }
+    const int tile_row0 = (int)args.tile_row0;
+    for (int t = warp; t < nrow_items; t += kLWarps) {
+        const int tb = t / B, b = t - tb * B;
+        const int Ir = Ia + (tb >> 4), r = tb & 15;
+        const int i = (tile_row0 + Ir) * kTile + r;
+        const int u0 = Ir * n_units;
+        if (u0 >= L0i && u0 + n_units <= L1i) {                       // every unit in this CTA
+            const float s = args.part_smem
+                ? warp_row_sum<false>(part + ((u0 - L0i) * kTile + r) * B + b, kTile * B, n_units)
+                : warp_row_sum<true>(args.gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
+            if (lane == 0) finish(b, i, s);
+        } else if (args.part_smem) {                                  // shared row: publish this CTA's units
+            const int s_lo = L0i - u0 > 0 ? L0i - u0 : 0, s_hi = L1i - u0 < n_units ? L1i - u0 : n_units;
+            for (int u = s_lo + lane; u < s_hi; u += 32)
+                args.gpart[((int64_t)b * m_pad + i) * n_units + u] = part[((u0 + u - L0i) * kTile + r) * B + b];
+        }
+    }
+    trace_mark(tr, 6);
+    if (rows_mode) {
+        // no shared rows.  RHT-out: every CTA takes a ticket after publishing its y~ rows; the last
+        // `finishers` arrivals run the RHT-out (the very last one alone when m = 2^a), the others
+        // exit at once and free their SM for the next launch (no grid barrier).
+        if (rht_out) {
+            __shared__ int s_ticket;
+            const int G = args.finishers;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long* cnt = reinterpret_cast<unsigned long long*>(args.bar + 64);
+                unsigned long long old;
+                __threadfence();
+                asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(cnt) : "memory");
+                const int tk = (int)(old % (unsigned long long)P);
+                s_ticket = tk;
+                if (tk >= P - G && tk < P - 1) {                        // wait for the remaining arrivals
+                    const unsigned long long target = (old / P + 1) * P;
+                    const uint64_t t0 = gtimer();
+                    while (true) {
+                        unsigned long long v;
+                        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+                        if (v >= target) break;
+                        if (gtimer() - t0 > 4000000000ull) __trap();
+                    }
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+            }
+            __syncthreads();
+            const int tk = s_ticket;
+            trace_mark(tr, 8);
+            if (tk >= P - G) rht_out_phase(args, smem, tk - (P - G), G, tr);
+        }
+    } else {
+        grid_sync(args.bar);
+        trace_mark(tr, 7);
+        // shared rows: finished by the owner of their last unit
+        for (int t = warp; t < nrow_items; t += kLWarps) {
+            const int tb = t / B, b = t - tb * B;
+            const int Ir = Ia + (tb >> 4), r = tb & 15;
+            const int u0 = Ir * n_units;
+            if ((u0 >= L0i && u0 + n_units <= L1i) || owner(u0 + n_units - 1) != c) continue;
+            const int i = (tile_row0 + Ir) * kTile + r;
+            const float s = warp_row_sum<true>(args.gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
+            if (lane == 0) finish(b, i, s);
+        }
+        if (rht_out) {
+            grid_sync(args.bar);
+            trace_mark(tr, 8);
+            rht_out_phase(args, smem, c, P, tr);
+        }
+    }
+    if (tr && threadIdx.x == 0) {
+        trace_mark(tr, 11);
+        const unsigned long long slot = atomicAdd(g_layer_trace, 1ull);
+        if (slot < (unsigned long long)g_layer_trace_cap) {
+            unsigned long long* r = g_layer_trace + 1 + (kMarks + 2) * slot;
+            r[0] = 5;
+            r[1] = blockIdx.x;
+            for (int q = 0; q < kMarks; ++q) r[2 + q] = g_trs[q];
+        }
+    }
+}
+
+// RHT-out, part `part` of `parts`: assemble y~ from ybuf, Sylvester FWHT, write this part's slice of
+// y = scale * S_m (H_m^T y~) / sqrt(m) (dense H_b^T mixing of the slice for b > 1).
+__device__ __noinline__ void rht_out_phase(const LayerArgs& args, uint8_t* smem, int64_t part, int64_t parts, bool tr) {
+    const int64_t m = args.lay.m, m_pad = args.lay.m_pad;
+    const int B = args.B;
+    const int lenm = (int)m;
+    const float os = args.scale * rsqrtf((float)m);
+    const int F = B * lenm;
+    const int f0 = (int)(part * F / parts), f1 = (int)((part + 1) * F / parts);
+    const int Ef = args.mb == 1 ? fwht_fast_E(m, args.ma, kLThreads) : 0;
+    if (Ef) {
+        float* scr = reinterpret_cast<float*>(smem + args.off_out);
+        for (int bt = 0; bt < B; ++bt) {
+            if (f1 <= bt * lenm || f0 >= (bt + 1) * lenm) continue;
+            auto run = [&](auto EE) {
+                constexpr int E = decltype(EE)::value;
+                float v[E];
+                const int T = lenm / E;
+                if ((int)threadIdx.x < T) {
+#pragma unroll
+                    for (int e = 0; e < E; e += 4) {
+                        const float4 q = __ldcg(reinterpret_cast<const float4*>(args.ybuf + bt * m_pad + threadIdx.x * E + e));
+                        v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) v[e] = 0.0f;
+                }
+                trace_mark(tr, 9);
+                const int i0 = fwht_fast<E>(v, args.ma, scr);
+                trace_mark(tr, 10);
+                park_tiles<E>(v, i0, args.ma, scr);
+                float* yr = args.y + bt * args.y_stride;
+                const int lo = f0 - bt * lenm, hi = f1 - bt * lenm;        // this part's outputs of the row
+                for (int tile = (lo > 0 ? lo >> 4 : 0) + threadIdx.x; tile < (lenm >> 4) && 16 * tile < hi;
+                     tile += kLThreads) {
+                    float o[16];
+                    tile_read<E>(scr, tile, o);
+                    const uint32_t sb = __ldg(reinterpret_cast<const uint16_t*>(args.sign_m) + tile);
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        o[q] *= os;
+                        if ((sb >> q) & 1u) o[q] = -o[q];
+                    }
+                    if (16 * tile >= lo && 16 * tile + 16 <= hi) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            *reinterpret_cast<float4*>(yr + 16 * tile + 4 * j) = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q)
+                            if (16 * tile + q >= lo && 16 * tile + q < hi) yr[16 * tile + q] = o[q];
+                    }
+                }
+                __syncthreads();
+            };
+            if (Ef == 4) run(std::integral_constant<int, 4>{});
+            else if (Ef == 8) run(std::integral_constant<int, 8>{});
+            else run(std::integral_constant<int, 16>{});
+        }
+        return;
+    }
+    float* vo = reinterpret_cast<float*>(smem + args.off_out);
+    float* ored = reinterpret_cast<float*>(smem + args.off_outred);
+    stage_input(vo, lenm, args.ybuf, m_pad, nullptr, B, lenm);
+    __syncthreads();
+    trace_mark(tr, 9);
+    cta_fwht(vo, B * lenm, args.ma);
+    trace_mark(tr, 10);
+    if (args.mb == 1) {
+        for (int f = f0 + threadIdx.x; f < f1; f += kLThreads) {
+            const int b = f / lenm, i = f - b * lenm;
+            float v = vo[swz(f)] * os;
+            if (sgn(args.sign_m, i)) v = -v;
+            args.y[b * args.y_stride + i] = v;
+        }
+    } else {
+        const uint8_t* sm_ = args.sign_m;
+        float* y = args.y;
+        const int64_t ys = args.y_stride;
+        dense_mix(vo, lenm, args.mb, args.ma, args.hbt_m, f0, f1, ored, [=](int f, float s) {
+            const int b = f / lenm, i = f - b * lenm;
+            float v = s * os;
+            if (sgn(sm_, i)) v = -v;
+            y[b * ys + i] = v;
+        });
+    }
+}
+
+template <int K, int CODE, bool kImm>
+cudaError_t launch_layer_t(LayerArgs a, size_t smem, cudaStream_t s) {
+    auto kern = layer_kernel<K, CODE, kImm>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kLThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;               // grid barrier needs co-residency
+    return launch_pdl(kern, dim3((unsigned)num_sms()), dim3(kLThreads), smem, s, a);
+}
+
+size_t align128(size_t v) { return (v + 127) & ~(size_t)127; }
+
+// Shared-memory plan; returns 0 when the layer does not fit one CTA per SM.
+struct LayerPlan {
+    int U, CP, S, max_units, part_smem;
+    int64_t T;
+    int n_units;
+    size_t smem;
+    uint32_t off_ring, off_x, off_v, off_red, off_out, off_outred, off_scr;
+};
+
+bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool coop, bool rht_out, int mb,
+                LayerPlan* pl) {
+    const int P = num_sms();
+    const bool hyb = code == QTIP_CODE_HYB;
+    const int n_pairs = (int)(lay.n_kc * 4);
+    // unit = one cell's tile row (4 tile pairs, 128 columns) for every shape: the association of
+    // a row's sum depends on n only, never on m, the row range or the grid
+    const int U = 4;
+    pl->U = U;
+    pl->CP = 4;
+    pl->n_units = (n_pairs + U - 1) / U;
+    pl->T = tile_rows * pl->n_units;
+    pl->max_units = tile_rows >= P ? (int)((tile_rows + P - 1) / P) * pl->n_units   // rows mode (see kernel)
+                                   : (int)((pl->T + P - 1) / P);
+    const size_t chunk = (size_t)pl->CP * 64 * lay.k;
+    const size_t head = 8 * kLWarps * kLMaxStages;
+    size_t part = align128((size_t)pl->max_units * kTile * B * 4);
+    pl->part_smem = part <= 48 * 1024;
+    if (!pl->part_smem) part = 0;
+    const size_t xs = align128((size_t)B * lay.n_pad * (hyb ? 2 : 4));
+    const size_t vin = align128(((size_t)B * lay.n + 31) / 32 * 32 * 4);
+    const size_t vin_pad = align128((size_t)B * lay.n_pad * 4);
+    const size_t red = (size_t)kLWarps * kMixChunk * 4;
+    const size_t vout = align128(((size_t)B * lay.m + 31) / 32 * 32 * 4);
+    auto layout = [&](int S) {                                        // offsets for ring depth S; total bytes
+        size_t off = head + part;
+        pl->off_ring = (uint32_t)off;
+        off += align128((size_t)kLWarps * S * chunk);
+        pl->off_x = (uint32_t)off;
+        if (coop) {
+            pl->off_v = (uint32_t)off;                                // x~ loaded after vin is dead
+            off += std::max(xs, vin);
+            pl->off_red = (uint32_t)off;
+            off += red;
+        } else {
+            pl->off_v = (uint32_t)off;                                // x~ written in place over vin
+            off += std::max(xs, vin_pad);
+            pl->off_red = (uint32_t)off;
+            pl->off_scr = (uint32_t)off;                              // fast FWHT transpose scratch
+            off += align128((size_t)lay.n_pad * 4);
+        }
+        const size_t endA = off;
+        size_t endB = head;                                           // RHT-out aliases everything after head
+        if (rht_out) {
+            pl->off_out = (uint32_t)endB;
+            endB += vout;
+            pl->off_outred = (uint32_t)endB;
+            if (mb > 1) endB += red;
+        } else {
+            pl->off_out = pl->off_outred = (uint32_t)head;
+        }
+        return std::max(endA, endB);
+    };
+    // the deepest ring that still lets a second CTA (the next layer's, under PDL) share the SM,
+    // else the deepest that fits one CTA per SM
+    int pick = 0;
+    for (int S = kLMaxStages; S >= 2 && !pick; --S)
+        if (layout(S) <= 113 * 1024) pick = S;
+    for (int S = kLMaxStages; S >= 2 && !pick; --S)
+        if (layout(S) <= 227 * 1024) pick = S;
+    if (!pick) return false;
+    pl->S = pick;
+    pl->smem = layout(pick);
+    return true;
+}
+
+}  // namespace
+
+int g_layer_debug = 0;
+
+cudaError_t set_cta_trace_layer(unsigned long long* buf, int cap) {
+    cudaError_t e = cudaMemcpyToSymbol(g_layer_trace, &buf, sizeof(buf));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_layer_trace_cap, &cap, sizeof(cap));
+    return e;
+}
+
+bool layer_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int64_t tile_rows, bool rht_in,
+                     bool rht_out) {
+    if (B < 1 || B > 4 || lay.k < 2 || lay.k > 4) return false;
+    if (code == QTIP_CODE_HYB && ca.two_sign) return false;
+    if (lay.n > (1 << 24) / 4 || lay.m > (1 << 24) / 4 || num_sms() > 256) return false;
+    int nb = 1, na = 0, mb = 1, ma = 0;
+    if (rht_in && !hadamard_factor(lay.n, &nb, &na)) return false;
+    if (rht_out && !hadamard_factor(lay.m, &mb, &ma)) return false;
+    LayerPlan pl;
+    return plan_layer(lay, code, B, tile_rows, rht_in && nb > 1, rht_out, mb, &pl);
+}
+
+size_t layer_workspace_floats(const Layout& lay, int64_t B, int64_t tile_rows) {
+    // ybuf [B][m_pad] + gpart [B][m_pad][n_units] (n_units = 2 n_kc)
+    (void)tile_rows;
+    return (size_t)B * lay.m_pad * (1 + 2 * lay.n_kc);
+}
+
+cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const void* packed, const uint16_t* lut,
+                         const float* x, const uint8_t* sign_n, const uint8_t* sign_m, float scale, float* y,
+                         int64_t B, int64_t row_begin, int64_t row_end, bool rht_in, bool rht_out, bool xt_ready,
+                         uint32_t* xt_g, int64_t row_words, float* ws_f, unsigned* bar, cudaStream_t s) {
+    LayerArgs a{};
+    a.packed = (const uint32_t*)packed;
+    a.lay = lay;
+    a.ca = ca;
+    a.lut = (const uint32_t*)lut;
+    a.x = x;
+    a.sign_n = sign_n;
+    a.sign_m = sign_m;
+    a.scale = scale;
+    a.code_factor = (code == QTIP_CODE_1MAD) ? 5.0f / 739.0f : 1.0f;
+    a.y = y;
+    a.row_lo = row_begin;
+    a.row_hi = row_end;
+    a.y_stride = rht_out ? lay.m : row_end - row_begin;
+    a.B = (int)B;
+    a.rht_in = rht_in;
+    a.rht_out = rht_out;
+    a.xt_ready = xt_ready;
+    a.nb = a.mb = 1;
+    a.na = a.ma = 0;
+    cudaError_t e = cudaSuccess;
+    if (rht_in && !xt_ready) {
+        if (!hadamard_factor(lay.n, &a.nb, &a.na)) return cudaErrorInvalidValue;
+        if (a.nb > 1) a.hb_n = hadamard_table_device(a.nb, false, &e);
+        if (e != cudaSuccess) return e;
+    }
+    if (rht_out) {
+        if (!hadamard_factor(lay.m, &a.mb, &a.ma)) return cudaErrorInvalidValue;
+        if (a.mb > 1) a.hbt_m = hadamard_table_device(a.mb, true, &e);
+        if (e != cudaSuccess) return e;
+    }
+    a.coop = rht_in && !xt_ready && a.nb > 1;
+    a.xt_g = xt_g;
+    a.row_words = row_words;
+    a.ybuf = ws_f;
+    a.gpart = ws_f + B * lay.m_pad;
+    a.bar = bar;
+    a.tile_row0 = row_begin / kTile;
+    const int64_t tile_rows = (row_end + kTile - 1) / kTile - a.tile_row0;
+    LayerPlan pl;
+    if (!plan_layer(lay, code, B, tile_rows, a.coop, rht_out, a.mb, &pl)) return cudaErrorInvalidConfiguration;
+    a.T = pl.T;
+    a.n_units = pl.n_units;
+    a.U = pl.U;
+    a.CP = pl.CP;
+    a.stages = pl.S;
+    a.max_units_cta = pl.max_units;
+    a.part_smem = pl.part_smem;
+    a.off_ring = pl.off_ring;
+    a.off_x = pl.off_x;
+    a.off_v = pl.off_v;
+    a.off_red = pl.off_red;
+    a.off_out = pl.off_out;
+    a.off_outred = pl.off_outred;
+    a.off_scr = pl.off_scr;
+    a.debug = g_layer_debug;
+    a.finishers = (a.mb == 1 && fwht_fast_E(lay.m, a.ma, kLThreads)) ? 1 : std::min(num_sms(), 32);
+    const bool imm = code != QTIP_CODE_HYB && ca.a == (code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&
+                     ca.b == (code == QTIP_CODE_1MAD ? 76625530u : 64248484u);
+    e = cudaErrorInvalidValue;
+#define QTIP_LAYER_CASE(KK, CC)                                                           \
+    if (lay.k == KK && code == CC) e = imm ? launch_layer_t<KK, CC, true>(a, pl.smem, s) \
+                                           : launch_layer_t<KK, CC, false>(a, pl.smem, s);
+    QTIP_LAYER_CASE(2, QTIP_CODE_3INST)
+    QTIP_LAYER_CASE(3, QTIP_CODE_3INST)
+    QTIP_LAYER_CASE(4, QTIP_CODE_3INST)
+    QTIP_LAYER_CASE(2, QTIP_CODE_1MAD)
+    QTIP_LAYER_CASE(3, QTIP_CODE_1MAD)
+    QTIP_LAYER_CASE(4, QTIP_CODE_1MAD)
+    QTIP_LAYER_CASE(2, QTIP_CODE_HYB)
+    QTIP_LAYER_CASE(3, QTIP_CODE_HYB)
+    QTIP_LAYER_CASE(4, QTIP_CODE_HYB)
+#undef QTIP_LAYER_CASE
+    count_launch(1);
+    return e;
+}
+
+}  // namespace qtip

@@ -42,7 +42,7 @@ class QTIPLinear:
     def workspace(self, B):
         if B not in self._ws:
             nb = qtip.workspace_bytes(self.p, self.m, self.n, B)
-            self._ws[B] = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            self._ws[B] = torch.zeros(nb, dtype=torch.uint8, device=self.device)   # grid-barrier counters start at 0
         return self._ws[B]
 
     # ------------------------------------------------------------------ compute
