@@ -260,6 +260,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const bool layer_ok = layer_supported(l, p->code, ca, B, launch_tile_rows, rin && !(flags & QTIP_XT_READY), rout);
     if (g_impl == 5 && !layer_ok)
         return fail(QTIP_ERR_UNSUPPORTED, "fused layer kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB, shared memory fit");
+    const bool gemv6_ok = layer_supported(l, p->code, ca, B, launch_tile_rows, false, false);
+    if (g_impl == 6 && !gemv6_ok)
+        return fail(QTIP_ERR_UNSUPPORTED, "persistent GEMV kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB, shared memory fit");
     int impl = g_impl;
     if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
     if (impl == 0) {
@@ -278,8 +281,34 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     float* yt = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
     int* cnt = (int*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad));
     const int n_rb = (int)(l.m_pad / kCellRows);
-    const int xmode = (use_mma || use_row || impl == 5) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
+    const int xmode = (use_mma || use_row || impl == 5 || impl == 6) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
     cudaError_t e;
+    if (impl == 6) {
+        // RHT-in kernel -> persistent row-owning decode-GEMV (k_layer.cu without its RHT phases,
+        // x~ from the workspace) -> RHT-out kernel
+        float* lws = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) +
+                              align256(4 * B * l.m_pad) + align256(4 * (l.m_pad / kCellRows + 2)));
+        unsigned* bar = (unsigned*)((char*)lws + align256(4 * layer_workspace_floats(l, B, 0)));
+        const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
+        e = cudaSuccess;
+        if (!(flags & QTIP_XT_READY)) {
+            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad);
+            else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
+        const bool prof = g_prof_start && g_prof_stop;
+        if (prof) record_event(g_prof_start, s);
+        e = launch_layer(l, p->code, ca, d_packed, d_lut, d_x, d_sign_n, d_sign_m, rout ? 1.0f : scale, rout ? yt : d_y,
+                         B, row_begin, row_end, false, false, true, (uint32_t*)xt, row_words, lws, bar, s);
+        if (prof) {
+            record_event(g_prof_stop, s);
+            g_prof_start = g_prof_stop = nullptr;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec gemv");
+        if (rout) e = launch_rht(pm, B, d_sign_m, yt, m, d_y, m, 1, scale, s);
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_out");
+        return QTIP_OK;
+    }
     if (impl == 5) {
         // one persistent launch: RHT-in, decode-GEMV, reduction, RHT-out (k_layer.cu)
         float* lws = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) +
@@ -406,6 +435,10 @@ extern "C" int qtip_internal_set_knob(int key, int value) {
     if (key == 2) { qtip::g_layer_debug = value; return 0; }
     if (key == 3) { g_layer_auto = value != 0; return 0; }
     return -1;
+}
+
+extern "C" int qtip_internal_set_layer_trace(void* buf, int cap) {
+    return (int)qtip::set_cta_trace_layer((unsigned long long*)buf, cap);
 }
 
 extern "C" int qtip_internal_set_cta_trace(void* buf, int cap) {

@@ -38,7 +38,7 @@ using namespace mma;
 
 constexpr int kLWarps = 16;
 constexpr int kLThreads = 32 * kLWarps;
-constexpr int kLMaxStages = 8;
+constexpr int kLMaxStages = 16;
 constexpr int kMixChunk = 256;               // outputs per dense-mixing round
 
 struct LayerArgs {
@@ -434,11 +434,10 @@ __device__ __forceinline__ void put_xt(uint32_t* xs, int64_t row_words, int bt, 
 
 __device__ __noinline__ void rht_out_phase(const LayerArgs& args, uint8_t* smem, int64_t c, int64_t P, bool tr);
 
-// 16 warps x 64 registers: half the register file, so the next layer's CTA can become resident
-// under PDL while this one runs (its parameter fetch, prologue and weight requests then overlap
-// this launch instead of following it).
+// 16 warps, up to 128 registers: exactly one CTA of this kernel per SM (the grid is one CTA per
+// SM, and two would not fit), while the small RHT kernels around it can still share the SM.
 template <int K, int CODE, bool kImm>
-__global__ void __launch_bounds__(kLThreads, 2) layer_kernel(const __grid_constant__ LayerArgs args) {
+__global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_constant__ LayerArgs args) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
     constexpr int TW = 8 * K;
@@ -625,34 +624,60 @@ __global__ void __launch_bounds__(kLThreads, 2) layer_kernel(const __grid_consta
     // ---------------------------------------------------------------- GEMV over the warp's units
     const CodeArgs ca = args.ca;
     const Lcg<CODE, kImm> lcg(ca);
-    int st = 0;
-    uint32_t phase = 0;
-    for (UnitIt it = first; it.L < L1i; it.step(n_units)) {
-        float acc[2][1][4] = {{{0.f, 0.f, 0.f, 0.f}}, {{0.f, 0.f, 0.f, 0.f}}};
-        ptx::mbar_wait(ptx::smem_u32(full + st), phase);
-        const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + (size_t)st * chunk_bytes);
+    // B-fragment base of this lane (batch row g, K-slot group tig); lanes with g >= B read a zero
+    // block instead (unit stride 0), so the loop has no predicated loads or zeroing
+    __shared__ __align__(16) uint32_t zero_b[128];
+    if (threadIdx.x < 128) zero_b[threadIdx.x] = 0u;
+    __syncthreads();
+    const bool bval = g < B;
+    const uint32_t* xsl = bval ? xs + g * rw + (kHyb ? 2 : 4) * tig : zero_b + (kHyb ? 2 : 4) * tig;
+    const int ustride = bval ? (kHyb ? 64 : 128) : 0;
+    const uint32_t* lut = args.lut;
+    const uint32_t full0 = ptx::smem_u32(full);
+    const uint8_t* ring0 = ring;
+    auto run = [&](auto kPartSmem) {
+        constexpr bool kSmemPart = decltype(kPartSmem)::value;
+        float* const gpart = args.gpart;
+        const int64_t row0 = args.tile_row0 * kTile;
+        int st = 0;
+        uint32_t phase = 0;
+        for (UnitIt it = first; it.L < L1i; it.step(n_units)) {
+            float acc[2][1][4] = {{{0.f, 0.f, 0.f, 0.f}}, {{0.f, 0.f, 0.f, 0.f}}};
+            ptx::mbar_wait(full0 + 8 * st, phase);
+            const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring0 + (size_t)st * chunk_bytes);
+            const uint32_t* xu = xsl + ustride * it.u;              // x~ of the unit's 8 tile columns
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-            const int J = 8 * it.u + 2 * pp;                        // tile columns J, J + 1
-            uint32_t bf[2][1][4];
-            load_bfrag<1, kHyb>(xs, (int)rw, J, g, tig, B, bf[0]);
-            load_bfrag<1, kHyb>(xs, (int)rw, J + 1, g, tig, B, bf[1]);
-            tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf, acc[pp & 1], g, tig, lcg, ca, args.lut);
-        }
-        __syncwarp();
-        if (lane == 0) issue_next();
-        if (++st == S) { st = 0; phase ^= 1u; }
-        // acc[e] = D[MMA row g + 8 (e >> 1)][batch 2 tig + (e & 1)] <-> tile row 2g + (e >> 1)
+            for (int pp = 0; pp < 4; ++pp) {
+                uint32_t bf[2][1][4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int b = 2 * tig + (e & 1), r = 2 * g + (e >> 1);
-            if (b < B) {
-                const float v = acc[0][0][e] + acc[1][0][e];
-                if (args.part_smem) part[((it.L - L0i) * kTile + r) * B + b] = v;
-                else args.gpart[(b * m_pad + (args.tile_row0 + it.Ir) * kTile + r) * n_units + it.u] = v;
+                for (int t = 0; t < 2; ++t) {
+                    if constexpr (!kHyb) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(xu + 16 * (2 * pp + t));
+                        bf[t][0][0] = v.x; bf[t][0][1] = v.y; bf[t][0][2] = v.z; bf[t][0][3] = v.w;
+                    } else {
+                        const uint2 v = *reinterpret_cast<const uint2*>(xu + 8 * (2 * pp + t));
+                        bf[t][0][0] = v.x; bf[t][0][1] = v.y; bf[t][0][2] = bf[t][0][3] = 0u;
+                    }
+                }
+                tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf, acc[pp & 1], g, tig, lcg, ca, lut);
+            }
+            __syncwarp();
+            if (lane == 0 && iit.L < L1i) issue_next();             // refill (only if the ring was too small)
+            if (++st == S) { st = 0; phase ^= 1u; }
+            // acc[e] = D[MMA row g + 8 (e >> 1)][batch 2 tig + (e & 1)] <-> tile row 2g + (e >> 1)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int b = 2 * tig + (e & 1), r = 2 * g + (e >> 1);
+                if (b < B) {
+                    const float v = acc[0][0][e] + acc[1][0][e];
+                    if constexpr (kSmemPart) part[((it.L - L0i) * kTile + r) * B + b] = v;
+                    else gpart[((int64_t)b * m_pad + row0 + it.Ir * kTile + r) * n_units + it.u] = v;
+                }
             }
         }
-    }
+    };
+    if (args.part_smem) run(std::true_type{});
+    else run(std::false_type{});
     __syncthreads();
     trace_mark(tr, 5);
 
@@ -921,7 +946,7 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
     for (int S = kLMaxStages; S >= 2 && !pick; --S)
         if (layout(S) <= 113 * 1024) pick = S;
     for (int S = kLMaxStages; S >= 2 && !pick; --S)
-        if (layout(S) <= 227 * 1024) pick = S;
+        if (layout(S) <= 225 * 1024) pick = S;                         // + static shared memory
     if (!pick) return false;
     pl->S = pick;
     pl->smem = layout(pick);

@@ -24,11 +24,12 @@ NL = int(sys.argv[5]) if len(sys.argv) > 5 else 4
 B = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 debug = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 pdl = int(sys.argv[8]) if len(sys.argv) > 8 else 1
+impl = int(sys.argv[9]) if len(sys.argv) > 9 else 5
 lib = qtip.load()
 lib.qtip_internal_set_knob(2, debug)
 qtip.set_pdl(bool(pdl))
-qtip.set_matvec_impl(5)
-lib.qtip_internal_set_cta_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
+qtip.set_matvec_impl(impl)
+lib.qtip_internal_set_layer_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 lut = synth.gaussian_lut(9) if code == "hyb" else None
 layers = [QTIPLinear(m, n, code=code, k=k).load_tiles(synth.random_tiles(m, n, k, seed=7 + i),
                                                       synth.random_sign_bytes(m, 1), synth.random_sign_bytes(n, 2),
@@ -51,10 +52,10 @@ for _ in range(3):
 torch.cuda.synchronize()
 cap = 148 * NL * 2
 buf = torch.zeros(1 + 14 * cap, dtype=torch.int64, device="cuda")
-lib.qtip_internal_set_cta_trace(ctypes.c_void_p(buf.data_ptr()), cap)
+lib.qtip_internal_set_layer_trace(ctypes.c_void_p(buf.data_ptr()), cap)
 g.replay()
 torch.cuda.synchronize()
-lib.qtip_internal_set_cta_trace(None, 0)
+lib.qtip_internal_set_layer_trace(None, 0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(10):
@@ -69,7 +70,7 @@ t = rec[:, 2:].astype(np.float64)
 # launches: CTAs sorted by entry time, split into groups of grid size
 order = np.argsort(t[:, 0])
 t = t[order]
-P = cnt // NL
+P = 148
 t0 = t[:, 0].min()
 names = ["entry", "pdl", "staged", "fwht", "x~", "gemv", "red", "prol/sh", "bar2", "ystg", "fwho", "exit"]
 for li in range(NL):

@@ -119,8 +119,8 @@ def _oracle_matvec(tiles, code, k, lut, m, n, x, seed, scale, flags=3, rows=None
                        rht_out=bool(flags & 2), rows=rows)
 
 
-IMPLS = [1, 2, 3, 4, 5]    # CUDA-core reference, tcgen05 (A in TMEM), register-fed mma.sync, row-tile mma.sync,
-                           # fused single-launch layer (RHT-in + GEMV + RHT-out, k_layer.cu)
+IMPLS = [1, 2, 3, 4, 5, 6] # CUDA-core reference, tcgen05 (A in TMEM), register-fed mma.sync, row-tile mma.sync,
+                           # fused single-launch layer (k_layer.cu), RHT kernels around the persistent k_layer GEMV
 
 
 @pytest.mark.parametrize("impl", IMPLS)
@@ -129,7 +129,7 @@ IMPLS = [1, 2, 3, 4, 5]    # CUDA-core reference, tcgen05 (A in TMEM), register-
 def test_matvec_small(cuda_lib, impl, code, k, B):
     if impl != 1 and k == 1:
         pytest.skip("tensor-core kernels cover k = 2..4")
-    if impl in (4, 5) and B > 4:
+    if impl in (4, 5, 6) and B > 4:
         pytest.skip("row-tile and fused layer kernels cover batch 1..4")
     m, n = 384, 768                                          # 3 row blocks x 6 cells
     tiles = synth.random_tiles(m, n, k, seed=11 + k)
@@ -179,7 +179,7 @@ def test_row_shards_are_bitwise_slices(cuda_lib, impl):
     assert np.array_equal(np.concatenate(parts, axis=1), full)
 
 
-@pytest.mark.parametrize("impl", [2, 3, 4, 5])
+@pytest.mark.parametrize("impl", [2, 3, 4, 5, 6])
 @pytest.mark.parametrize("code,k,m,n", [("3inst", 2, 4096, 4096), ("1mad", 2, 11008, 4096), ("3inst", 2, 4096, 11008),
                                         ("hyb", 4, 4096, 4096), ("3inst", 2, 11008, 11008)])
 def test_matvec_full_size_sampled_rows(cuda_lib, impl, code, k, m, n):
