@@ -265,6 +265,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         return fail(QTIP_ERR_UNSUPPORTED, "persistent GEMV kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB, shared memory fit");
     int impl = g_impl;
     if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
+    // measured: for HYB k = 4 the persistent GEMV with the shared-memory LUT
+    // fast path (impl 6) beats the row-tile kernel
+    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && l.k == 4) impl = 6;
     if (impl == 0) {
         // measured: the row-tile kernel wins while its CTAs (one per 16 rows,
         // 8-16 warps each) fill the GPU in one wave; beyond that the split-K kernel balances better
@@ -290,10 +293,11 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
                               align256(4 * B * l.m_pad) + align256(4 * (l.m_pad / kCellRows + 2)));
         unsigned* bar = (unsigned*)((char*)lws + align256(4 * layer_workspace_floats(l, B, 0)));
         const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
+        const int xmode6 = (p->code == QTIP_CODE_HYB && l.k == 4) ? 5 : xmode;   // HYB k = 4: swapped pairs
         e = cudaSuccess;
         if (!(flags & QTIP_XT_READY)) {
-            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad);
-            else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s);
+            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode6, l.n_pad);
+            else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode6, l.n_pad, s);
         }
         if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
         const bool prof = g_prof_start && g_prof_stop;

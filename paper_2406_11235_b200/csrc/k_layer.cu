@@ -68,7 +68,7 @@ struct LayerArgs {
     int stages;
     int max_units_cta;
     int part_smem;                           // unit partials in shared memory (else in gpart)
-    uint32_t off_ring, off_x, off_v, off_red, off_out, off_outred, off_scr;
+    uint32_t off_ring, off_x, off_v, off_red, off_out, off_outred, off_scr, off_lut;
     int finishers;                           // rows mode: CTAs (last arrivals) that run the RHT-out
     int debug;                               // knob 2: bit 0 = run the fast x~ phase twice (cold/warm probe)
 };
@@ -233,7 +233,7 @@ __device__ __forceinline__ void tile_read(const float* scr, int tile, float (&o)
 // one tile of x~ (16 values, already scaled) -> binary16 B-fragment words at dst (16 words
 // K-doubled, 8 words HYB); the 16-B chunks go out in a lane-rotated order (consecutive lanes write
 // consecutive tiles, 64 B apart: rotation spreads a store instruction over 8 bank groups)
-template <bool kHyb>
+template <bool kHyb, bool kSwap = false>
 __device__ __forceinline__ void put_tile(uint32_t* dst, const float (&v)[16]) {
     auto h = [&](int c) { return (uint32_t)__half_as_ushort(__float2half_rn(v[c])); };
     if constexpr (!kHyb) {
@@ -258,7 +258,7 @@ __device__ __forceinline__ void put_tile(uint32_t* dst, const float (&v)[16]) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int ww = 4 * j + k, pr = 4 * (ww & 1) + (ww >> 1);
-                u[k] = h(2 * pr) | (h(2 * pr + 1) << 16);
+                u[k] = kSwap ? (h(2 * pr + 1) | (h(2 * pr) << 16)) : (h(2 * pr) | (h(2 * pr + 1) << 16));
             }
             w[j] = make_uint4(u[0], u[1], u[2], u[3]);
         }
@@ -416,8 +416,8 @@ __device__ __noinline__ void stage_input(float* vb, int dst_stride, const float*
     }
 }
 
-// x~ element (bt, e) -> binary16 in B-fragment order (the RHT kernel's out_mode 3 / 4).
-template <bool kHyb>
+// x~ element (bt, e) -> binary16 in B-fragment order (the RHT kernel's out_mode 3 / 4, or 5 with kSwap).
+template <bool kHyb, bool kSwap = false>
 __device__ __forceinline__ void put_xt(uint32_t* xs, int64_t row_words, int bt, int64_t e, float v) {
     const uint32_t h = __half_as_ushort(__float2half_rn(v));
     const int64_t tile = e >> 4;
@@ -428,7 +428,7 @@ __device__ __forceinline__ void put_xt(uint32_t* xs, int64_t row_words, int bt, 
     } else {
         const int j = c >> 1;
         const int64_t w = tile * 8 + 2 * (j & 3) + (j >> 2);
-        reinterpret_cast<uint16_t*>(xs + bt * row_words)[2 * w + (c & 1)] = (uint16_t)h;
+        reinterpret_cast<uint16_t*>(xs + bt * row_words)[2 * w + ((c & 1) ^ (kSwap ? 1 : 0))] = (uint16_t)h;
     }
 }
 
@@ -440,6 +440,7 @@ template <int K, int CODE, bool kImm>
 __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_constant__ LayerArgs args) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
+    constexpr bool kHybFast = kHyb && K == 4;                      // Q = 9 (layer_supported)
     constexpr int TW = 8 * K;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tig = lane & 3;
@@ -480,14 +481,26 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     };
     const int L0i = (int)L0, L1i = (int)L1;
     UnitIt first{L0i + warp, (L0i + warp) / n_units, (L0i + warp) % n_units};
+    // Weight chunks are fetched by the whole warp with 16-byte cp.async (LDGSTS) into its ring stage,
+    // each lane arriving on the stage's mbarrier when its copies land.  Measured: one
+    // cp.async.bulk per 512-B chunk (lane 0) capped the steady state at 8.6 weights/clk/SM
+    // (scripts/gemv_rate.py); per-lane copies keep many more requests in flight.
     auto issue = [&](const UnitIt& it, int st) {
         const int I = (int)args.tile_row0 + it.Ir;
         const uint32_t bar = ptx::smem_u32(full + st);
-        ptx::mbar_arrive_expect_tx(bar, chunk_bytes);
-        ptx::bulk_g2s(ptx::smem_u32(ring + (size_t)st * chunk_bytes),
-                      args.packed + ((int64_t)(I >> 3) * n_kc + it.u) * (512 * K) + (I & 7) * (64 * K), chunk_bytes, bar);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(
+            args.packed + ((int64_t)(I >> 3) * n_kc + it.u) * (512 * K) + (I & 7) * (64 * K));
+        const uint32_t dst = ptx::smem_u32(ring + (size_t)st * chunk_bytes);
+#pragma unroll
+        for (int q = 0; q < (16 * K + 31) / 32; ++q) {               // 16 K pieces of 16 B
+            const int piece = lane + 32 * q;
+            if (piece < 16 * K)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * piece), "l"(src + 16 * piece)
+                             : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
     };
-    UnitIt iit = first;                                             // issue-side iterator (lane 0)
+    UnitIt iit = first;                                             // issue-side iterator (all lanes)
     int ist = 0;
     auto issue_next = [&]() {
         if (iit.L >= L1i) return;
@@ -496,13 +509,21 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         iit.step(n_units);
     };
     if (lane == 0) {
-        for (int st = 0; st < S; ++st) ptx::mbar_init(ptx::smem_u32(full + st), 1);
+        for (int st = 0; st < S; ++st) ptx::mbar_init(ptx::smem_u32(full + st), 32);
         ptx::fence_mbar_init();
-        for (int st = 0; st < S; ++st) issue_next();
     }
+    __syncwarp();
+    for (int st = 0; st < S; ++st) issue_next();
     __syncwarp();
     trace_mark(tr, 7);
 
+    if constexpr (kHybFast) {                                       // 32-way replicated LUT, words (c0 << 16) | c1
+        uint32_t* lsm = reinterpret_cast<uint32_t*>(smem + args.off_lut);
+        for (int i = threadIdx.x; i < (512 << 5); i += kLThreads) {
+            const uint32_t v = __ldg(args.lut + (i >> 5));
+            lsm[i] = (v << 16) | (v >> 16);
+        }
+    }
     ptx::pdl_wait();                                                // x may be the previous kernel's output
     trace_mark(tr, 1);
 
@@ -520,11 +541,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             const int64_t F = (int64_t)B * len;
             uint32_t* xg = args.xt_g;
             dense_mix(vb, len, args.nb, args.na, args.hb_n, (int)(c * F / P), (int)((c + 1) * F / P), red,
-                      [=](int f, float s) { put_xt<kHyb>(xg, rw, f / len, f % len, s * rs); });
+                      [=](int f, float s) { put_xt<kHyb, kHybFast>(xg, rw, f / len, f % len, s * rs); });
             if (c == 0) {                                           // zero padding columns [n, n_pad)
                 const int pad = (int)(n_pad - n);
                 for (int i = threadIdx.x; i < B * pad; i += kLThreads)
-                    put_xt<kHyb>(args.xt_g, rw, i / pad, n + i % pad, 0.0f);
+                    put_xt<kHyb, kHybFast>(args.xt_g, rw, i / pad, n + i % pad, 0.0f);
             }
             grid_sync(args.bar);
         }
@@ -570,8 +591,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
                         tile_read<E>(scr, tile, o);
 #pragma unroll
                         for (int q = 0; q < 16; ++q) o[q] *= rs;
-                        put_tile<kHyb>(xs + bt * rw + tile * wpt, o);
-                        if (c == 0 && args.xt_g) put_tile<kHyb>(args.xt_g + bt * rw + tile * wpt, o);
+                        put_tile<kHyb, kHybFast>(xs + bt * rw + tile * wpt, o);
+                        if (c == 0 && args.xt_g) put_tile<kHyb, kHybFast>(args.xt_g + bt * rw + tile * wpt, o);
                     }
                     __syncthreads();                                // scr reused by the next batch row
                 };
@@ -583,7 +604,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             }
             for (int i = threadIdx.x; i < B * (np - len); i += kLThreads) {   // zero padding columns
                 const int bt = i / (np - len);
-                put_xt<kHyb>(xs, rw, bt, len + i - bt * (np - len), 0.0f);
+                put_xt<kHyb, kHybFast>(xs, rw, bt, len + i - bt * (np - len), 0.0f);
             }
         } else {
         // x~ in place: vb (fp32, batch stride n_pad, zero padded) and xs share memory; each thread
@@ -609,8 +630,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
                 const int bt = t / tpr, e0 = 16 * (t - bt * tpr);
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
-                    put_xt<kHyb>(xs, rw, bt, e0 + q, v[q]);
-                    if (c == 0 && args.xt_g) put_xt<kHyb>(args.xt_g, rw, bt, e0 + q, v[q]);   // QTIP_XT_READY reuse
+                    put_xt<kHyb, kHybFast>(xs, rw, bt, e0 + q, v[q]);
+                    if (c == 0 && args.xt_g) put_xt<kHyb, kHybFast>(args.xt_g, rw, bt, e0 + q, v[q]);   // QTIP_XT_READY reuse
                 }
             }
             __syncthreads();
@@ -633,6 +654,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     const uint32_t* xsl = bval ? xs + g * rw + (kHyb ? 2 : 4) * tig : zero_b + (kHyb ? 2 : 4) * tig;
     const int ustride = bval ? (kHyb ? 64 : 128) : 0;
     const uint32_t* lut = args.lut;
+    const uint32_t lut_lane = ptx::smem_u32(smem + args.off_lut) + 4u * lane;
+    const mma::HybFastLane hl = mma::hyb_fast_lane(g, tig);
     const uint32_t full0 = ptx::smem_u32(full);
     const uint8_t* ring0 = ring;
     auto run = [&](auto kPartSmem) {
@@ -646,23 +669,41 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             ptx::mbar_wait(full0 + 8 * st, phase);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring0 + (size_t)st * chunk_bytes);
             const uint32_t* xu = xsl + ustride * it.u;              // x~ of the unit's 8 tile columns
+            // all shared-memory operands of the unit are loaded up front (the decode then never waits
+            // on LDS latency in the middle of a tile pair: short_scoreboard stalls in ncu)
+            uint32_t bf[4][2][1][4];
 #pragma unroll
-            for (int pp = 0; pp < 4; ++pp) {
-                uint32_t bf[2][1][4];
+            for (int pp = 0; pp < 4; ++pp)
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     if constexpr (!kHyb) {
                         const uint4 v = *reinterpret_cast<const uint4*>(xu + 16 * (2 * pp + t));
-                        bf[t][0][0] = v.x; bf[t][0][1] = v.y; bf[t][0][2] = v.z; bf[t][0][3] = v.w;
+                        bf[pp][t][0][0] = v.x; bf[pp][t][0][1] = v.y; bf[pp][t][0][2] = v.z; bf[pp][t][0][3] = v.w;
                     } else {
                         const uint2 v = *reinterpret_cast<const uint2*>(xu + 8 * (2 * pp + t));
-                        bf[t][0][0] = v.x; bf[t][0][1] = v.y; bf[t][0][2] = bf[t][0][3] = 0u;
+                        bf[pp][t][0][0] = v.x; bf[pp][t][0][1] = v.y; bf[pp][t][0][2] = bf[pp][t][0][3] = 0u;
                     }
                 }
-                tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf, acc[pp & 1], g, tig, lcg, ca, lut);
+            if constexpr (K == 2 && !kHyb) {
+                uint4 w01[4];
+                uint2 w2[4];
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp) {
+                    w01[pp] = *reinterpret_cast<const uint4*>(chunk + pp * TW * 2 + 2 * (2 * g));
+                    w2[pp] = *reinterpret_cast<const uint2*>(chunk + pp * TW * 2 + 2 * ((2 * g + 2) & 15));
+                }
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp)
+                    tile_pair_k2_words<CODE, 1, kImm>(w01[pp], w2[pp], bf[pp], acc[pp & 1], tig, lcg, ca);
+            } else {
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp) {
+                    if constexpr (kHybFast) tile_pair_hyb4<1>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hl, lut_lane);
+                    else tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], g, tig, lcg, ca, lut);
+                }
             }
             __syncwarp();
-            if (lane == 0 && iit.L < L1i) issue_next();             // refill (only if the ring was too small)
+            if (iit.L < L1i) issue_next();                           // refill (only if the ring was too small)
             if (++st == S) { st = 0; phase ^= 1u; }
             // acc[e] = D[MMA row g + 8 (e >> 1)][batch 2 tig + (e & 1)] <-> tile row 2g + (e >> 1)
 #pragma unroll
@@ -881,6 +922,7 @@ size_t align128(size_t v) { return (v + 127) & ~(size_t)127; }
 // Shared-memory plan; returns 0 when the layer does not fit one CTA per SM.
 struct LayerPlan {
     int U, CP, S, max_units, part_smem;
+    uint32_t off_lut;
     int64_t T;
     int n_units;
     size_t smem;
@@ -911,8 +953,11 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
     const size_t vin_pad = align128((size_t)B * lay.n_pad * 4);
     const size_t red = (size_t)kLWarps * kMixChunk * 4;
     const size_t vout = align128(((size_t)B * lay.m + 31) / 32 * 32 * 4);
+    const size_t lutb = (code == QTIP_CODE_HYB && lay.k == 4) ? (size_t)(512 * 32 * 4) : 0;   // HYB k = 4 fast path
     auto layout = [&](int S) {                                        // offsets for ring depth S; total bytes
         size_t off = head + part;
+        pl->off_lut = (uint32_t)off;
+        off += lutb;
         pl->off_ring = (uint32_t)off;
         off += align128((size_t)kLWarps * S * chunk);
         pl->off_x = (uint32_t)off;
@@ -929,7 +974,7 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
             off += align128((size_t)lay.n_pad * 4);
         }
         const size_t endA = off;
-        size_t endB = head;                                           // RHT-out aliases everything after head
+        size_t endB = head + part + lutb;                             // RHT-out aliases everything after the LUT
         if (rht_out) {
             pl->off_out = (uint32_t)endB;
             endB += vout;
@@ -967,6 +1012,7 @@ bool layer_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B,
                      bool rht_out) {
     if (B < 1 || B > 4 || lay.k < 2 || lay.k > 4) return false;
     if (code == QTIP_CODE_HYB && ca.two_sign) return false;
+    if (code == QTIP_CODE_HYB && lay.k == 4 && ca.Q != 9) return false;   // fast path: 2^9-entry LUT
     if (lay.n > (1 << 24) / 4 || lay.m > (1 << 24) / 4 || num_sms() > 256) return false;
     int nb = 1, na = 0, mb = 1, ma = 0;
     if (rht_in && !hadamard_factor(lay.n, &nb, &na)) return false;
@@ -1040,6 +1086,7 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
     a.off_out = pl.off_out;
     a.off_outred = pl.off_outred;
     a.off_scr = pl.off_scr;
+    a.off_lut = pl.off_lut;
     a.debug = g_layer_debug;
     a.finishers = (a.mb == 1 && fwht_fast_E(lay.m, a.ma, kLThreads)) ? 1 : std::min(num_sms(), 32);
     const bool imm = code != QTIP_CODE_HYB && ca.a == (code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&

@@ -24,6 +24,7 @@ namespace qtip {
 
 constexpr int kRhtThreads = 256;
 
+// out_mode 5 = mode 4 with the halves of every pair word swapped (HYB k = 4 fast path, k_layer.cu).
 // out_mode 0: float32; 1: binary16 duplicated into both halves of a 32-bit word (the K-doubled
 // UMMA B operand); 2: binary16; 3 / 4: modes 1 / 2 permuted into mma.sync B-fragment order
 // within each 16-column tile (k_gemv_mma.cu): mode 3 puts columns (2t, 2t+8, 2t+1, 2t+9) at
@@ -47,7 +48,8 @@ __device__ __forceinline__ void store_out(void* out, int mode, int64_t row, int6
     } else {
         const int j = c >> 1;                                  // column pair
         const int64_t w = tile * 8 + 2 * (j & 3) + (j >> 2);
-        static_cast<uint16_t*>(out)[row + 2 * w + (c & 1)] = (uint16_t)h;
+        // mode 5 (HYB fast path): the two halves of each pair word swapped (LUT words (c0 << 16) | c1)
+        static_cast<uint16_t*>(out)[row + 2 * w + ((c & 1) ^ (mode == 5 ? 1 : 0))] = (uint16_t)h;
     }
 }
 

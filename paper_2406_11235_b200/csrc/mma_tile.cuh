@@ -121,6 +121,33 @@ __device__ __forceinline__ void load_bfrag(const uint32_t* xs, int row_words, in
     }
 }
 
+// k = 2 3INST / 1MAD tile pair from preloaded words: w01 = words (2g, 2g+1) of both tiles
+// (interleaved: .x/.y word 2g of tiles 0/1, .z/.w word 2g+1), w2 = word 2g+2 (mod 16) of both.
+template <int CODE, int NG, bool kImm>
+__device__ __forceinline__ void tile_pair_k2_words(const uint4 w01, const uint2 w2, const uint32_t (&bf)[2][NG][4],
+                                                   float (&acc)[NG][4], int tig, const Lcg<CODE, kImm>& lcg,
+                                                   const CodeArgs& ca) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const uint32_t W0 = t ? w01.y : w01.x, W1 = t ? w01.w : w01.z, W2 = t ? w2.y : w2.x;
+        const uint32_t A0 = __funnelshift_l(W1, W0, 4 * tig);   // row 2g, from bit 4 tig
+        const uint32_t A1 = __funnelshift_l(W1, W0, 4 * tig + 2);
+        const uint32_t C0 = __funnelshift_l(W2, W1, 4 * tig);   // row 2g+1
+        const uint32_t C1 = __funnelshift_l(W2, W1, 4 * tig + 2);
+        uint32_t z00, z08, z01, z09, z10, z18, z11, z19;        // z<row><col offset>
+        constexpr bool kLoFma = CODE == QTIP_CODE_3INST;
+        lcg_pair<CODE, kLoFma, kImm>(A0, lcg, ca.magic, z00, z08);
+        lcg_pair<CODE, kLoFma, kImm>(A1, lcg, ca.magic, z01, z09);
+        lcg_pair<CODE, kLoFma, kImm>(C0, lcg, ca.magic, z10, z18);
+        lcg_pair<CODE, kLoFma, kImm>(C1, lcg, ca.magic, z11, z19);
+#pragma unroll
+        for (int ng = 0; ng < NG; ++ng) {
+            hmma_16816(acc[ng], z00, z10, z08, z18, bf[t][ng][0], bf[t][ng][1]);
+            hmma_16816(acc[ng], z01, z11, z09, z19, bf[t][ng][2], bf[t][ng][3]);
+        }
+    }
+}
+
 // acc[ng] += W~(tiles t = 0, 1 of a tile pair) x~: pw = the pair's interleaved words (word w of
 // tile t at pw[2w + t], TW = 8K words per tile), bf[t] the B fragments of tile t.
 template <int K, int CODE, int NG, bool kImm>
@@ -133,25 +160,7 @@ __device__ __forceinline__ void tile_pair(const uint32_t* pw, const uint32_t (&b
         // tile rows 2g, 2g+1 use words 2g, 2g+1, 2g+2 (mod 16) of each tile
         const uint4 w01 = *reinterpret_cast<const uint4*>(pw + 2 * (2 * g));
         const uint2 w2 = *reinterpret_cast<const uint2*>(pw + 2 * ((2 * g + 2) & 15));
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const uint32_t W0 = t ? w01.y : w01.x, W1 = t ? w01.w : w01.z, W2 = t ? w2.y : w2.x;
-            const uint32_t A0 = __funnelshift_l(W1, W0, 4 * tig);   // row 2g, from bit 4 tig
-            const uint32_t A1 = __funnelshift_l(W1, W0, 4 * tig + 2);
-            const uint32_t C0 = __funnelshift_l(W2, W1, 4 * tig);   // row 2g+1
-            const uint32_t C1 = __funnelshift_l(W2, W1, 4 * tig + 2);
-            uint32_t z00, z08, z01, z09, z10, z18, z11, z19;        // z<row><col offset>
-            constexpr bool kLoFma = CODE == QTIP_CODE_3INST;
-            lcg_pair<CODE, kLoFma, kImm>(A0, lcg, ca.magic, z00, z08);
-            lcg_pair<CODE, kLoFma, kImm>(A1, lcg, ca.magic, z01, z09);
-            lcg_pair<CODE, kLoFma, kImm>(C0, lcg, ca.magic, z10, z18);
-            lcg_pair<CODE, kLoFma, kImm>(C1, lcg, ca.magic, z11, z19);
-#pragma unroll
-            for (int ng = 0; ng < NG; ++ng) {
-                hmma_16816(acc[ng], z00, z10, z08, z18, bf[t][ng][0], bf[t][ng][1]);
-                hmma_16816(acc[ng], z01, z11, z09, z19, bf[t][ng][2], bf[t][ng][3]);
-            }
-        }
+        tile_pair_k2_words<CODE, NG, kImm>(w01, w2, bf, acc, tig, lcg, ca);
     } else {
         // general k: three words per tile row (rows 2g, 2g+1)
 #pragma unroll
@@ -183,6 +192,70 @@ __device__ __forceinline__ void tile_pair(const uint32_t* pw, const uint32_t (&b
             }
         }
     }
+}
+
+// HYB, k = 4, V = 2, Q = 9 fast path (Alg. 3).  Lane (g, tig) owns tile rows
+// 2g + rr (MMA rows g, g + 8) and the column pairs tig, tig + 4 of each row: pair windows at bit
+// offsets 64 rho + 8 tig and + 32 of the tile stream.  With qa = (64 rho + 8 tig - 16) >> 5 and
+// n = (64 rho + 8 tig - 16) & 31 (lane constants; qa = -1 wraps to the last word: those bits are
+// above the window and HYB ignores them), x1 = funnel(W[qa+1], W[qa], n) and x2 = funnel(W[qa+2],
+// W[qa+1], n) hold the windows in their low 16 bits -- one SHF per pair of weights, no zero fill:
+// x^2 + x mod 2^16 depends on x mod 2^16 only.  The LUT lives in shared memory replicated 32x
+// (entry e of replica r at word 32 e + r, conflict-free) as (c0 << 16) | c1, so the sign flip of
+// Alg. 3 is a single LOP3 on bit 15 and the address is ((h + h) & 0xFF80) + 4 lane; the A words
+// are then (c1, c0) per column pair and x~ comes with the pair halves swapped (RHT out_mode 5).
+struct HybFastLane {
+    int wa[2];          // word offsets (2 * word index, pair-interleaved) of W[qa], per row rr
+    int wb[2], wc[2];   // W[qa + 1], W[qa + 2]
+    uint32_t n;         // funnel amount (same for both rows)
+};
+
+__device__ __forceinline__ HybFastLane hyb_fast_lane(int g, int tig) {
+    HybFastLane hl;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const int s = 64 * (2 * g + rr) + 8 * tig - 16;
+        const int q = s >> 5;                                  // arithmetic: -1 for s < 0
+        hl.wa[rr] = 2 * ((q + 32) & 31);
+        hl.wb[rr] = 2 * ((q + 33) & 31);
+        hl.wc[rr] = 2 * ((q + 34) & 31);
+        hl.n = (uint32_t)(s & 31);
+    }
+    return hl;
+}
+
+__device__ __forceinline__ uint32_t hyb_fast_word(uint32_t x, uint32_t lut_lane) {
+    const uint32_t h = x * x + x;
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut_lane + ((h + h) & 0xFF80u)));
+    uint32_t w;
+    asm("lop3.b32 %0, %1, %2, 0x8000, 0x78;" : "=r"(w) : "r"(v), "r"(h));      // v ^ (h & 0x8000)
+    return w;
+}
+
+// acc += W~(tiles t = 0, 1 of a pair) x~ for the HYB k = 4 fast path; pw = the pair's words,
+// lut_lane = shared-memory address of this lane's LUT replica, bf[t] from x~ mode 5.
+template <int NG>
+__device__ __forceinline__ void tile_pair_hyb4(const uint32_t* pw, const uint32_t (&bf)[2][NG][4], float (&acc)[NG][4],
+                                               const HybFastLane& hl, uint32_t lut_lane) {
+    uint32_t z[2][2][2];                                       // [tile][row rr][pair: tig, tig + 4]
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint2 A = *reinterpret_cast<const uint2*>(pw + hl.wa[rr]);
+        const uint2 Bw = *reinterpret_cast<const uint2*>(pw + hl.wb[rr]);
+        const uint2 C = *reinterpret_cast<const uint2*>(pw + hl.wc[rr]);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const uint32_t a = t ? A.y : A.x, b = t ? Bw.y : Bw.x, c = t ? C.y : C.x;
+            z[t][rr][0] = hyb_fast_word(__funnelshift_l(b, a, hl.n), lut_lane);
+            z[t][rr][1] = hyb_fast_word(__funnelshift_l(c, b, hl.n), lut_lane);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int ng = 0; ng < NG; ++ng)
+            hmma_16816(acc[ng], z[t][0][0], z[t][1][0], z[t][0][1], z[t][1][1], bf[t][ng][0], bf[t][ng][1]);
 }
 
 }  // namespace mma
