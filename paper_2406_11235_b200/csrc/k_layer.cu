@@ -476,7 +476,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         __device__ __forceinline__ void step(int n_units) {
             L += kLWarps;
             u += kLWarps;
-            while (u >= n_units) { u -= n_units; ++Ir; }
+            if (u >= n_units) {                                     // n_units >= 16: at most one wrap
+                u -= n_units;
+                ++Ir;
+                while (u >= n_units) { u -= n_units; ++Ir; }        // narrow layers only
+            }
         }
     };
     const int L0i = (int)L0, L1i = (int)L1;
@@ -658,6 +662,15 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     const mma::HybFastLane hl = mma::hyb_fast_lane(g, tig);
     const uint32_t full0 = ptx::smem_u32(full);
     const uint8_t* ring0 = ring;
+    const uint32_t part_u32 = ptx::smem_u32(part);
+    uint32_t poff[4];
+    bool pok[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int b = 2 * tig + (e & 1), r = 2 * g + (e >> 1);
+        pok[e] = b < B;
+        poff[e] = (uint32_t)(r * B + (b < B ? b : 0)) * 4u;
+    }
     auto run = [&](auto kPartSmem) {
         constexpr bool kSmemPart = decltype(kPartSmem)::value;
         float* const gpart = args.gpart;
@@ -705,14 +718,21 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             __syncwarp();
             if (iit.L < L1i) issue_next();                           // refill (only if the ring was too small)
             if (++st == S) { st = 0; phase ^= 1u; }
-            // acc[e] = D[MMA row g + 8 (e >> 1)][batch 2 tig + (e & 1)] <-> tile row 2g + (e >> 1)
+            // acc[e] = D[MMA row g + 8 (e >> 1)][batch 2 tig + (e & 1)] <-> tile row 2g + (e >> 1);
+            // branch-free predicated stores (lane-constant offsets and predicates)
+            if constexpr (kSmemPart) {
+                const uint32_t ub = part_u32 + (uint32_t)(it.L - L0i) * (uint32_t)(kTile * 4 * B);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int b = 2 * tig + (e & 1), r = 2 * g + (e >> 1);
-                if (b < B) {
+                for (int e = 0; e < 4; ++e) {
                     const float v = acc[0][0][e] + acc[1][0][e];
-                    if constexpr (kSmemPart) part[((it.L - L0i) * kTile + r) * B + b] = v;
-                    else gpart[((int64_t)b * m_pad + row0 + it.Ir * kTile + r) * n_units + it.u] = v;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.f32 [%0], %1;\n\t}"
+                                 ::"r"(ub + poff[e]), "f"(v), "r"((uint32_t)pok[e]) : "memory");
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int b = 2 * tig + (e & 1), r = 2 * g + (e >> 1);
+                    if (b < B) gpart[((int64_t)b * m_pad + row0 + it.Ir * kTile + r) * n_units + it.u] = acc[0][0][e] + acc[1][0][e];
                 }
             }
         }

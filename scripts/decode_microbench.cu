@@ -18,10 +18,10 @@ constexpr int N_IT = 256;
 // into TMEM (the tcgen05 path's data movement, no MMA)
 template <int NACC, int MODE = 0>
 __global__ void loop(const uint32_t* __restrict__ src, float* out, long long* cyc) {
-    __shared__ __align__(16) uint32_t chunk[4 * 64];      // 4 tile pairs (k = 2: 32 words each)
-    __shared__ __align__(16) uint32_t xs[128];             // x~ of 8 tiles (fragment order, K-doubled)
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) chunk[i] = src[i];
-    for (int i = threadIdx.x; i < 128; i += blockDim.x) xs[i] = 0x3c003c00u;
+    __shared__ __align__(16) uint32_t chunk[8 * 4 * 64];  // 8 units x 4 tile pairs (k = 2: 32 words each)
+    __shared__ __align__(16) uint32_t xs[8 * 128];         // x~ of 8 x 8 tiles (fragment order, K-doubled)
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) chunk[i] = src[i & 1023];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) xs[i] = 0x3c003c00u;
     __syncthreads();
     const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     CodeArgs ca;
@@ -45,10 +45,11 @@ __global__ void loop(const uint32_t* __restrict__ src, float* out, long long* cy
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp) {
             uint32_t bf[2][1][4];
-            load_bfrag<1, false>(xs, 128, 2 * pp, g, tig, 1, bf[0]);
-            load_bfrag<1, false>(xs, 128, 2 * pp + 1, g, tig, 1, bf[1]);
+            const int ub = (it + (threadIdx.x >> 5)) & 7;            // a different unit every iteration (no hoisting)
+            load_bfrag<1, false>(xs + 128 * ub, 128, 2 * pp, g, tig, 1, bf[0]);
+            load_bfrag<1, false>(xs + 128 * ub, 128, 2 * pp + 1, g, tig, 1, bf[1]);
             if constexpr (MODE == 0) {
-                tile_pair<2, QTIP_CODE_3INST, 1, true>(chunk + pp * 32, bf, acc[pp % NACC], g, tig, lcg, ca, nullptr);
+                tile_pair<2, QTIP_CODE_3INST, 1, true>(chunk + 256 * ub + pp * 32, bf, acc[pp % NACC], g, tig, lcg, ca, nullptr);
             } else if constexpr (MODE == 1) {
                 const uint4 w = *reinterpret_cast<const uint4*>(chunk + pp * 32 + 4 * g);
 #pragma unroll
