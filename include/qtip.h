@@ -133,9 +133,31 @@ qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d
 /* The Hadamard factorisation used for order n: n = b * 2^a.  QTIP_ERR_SHAPE if none. */
 qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a);
 
+/* Tail-biting trellis quantizer (P:127-141 Viterbi DP; Algorithm 4): for each of nseq
+ * independent length-T source sequences, the walk returned by Algorithm 4 -- rotate the sequence
+ * right by floor(T/2), run the unconstrained Viterbi, take the L-kV bit overlap O at the seam
+ * (reading R3: bottom L-kV bits of the rotated walk's state at 1-indexed position floor(T/2)),
+ * then run the Viterbi on the original sequence with the first state's top and the last state's
+ * bottom L-kV bits both equal to O (a tail-biting walk).
+ *   p: L = 16, V = 1, k in {2, 3}, code 3INST or 1MAD (else QTIP_ERR_UNSUPPORTED).
+ *   d_source: DEVICE float32 [nseq][T], already in code units (the caller scales the source by
+ *     the code's state standard deviation, reading R9); d_states: DEVICE uint32 [nseq][T] walk
+ *     (feed to qtip_pack_states after copying to the host); d_cost: DEVICE float32 [nseq], the
+ *     walk's squared error sum.
+ *   Arithmetic: code values C_y are the binary16 codes of qtip_decode widened to binary32; the DP
+ *     is binary32 with each operation rounded separately, ties to the smallest predecessor index
+ *     and the smallest final state (reading R4), as oracle/viterbi.c qo_viterbi_f32 (R17).
+ *   d_workspace: qtip_viterbi_workspace_bytes(p, T) bytes, caller-owned (backpointers). */
+size_t qtip_viterbi_workspace_bytes(const qtip_params* p, int64_t T);
+qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T, const float* d_source,
+                                  uint32_t* d_states, float* d_cost, void* d_workspace, size_t workspace_bytes,
+                                  void* stream);
+
 /* Selects the matvec kernel: 0 = auto (the measured-fastest supported kernel), 1 = CUDA-core
  * reference kernel, 2 = tcgen05 kernel (A in TMEM), 3 = register-fed mma.sync kernel with
- * split-K over 128-column cells, 4 = row-tile mma.sync kernel (one CTA per 16 rows, B <= 4).
+ * split-K over 128-column cells, 4 = row-tile mma.sync kernel (one CTA per 16 rows, B <= 4),
+ * 5 = fused single-launch layer kernel (RHT-in, GEMV, RHT-out with in-kernel grid barriers),
+ * 6 = RHT kernels around the persistent row-owning GEMV of 5 (HYB k = 4 auto choice).
  * Process-wide; for ablations and tests. */
 void qtip_set_matvec_impl(int impl);
 int qtip_get_matvec_impl(void);

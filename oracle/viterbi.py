@@ -35,6 +35,11 @@ def _load():
                                                           ctypes.c_void_p]
         _lib.qo_viterbi_batch.restype = None
         _lib.qo_viterbi_batch.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_int] + [ctypes.c_void_p] * 4
+        _lib.qo_viterbi_f32.restype = ctypes.c_float
+        _lib.qo_viterbi_f32.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long,
+                                                              ctypes.c_void_p]
+        _lib.qo_viterbi_f32_batch.restype = None
+        _lib.qo_viterbi_f32_batch.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_int] + [ctypes.c_void_p] * 4
     return _lib
 
 
@@ -146,3 +151,41 @@ def brute_force(s, L, k, V, code_table, tail_biting=False):
 def reconstruct(states, code_table, L, V):
     tab = _table(code_table, L, V)
     return tab[np.asarray(states, dtype=np.int64)].reshape(-1)
+
+
+# ------------------------------------------------------------------ binary32 variant (reading R17)
+def viterbi_f32(s, L, k, V, code_table, overlap=None):
+    """Viterbi with every cost operation in binary32 (same order as viterbi())."""
+    lib = _load()
+    s = np.ascontiguousarray(np.asarray(s, dtype=np.float32))
+    n = len(s) // V
+    tab = np.ascontiguousarray(np.asarray(code_table, dtype=np.float32).reshape(1 << L, V))
+    out = np.zeros(n, dtype=np.uint32)
+    cost = lib.qo_viterbi_f32(L, k * V, V, n, tab.ctypes.data, s.ctypes.data, -1 if overlap is None else int(overlap),
+                              out.ctypes.data)
+    return out, float(cost)
+
+
+def viterbi_f32_batch(S, L, k, V, code_table, overlaps=None):
+    lib = _load()
+    S = np.ascontiguousarray(np.asarray(S, dtype=np.float32))
+    nseq, T = S.shape
+    n = T // V
+    tab = np.ascontiguousarray(np.asarray(code_table, dtype=np.float32).reshape(1 << L, V))
+    ov = np.full(nseq, -1, dtype=np.int64) if overlaps is None else np.ascontiguousarray(overlaps, dtype=np.int64)
+    out = np.zeros((nseq, n), dtype=np.uint32)
+    cost = np.zeros(nseq, dtype=np.float32)
+    lib.qo_viterbi_f32_batch(L, k * V, V, n, tab.ctypes.data, nseq, S.ctypes.data, ov.ctypes.data, out.ctypes.data,
+                             cost.ctypes.data)
+    return out, cost
+
+
+def tailbite_encode_f32_batch(S, L, k, V, code_table):
+    """Algorithm 4 with the binary32 DP: rotate right by floor(T/2), unconstrained
+    Viterbi, seam overlap (reading R3), constrained Viterbi on the original sequence."""
+    S = np.asarray(S, dtype=np.float32)
+    T = S.shape[1]
+    S_rot = np.roll(S, T // 2, axis=1)
+    st_rot, _ = viterbi_f32_batch(S_rot, L, k, V, code_table)
+    O = np.array([seam_overlap(r, T, L, k, V) for r in st_rot], dtype=np.int64)
+    return viterbi_f32_batch(S, L, k, V, code_table, overlaps=O)

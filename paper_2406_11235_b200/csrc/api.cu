@@ -391,6 +391,27 @@ qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d
     return QTIP_OK;
 }
 
+size_t qtip_viterbi_workspace_bytes(const qtip_params* p, int64_t T) {
+    if (qtip_params_check(p) != QTIP_OK || T < 1) return 0;
+    return viterbi_workspace_bytes((int)T);
+}
+
+qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T, const float* d_source,
+                                  uint32_t* d_states, float* d_cost, void* d_workspace, size_t workspace_bytes,
+                                  void* stream) {
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if (!viterbi_supported(p->code, p->k, p->V, p->L))
+        return fail(QTIP_ERR_UNSUPPORTED, "GPU quantizer: L = 16, V = 1, k in {2, 3}, 3INST or 1MAD");
+    if (nseq < 1 || T < 2 || T > 4096 || nseq > (1 << 30)) return fail(QTIP_ERR_SHAPE, "need nseq >= 1, 2 <= T <= 4096");
+    if (!d_source || !d_states || !d_cost || !d_workspace) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (workspace_bytes < viterbi_workspace_bytes((int)T)) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
+    const cudaError_t e = launch_viterbi(p->code, p->k * p->V, code_args(p), d_source, (int)nseq, (int)T, d_states,
+                                         d_cost, d_workspace, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_viterbi_tailbite");
+    return QTIP_OK;
+}
+
 qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a) {
     int bb, aa;
     if (!b || !a) return fail(QTIP_ERR_INVALID_PARAMS, "NULL output");

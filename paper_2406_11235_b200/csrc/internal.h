@@ -118,6 +118,13 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
                          int64_t B, int64_t row_begin, int64_t row_end, bool rht_in, bool rht_out, bool xt_ready,
                          uint32_t* xt_g, int64_t row_words, float* ws_f, unsigned* bar, cudaStream_t s);
 
+// Tail-biting trellis quantizer (k_viterbi.cu): Algorithm 4 per sequence of T source values (in
+// code units), binary32 DP.  ws: viterbi_workspace_bytes(T) bytes (backpointers, per CTA).
+bool viterbi_supported(int code, int k, int V, int L);
+size_t viterbi_workspace_bytes(int T);
+cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, int nseq, int T, uint32_t* states,
+                           float* cost, void* ws, cudaStream_t s);
+
 // Debug CTA timelines (trace.cuh), per translation unit.
 cudaError_t set_cta_trace_rht(unsigned long long* buf, int cap);
 cudaError_t set_cta_trace_mma(unsigned long long* buf, int cap);

@@ -1,0 +1,212 @@
+// k_viterbi.cu -- tail-biting trellis quantizer on the GPU (PAPER.md:127-141 Viterbi, :331-353
+// Algorithm 4), the step that produces the packed streams the GEMV decodes (SURVEY.md 8(f)
+// NEXT-1).  L = 16, V = 1, kV in {2, 3}; one CTA (1024 threads) per sequence at a time,
+// persistent over the batch.
+//
+// The DP: V_t(y) = min over the 2^kV predecessors x = c 2^(L-kV) + (y >> kV) of
+// V_{t-1}(x), plus (C_y - s_t)^2.  States sharing a group q = y >> kV share their predecessor
+// set P(q) = {c 2^(L-kV) + q}, so a step is: m_t(q) = min_{x in P(q)} V_{t-1}(x) for the
+// 2^(L-kV) groups, V_t(y) = m_t(y >> kV) + d(y, t).  Ownership follows the de Bruijn structure:
+// "base" b in [0, 2^(L-2kV)) owns the groups c 2^(L-2kV) + b (c < 2^kV) and their 2^(2kV)
+// states, which are exactly P((b << kV) | j) for j < 2^kV.  So the owner of b turns the minima
+// of its own groups (read from shared memory) straight into the next minima of the groups
+// (b << kV) | j -- V_t itself is never stored -- and writes those back after a barrier.  Per
+// thread: 64 states; per step its 2^kV x (bases per thread) minima in, the same number out,
+// 64 x (convert, sub, mul, add, compare).  The code values C_y = fp32(binary16 code(y))
+// (bit-exact with qtip_decode) sit in shared memory; the argmins (kV bits per group, one u32
+// per thread per step) go to a per-CTA global backpointer array walked back at the end.
+//
+// Arithmetic is binary32 with every operation rounded on its own (no FMA contraction), in the
+// order of the oracle's binary32 DP (oracle/viterbi.c qo_viterbi_f32, reading R17): ties go to
+// the smallest predecessor index c and the smallest final state (reading R4).
+#include "decode.cuh"
+#include "internal.h"
+
+namespace qtip {
+namespace {
+
+constexpr int kVThreads = 1024;
+constexpr int kVStates = 64;                   // states per thread (2^16 / 1024)
+
+struct ViterbiArgs {
+    CodeArgs ca;
+    int code;
+    const float* src;                          // [nseq][T], in code units
+    int nseq, T;
+    uint32_t* states;                          // [nseq][T]
+    float* cost;                               // [nseq]
+    uint32_t* bp;                              // per CTA: [T][kVThreads] words
+};
+
+__device__ __forceinline__ __half code_half(uint32_t y, const CodeArgs& ca, int code) {
+    if (code == QTIP_CODE_3INST) return inst3_value(inst3_word(y, ca.a, ca.b, ca.magic));
+    return onemad_value(onemad_sum(y, ca.a, ca.b));
+}
+
+template <int KV>
+__global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs args) {
+    constexpr int L = 16;
+    constexpr int SH = L - KV;                         // group index bits
+    constexpr int NB = 1 << (L - 2 * KV);              // bases
+    constexpr int BPT = NB / kVThreads;                // bases per thread (2^(6 - 2kV))
+    constexpr int NC = 1 << KV;
+    static_assert(BPT * NC * NC == kVStates, "64 states per thread");
+    extern __shared__ __align__(16) float sm[];
+    float* M = sm;                                     // [2^SH] group minima
+    __half* codeh = reinterpret_cast<__half*>(sm + (1 << SH));   // [1024][64] this thread's C_y
+    float* s_src = sm + (1 << SH) + kVThreads * kVStates / 2;    // [T] source of the pass
+    __shared__ float red_v[32];
+    __shared__ uint32_t red_i[32];
+    __shared__ uint32_t s_state;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int T = args.T;
+    uint32_t* bp = args.bp + (size_t)blockIdx.x * T * kVThreads;
+    // slot i = (bb NC + c) NC + j <-> base b = tid BPT + bb, group q = c NB + b, state (q << KV) | j
+    auto state_of = [&](int i) {
+        const int bb = i / (NC * NC), c = (i / NC) % NC, j = i % NC;
+        return ((uint32_t)(c * NB + tid * BPT + bb) << KV) | (uint32_t)j;
+    };
+    __half* myc = codeh + tid * kVStates;
+#pragma unroll 4
+    for (int i = 0; i < kVStates; ++i) myc[i] = code_half(state_of(i), args.ca, args.code);
+
+    for (int seq = blockIdx.x; seq < args.nseq; seq += gridDim.x) {
+        const float* s = args.src + (size_t)seq * T;
+        uint32_t O = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            // pass 0: s rotated right by floor(T/2), free ends; pass 1: s, overlap O at both ends
+            __syncthreads();
+            for (int t = tid; t < T; t += kVThreads) s_src[t] = pass ? s[t] : s[(t - T / 2 + T) % T];
+            __syncthreads();
+            // m for step 1: the minima over P(q') of V_0, V_0(y) = d(y, 0) (or inf off the start set)
+            float m[BPT * NC];                              // this thread's group minima (c, bb)
+            for (int t = 1; t < T; ++t) {
+                // V_{t-1}(y) = m_{t-1}(q(y)) + d(y, t-1) folded into the minima m_t of (b << KV) | j
+                const float st = s_src[t - 1];
+                uint32_t word = 0;
+#pragma unroll
+                for (int bb = 0; bb < BPT; ++bb)
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) {
+                        float best = INFINITY;
+                        uint32_t bc = 0;
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) {
+                            const int i = (bb * NC + c) * NC + j;
+                            const float e = __fsub_rn(__half2float(myc[i]), st);
+                            const float d = __fmul_rn(e, e);
+                            float x;
+                            if (t == 1) x = (pass == 0 || (uint32_t)(c * NB + tid * BPT + bb) == O) ? d : INFINITY;
+                            else x = __fadd_rn(m[c * BPT + bb], d);
+                            if (x < best) { best = x; bc = c; }
+                        }
+                        M[((tid * BPT + bb) << KV) | j] = best;
+                        word |= bc << ((bb * NC + j) * KV);
+                    }
+                bp[(size_t)t * kVThreads + tid] = word;
+                __syncthreads();
+#pragma unroll
+                for (int bb = 0; bb < BPT; ++bb)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) m[c * BPT + bb] = M[c * NB + tid * BPT + bb];
+                __syncthreads();                                // M is rewritten by the next step
+            }
+            // final state (recomputed V_{T-1}): smallest cost, then smallest index
+            float best = INFINITY;
+            uint32_t by = 0xFFFFFFFFu;
+            {
+                const float st = s_src[T - 1];
+#pragma unroll
+                for (int i = 0; i < kVStates; ++i) {
+                    const int bb = i / (NC * NC), c = (i / NC) % NC;
+                    const uint32_t y = state_of(i);
+                    const float e = __fsub_rn(__half2float(myc[i]), st);
+                    const float d = __fmul_rn(e, e);
+                    float x = T == 1 ? ((pass == 0 || (y >> KV) == O) ? d : INFINITY) : __fadd_rn(m[c * BPT + bb], d);
+                    const bool ok = pass == 0 || (y & ((1u << SH) - 1u)) == O;
+                    if (ok && (x < best || (x == best && y < by))) { best = x; by = y; }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const uint32_t oy = __shfl_xor_sync(0xffffffffu, by, o);
+                if (ob < best || (ob == best && oy < by)) { best = ob; by = oy; }
+            }
+            if (lane == 0) { red_v[warp] = best; red_i[warp] = by; }
+            __syncthreads();
+            if (warp == 0) {
+                best = red_v[lane];
+                by = red_i[lane];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const uint32_t oy = __shfl_xor_sync(0xffffffffu, by, o);
+                    if (ob < best || (ob == best && oy < by)) { best = ob; by = oy; }
+                }
+                if (lane == 0) {
+                    // no finite walk (tail-biting infeasible, kT < L): state 0, as the oracle's strict <
+                    if (!(best < INFINITY)) by = 0;
+                    // backpointers: group q of y -> base q >> KV (thread (q >> KV) / BPT), slot q & (NC-1)
+                    uint32_t y = by;
+                    const int g = T / 2;                    // Alg. 4 seam: 1-indexed group floor(T/(2V)) (R3)
+                    if (pass == 1) {
+                        args.states[(size_t)seq * T + T - 1] = y;
+                        args.cost[seq] = best;
+                    }
+                    if (pass == 0 && g - 1 == T - 1) s_state = y & ((1u << SH) - 1u);
+                    for (int t = T - 1; t >= 1; --t) {
+                        const uint32_t q = y >> KV;
+                        const uint32_t b = q >> KV, jj = q & (NC - 1);
+                        const uint32_t w = __ldcg(bp + (size_t)t * kVThreads + b / BPT);
+                        const uint32_t c = (w >> (((b % BPT) * NC + jj) * KV)) & (NC - 1);
+                        y = (c << SH) | q;
+                        if (pass == 1) args.states[(size_t)seq * T + t - 1] = y;
+                        if (pass == 0 && t - 1 == g - 1) {
+                            s_state = y & ((1u << SH) - 1u);
+                            break;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            O = s_state;
+        }
+    }
+}
+
+}  // namespace
+
+size_t viterbi_workspace_bytes(int T) { return (size_t)num_sms() * T * kVThreads * 4; }
+
+bool viterbi_supported(int code, int k, int V, int L) {
+    return L == 16 && V == 1 && (k == 2 || k == 3) && (code == QTIP_CODE_3INST || code == QTIP_CODE_1MAD);
+}
+
+cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, int nseq, int T, uint32_t* states,
+                           float* cost, void* ws, cudaStream_t s) {
+    ViterbiArgs a;
+    a.ca = ca;
+    a.code = code;
+    a.src = src;
+    a.nseq = nseq;
+    a.T = T;
+    a.states = states;
+    a.cost = cost;
+    a.bp = (uint32_t*)ws;
+    const int grid = nseq < num_sms() ? nseq : num_sms();
+    cudaError_t e = cudaErrorInvalidValue;
+    auto go = [&](auto kern, int sh) {
+        const size_t smem = ((size_t)1 << sh) * 4 + (size_t)kVThreads * kVStates * 2 + (size_t)T * 4;
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) return r;
+        kern<<<grid, kVThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    };
+    if (kv == 2) e = go(viterbi_kernel<2>, 14);
+    else if (kv == 3) e = go(viterbi_kernel<3>, 13);
+    count_launch(1);
+    return e;
+}
+
+}  // namespace qtip

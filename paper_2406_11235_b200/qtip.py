@@ -26,7 +26,8 @@ STATUS = {0: "QTIP_OK", -1: "QTIP_ERR_INVALID_PARAMS", -2: "QTIP_ERR_SHAPE", -3:
 EXPORTS = ["qtip_params_default", "qtip_params_check", "qtip_packed_bytes", "qtip_pack", "qtip_pack_states",
            "qtip_decode", "qtip_matvec", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
            "qtip_set_matvec_impl", "qtip_get_matvec_impl", "qtip_status_string", "qtip_last_error",
-           "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl"]
+           "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl", "qtip_viterbi_workspace_bytes",
+           "qtip_viterbi_tailbite"]
 
 
 class QtipParams(ctypes.Structure):
@@ -77,6 +78,10 @@ def load(path=LIB_PATH):
     lib.qtip_rht.restype = ctypes.c_int
     lib.qtip_hadamard_order.argtypes = [i64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.qtip_hadamard_order.restype = ctypes.c_int
+    lib.qtip_viterbi_workspace_bytes.argtypes = [P, i64]
+    lib.qtip_viterbi_workspace_bytes.restype = ctypes.c_size_t
+    lib.qtip_viterbi_tailbite.argtypes = [P, i64, i64, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.qtip_viterbi_tailbite.restype = ctypes.c_int
     lib.qtip_set_matvec_impl.argtypes = [ctypes.c_int]
     lib.qtip_set_matvec_impl.restype = None
     lib.qtip_get_matvec_impl.argtypes = []
@@ -168,6 +173,18 @@ def qtip_matvec(p, m, n, B, d_packed, d_lut, d_sign_n, d_sign_m, scale, d_x, d_y
     _check("qtip_matvec", load().qtip_matvec(ctypes.byref(p), m, n, B, _ptr(d_packed), _ptr(d_lut), _ptr(d_sign_n),
                                              _ptr(d_sign_m), float(scale), _ptr(d_x), _ptr(d_y), row_begin, row_end,
                                              flags, _ptr(d_workspace), ws_bytes, _stream(stream)))
+
+
+def viterbi_workspace_bytes(p, T):
+    return int(load().qtip_viterbi_workspace_bytes(ctypes.byref(p), T))
+
+
+def qtip_viterbi_tailbite(p, nseq, T, d_source, d_states, d_cost, d_workspace, stream=None):
+    """Algorithm 4 on nseq device sequences (float32 [nseq][T], code units) -> device walks
+    (uint32 [nseq][T]) and costs (float32 [nseq])."""
+    _check("qtip_viterbi_tailbite", load().qtip_viterbi_tailbite(
+        ctypes.byref(p), nseq, T, _ptr(d_source), _ptr(d_states), _ptr(d_cost), _ptr(d_workspace),
+        d_workspace.numel() * d_workspace.element_size(), _stream(stream)))
 
 
 def qtip_rht(n, B, d_sign, d_in, d_out, inverse=False, stream=None):

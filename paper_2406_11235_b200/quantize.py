@@ -1,0 +1,45 @@
+"""QTIPQuantizer: tail-biting trellis quantization of RHT-domain weight tiles on the GPU
+(Algorithm 4), producing the packed stream QTIPLinear decodes.
+
+All arithmetic runs in libqtip (qtip_viterbi_tailbite, k_viterbi.cu); this module only moves
+buffers: it scales the source into code units (reading R9: the code is normalised to unit
+state variance, i.e. the source is multiplied by the code's state standard deviation), calls the
+kernel, and hands the walks to qtip_pack_states.
+"""
+import numpy as np
+import torch
+
+from . import qtip
+
+
+class QTIPQuantizer:
+    def __init__(self, code="3inst", k=2, device="cuda"):
+        self.code, self.k = code, k
+        self.p = qtip.params_default(code, k)
+        self.device = torch.device(device)
+        self._ws = {}
+
+    def workspace(self, T):
+        if T not in self._ws:
+            self._ws[T] = torch.empty(qtip.viterbi_workspace_bytes(self.p, T), dtype=torch.uint8, device=self.device)
+        return self._ws[T]
+
+    def encode(self, src_code_units):
+        """src_code_units: float32 CUDA [nseq][T] (already multiplied by the code's state std).
+        Returns (walks uint32 CUDA [nseq][T], costs float32 CUDA [nseq])."""
+        assert src_code_units.dtype == torch.float32 and src_code_units.is_cuda and src_code_units.is_contiguous()
+        nseq, T = src_code_units.shape
+        states = torch.empty((nseq, T), dtype=torch.int32, device=self.device)
+        cost = torch.empty(nseq, dtype=torch.float32, device=self.device)
+        qtip.qtip_viterbi_tailbite(self.p, nseq, T, src_code_units, states, cost, self.workspace(T))
+        return states, cost
+
+    def quantize_tiles(self, W_tilde, code_std):
+        """W_tilde: float32 [m][n] RHT-domain weights (m, n multiples of 16), each 16 x 16 tile one
+        T = 256 sequence in row-major scan.  Returns the host walks
+        (uint32 [m/16][n/16][256]) for qtip_pack_states and the per-tile costs."""
+        m, n = W_tilde.shape
+        tiles = (W_tilde.reshape(m // 16, 16, n // 16, 16).permute(0, 2, 1, 3).reshape(-1, 256)
+                 .to(torch.float32) * np.float32(code_std)).contiguous()
+        states, cost = self.encode(tiles.to(self.device))
+        return states.cpu().numpy().astype(np.uint32).reshape(m // 16, n // 16, 256), cost
