@@ -19,6 +19,8 @@
 // Arithmetic is binary32 with every operation rounded on its own (no FMA contraction), in the
 // order of the oracle's binary32 DP (oracle/viterbi.c qo_viterbi_f32, reading R17): ties go to
 // the smallest predecessor index c and the smallest final state (reading R4).
+#include <type_traits>
+
 #include "decode.cuh"
 #include "internal.h"
 
@@ -37,6 +39,10 @@ struct ViterbiArgs {
     float* cost;                               // [nseq]
     uint32_t* bp;                              // per CTA: [T][kVThreads] words
 };
+
+// Group-minimum array layout: q -> q ^ ((q >> 5) & 31).  The writes (q = (b << kV) | j, lanes
+// 2^(2kV) floats apart) and the reads (q = c 2^(16-2kV) + tid BPT + bb) both hit 32 distinct banks.
+__device__ __forceinline__ int mphys(int q) { return q ^ ((q >> 5) & 31); }
 
 __device__ __forceinline__ __half code_half(uint32_t y, const CodeArgs& ca, int code) {
     if (code == QTIP_CODE_3INST) return inst3_value(inst3_word(y, ca.a, ca.b, ca.magic));
@@ -80,8 +86,11 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
             __syncthreads();
             // m for step 1: the minima over P(q') of V_0, V_0(y) = d(y, 0) (or inf off the start set)
             float m[BPT * NC];                              // this thread's group minima (c, bb)
-            for (int t = 1; t < T; ++t) {
-                // V_{t-1}(y) = m_{t-1}(q(y)) + d(y, t-1) folded into the minima m_t of (b << KV) | j
+            // step t: V_{t-1}(y) = m_{t-1}(q(y)) + d(y, t-1) folded into the minima m_t of (b << KV) | j;
+            // the first step (V_0 = d, start constraint) is a separate instantiation so the main
+            // loop is branch-free
+            auto step = [&](int t, auto kFirst) {
+                constexpr bool first = decltype(kFirst)::value;
                 const float st = s_src[t - 1];
                 uint32_t word = 0;
 #pragma unroll
@@ -96,11 +105,11 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
                             const float e = __fsub_rn(__half2float(myc[i]), st);
                             const float d = __fmul_rn(e, e);
                             float x;
-                            if (t == 1) x = (pass == 0 || (uint32_t)(c * NB + tid * BPT + bb) == O) ? d : INFINITY;
+                            if constexpr (first) x = (pass == 0 || (uint32_t)(c * NB + tid * BPT + bb) == O) ? d : INFINITY;
                             else x = __fadd_rn(m[c * BPT + bb], d);
                             if (x < best) { best = x; bc = c; }
                         }
-                        M[((tid * BPT + bb) << KV) | j] = best;
+                        M[mphys(((tid * BPT + bb) << KV) | j)] = best;
                         word |= bc << ((bb * NC + j) * KV);
                     }
                 bp[(size_t)t * kVThreads + tid] = word;
@@ -108,9 +117,11 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
 #pragma unroll
                 for (int bb = 0; bb < BPT; ++bb)
 #pragma unroll
-                    for (int c = 0; c < NC; ++c) m[c * BPT + bb] = M[c * NB + tid * BPT + bb];
+                    for (int c = 0; c < NC; ++c) m[c * BPT + bb] = M[mphys(c * NB + tid * BPT + bb)];
                 __syncthreads();                                // M is rewritten by the next step
-            }
+            };
+            if (T > 1) step(1, std::true_type{});
+            for (int t = 2; t < T; ++t) step(t, std::false_type{});
             // final state (recomputed V_{T-1}): smallest cost, then smallest index
             float best = INFINITY;
             uint32_t by = 0xFFFFFFFFu;
