@@ -354,6 +354,9 @@ def run_ours(args):
                "sample": f"3 x one 2048x4096 {code} k={k} layer (decode + float64 RHT-in/GEMV/RHT-out), "
                          f"single thread, host nproc={os.cpu_count()}"}
 
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk_sum = clk.summary()
+    clk_mhz = clk_sum.get("sm_mhz") or 1965.0
     if rank == 0:
         line = {
             "metric": "fused trellis-decode GEMV: compressed-byte HBM GB/s vs peak; us/layer batch=1",
@@ -372,12 +375,18 @@ def run_ours(args):
                          "frac": round(gemv_gbs / peak, 4), "traffic": traffic(args.workload, code, k, qtip.get_matvec_impl()),
                          "kernel": "fused decode-GEMV (+ split-K reduce where used), back-to-back graph",
                          "peak_kind": peak_kind,
-                         "avg_launch_us": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3)},
+                         "avg_launch_us": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3),
+                         # context: the measured decode-MMA loop ceiling of 3INST k=2
+                         # (scripts/decode_microbench.cu, 19.2 weights/clk/SM), the practical bound
+                         # below HBM for this code
+                         "decode_loop_ceiling": (None if (code, k) != ("3inst", 2) else {
+                             "weights_per_clk_per_sm": 19.2, "GBps": round(19.2 * sm_count * clk_mhz * 1e6 * k / 8 / 1e9, 1),
+                             "frac": round(gemv_gbs / (19.2 * sm_count * clk_mhz * 1e6 * k / 8 / 1e9), 4)})},
             "cpu_baseline": cpu,
             "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 5)},
             "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
