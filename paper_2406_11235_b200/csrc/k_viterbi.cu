@@ -67,14 +67,39 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int T = args.T;
     uint32_t* bp = args.bp + (size_t)blockIdx.x * T * kVThreads;
-    // slot i = (bb NC + c) NC + j <-> base b = tid BPT + bb, group q = c NB + b, state (q << KV) | j
+    // slot i = (bb NC + j) NC + c <-> base b = tid BPT + bb, group q = c NB + b, state (q << KV) | j;
+    // code halves stored chunk-interleaved (8 halves of a thread per 16-B chunk, chunks of all
+    // threads side by side) so a warp's vector loads are conflict-free
     auto state_of = [&](int i) {
-        const int bb = i / (NC * NC), c = (i / NC) % NC, j = i % NC;
+        const int bb = i / (NC * NC), j = (i / NC) % NC, c = i % NC;
         return ((uint32_t)(c * NB + tid * BPT + bb) << KV) | (uint32_t)j;
     };
-    __half* myc = codeh + tid * kVStates;
+    auto hoff = [&](int i) { return ((i >> 3) * kVThreads + tid) * 8 + (i & 7); };
 #pragma unroll 4
-    for (int i = 0; i < kVStates; ++i) myc[i] = code_half(state_of(i), args.ca, args.code);
+    for (int i = 0; i < kVStates; ++i) codeh[hoff(i)] = code_half(state_of(i), args.ca, args.code);
+    // the NC code values of (bb, j), c = 0 .. NC-1, as floats
+    auto codes_of = [&](int bb, int j, float (&cv)[NC]) {
+        const int i0 = (bb * NC + j) * NC;
+        if constexpr (NC == 8) {
+            const uint4 q = *reinterpret_cast<const uint4*>(codeh + hoff(i0));
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+                cv[2 * k] = f.x;
+                cv[2 * k + 1] = f.y;
+            }
+        } else {
+            const uint2 q = *reinterpret_cast<const uint2*>(codeh + hoff(i0));
+            const uint32_t w[2] = {q.x, q.y};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+                cv[2 * k] = f.x;
+                cv[2 * k + 1] = f.y;
+            }
+        }
+    };
 
     for (int seq = blockIdx.x; seq < args.nseq; seq += gridDim.x) {
         const float* s = args.src + (size_t)seq * T;
@@ -99,10 +124,11 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
                     for (int j = 0; j < NC; ++j) {
                         float best = INFINITY;
                         uint32_t bc = 0;
+                        float cv[NC];
+                        codes_of(bb, j, cv);
 #pragma unroll
                         for (int c = 0; c < NC; ++c) {
-                            const int i = (bb * NC + c) * NC + j;
-                            const float e = __fsub_rn(__half2float(myc[i]), st);
+                            const float e = __fsub_rn(cv[c], st);
                             const float d = __fmul_rn(e, e);
                             float x;
                             if constexpr (first) x = (pass == 0 || (uint32_t)(c * NB + tid * BPT + bb) == O) ? d : INFINITY;
@@ -128,15 +154,22 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
             {
                 const float st = s_src[T - 1];
 #pragma unroll
-                for (int i = 0; i < kVStates; ++i) {
-                    const int bb = i / (NC * NC), c = (i / NC) % NC;
-                    const uint32_t y = state_of(i);
-                    const float e = __fsub_rn(__half2float(myc[i]), st);
-                    const float d = __fmul_rn(e, e);
-                    float x = T == 1 ? ((pass == 0 || (y >> KV) == O) ? d : INFINITY) : __fadd_rn(m[c * BPT + bb], d);
-                    const bool ok = pass == 0 || (y & ((1u << SH) - 1u)) == O;
-                    if (ok && (x < best || (x == best && y < by))) { best = x; by = y; }
-                }
+                for (int bb = 0; bb < BPT; ++bb)
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) {
+                        float cv[NC];
+                        codes_of(bb, j, cv);
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) {
+                            const uint32_t y = ((uint32_t)(c * NB + tid * BPT + bb) << KV) | (uint32_t)j;
+                            const float e = __fsub_rn(cv[c], st);
+                            const float d = __fmul_rn(e, e);
+                            const float x = T == 1 ? ((pass == 0 || (y >> KV) == O) ? d : INFINITY)
+                                                   : __fadd_rn(m[c * BPT + bb], d);
+                            const bool ok = pass == 0 || (y & ((1u << SH) - 1u)) == O;
+                            if (ok && (x < best || (x == best && y < by))) { best = x; by = y; }
+                        }
+                    }
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
