@@ -265,9 +265,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         return fail(QTIP_ERR_UNSUPPORTED, "persistent GEMV kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB, shared memory fit");
     int impl = g_impl;
     if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
-    // measured: for HYB k = 4 at batch 1 the persistent GEMV with the
-    // shared-memory LUT fast path (impl 6) beats the row-tile kernel (at B = 4 it does not)
-    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && l.k == 4 && B == 1) impl = 6;
+    // measured: for HYB at batch 1 the persistent GEMV with the shared-memory
+    // LUT fast path (impl 6) beats the row-tile and split-K kernels (at B = 4 it does not)
+    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1) impl = 6;
     if (impl == 0) {
         // measured: the row-tile kernel wins while its CTAs (one per 16 rows,
         // 8-16 warps each) fill the GPU in one wave; beyond that the split-K kernel balances better
@@ -293,7 +293,7 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
                               align256(4 * B * l.m_pad) + align256(4 * (l.m_pad / kCellRows + 2)));
         unsigned* bar = (unsigned*)((char*)lws + align256(4 * layer_workspace_floats(l, B, 0)));
         const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
-        const int xmode6 = (p->code == QTIP_CODE_HYB && l.k == 4) ? 5 : xmode;   // HYB k = 4: swapped pairs
+        const int xmode6 = p->code == QTIP_CODE_HYB ? 5 : xmode;   // HYB fast path: swapped pairs
         e = cudaSuccess;
         if (!(flags & QTIP_XT_READY)) {
             if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode6, l.n_pad);

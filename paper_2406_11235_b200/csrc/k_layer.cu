@@ -440,7 +440,7 @@ template <int K, int CODE, bool kImm>
 __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_constant__ LayerArgs args) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
-    constexpr bool kHybFast = kHyb && K == 4;                      // Q = 9 (layer_supported)
+    constexpr bool kHybFast = kHyb;                                // Q = 9 (layer_supported)
     constexpr int TW = 8 * K;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tig = lane & 3;
@@ -660,6 +660,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     const uint32_t* lut = args.lut;
     const uint32_t lut_lane = ptx::smem_u32(smem + args.off_lut) + 4u * lane;
     const mma::HybFastLane hl = mma::hyb_fast_lane(g, tig);
+    const mma::HybFastLaneK<K> hlk = mma::hyb_fast_lane_k<K>(g, tig);
     const uint32_t full0 = ptx::smem_u32(full);
     const uint8_t* ring0 = ring;
     const uint32_t part_u32 = ptx::smem_u32(part);
@@ -711,7 +712,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             } else {
 #pragma unroll
                 for (int pp = 0; pp < 4; ++pp) {
-                    if constexpr (kHybFast) tile_pair_hyb4<1>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hl, lut_lane);
+                    if constexpr (kHybFast && K == 4) tile_pair_hyb4<1>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hl, lut_lane);
+                    else if constexpr (kHybFast) tile_pair_hyb_k<K, 1>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hlk, lut_lane);
                     else tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], g, tig, lcg, ca, lut);
                 }
             }
@@ -973,7 +975,7 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
     const size_t vin_pad = align128((size_t)B * lay.n_pad * 4);
     const size_t red = (size_t)kLWarps * kMixChunk * 4;
     const size_t vout = align128(((size_t)B * lay.m + 31) / 32 * 32 * 4);
-    const size_t lutb = (code == QTIP_CODE_HYB && lay.k == 4) ? (size_t)(512 * 32 * 4) : 0;   // HYB k = 4 fast path
+    const size_t lutb = code == QTIP_CODE_HYB ? (size_t)(512 * 32 * 4) : 0;   // HYB fast path LUT
     auto layout = [&](int S) {                                        // offsets for ring depth S; total bytes
         size_t off = head + part;
         pl->off_lut = (uint32_t)off;
@@ -1032,7 +1034,7 @@ bool layer_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B,
                      bool rht_out) {
     if (B < 1 || B > 4 || lay.k < 2 || lay.k > 4) return false;
     if (code == QTIP_CODE_HYB && ca.two_sign) return false;
-    if (code == QTIP_CODE_HYB && lay.k == 4 && ca.Q != 9) return false;   // fast path: 2^9-entry LUT
+    if (code == QTIP_CODE_HYB && ca.Q != 9) return false;   // fast path: 2^9-entry shared-memory LUT
     if (lay.n > (1 << 24) / 4 || lay.m > (1 << 24) / 4 || num_sms() > 256) return false;
     int nb = 1, na = 0, mb = 1, ma = 0;
     if (rht_in && !hadamard_factor(lay.n, &nb, &na)) return false;

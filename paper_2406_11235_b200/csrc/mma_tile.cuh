@@ -258,5 +258,52 @@ __device__ __forceinline__ void tile_pair_hyb4(const uint32_t* pw, const uint32_
             hmma_16816(acc[ng], z[t][0][0], z[t][1][0], z[t][0][1], z[t][1][1], bf[t][ng][0], bf[t][ng][1]);
 }
 
+// HYB fast path for k = 2, 3 (windows not byte-aligned, and the pair tig + 4 window is 8k bits
+// after the pair tig one, so it may start in the same or the next word): per lane, row and window a
+// word offset and funnel amount (lane constants), two LDS.64 (both tiles of the pair) per window.
+template <int K>
+struct HybFastLaneK {
+    int w0[2][2];       // [row rr][window] pair-interleaved offset of W[q] (W[q + 1] is at w1)
+    int w1[2][2];
+    uint32_t n[2][2];
+};
+
+template <int K>
+__device__ __forceinline__ HybFastLaneK<K> hyb_fast_lane_k(int g, int tig) {
+    constexpr int TW = 8 * K;
+    HybFastLaneK<K> hl;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const int s = 16 * K * (2 * g + rr) + 2 * K * (tig + 4 * w) - 16;   // window start - 16
+            const int q = s >> 5;                                                // -1 wraps: garbage bits
+            hl.w0[rr][w] = 2 * ((q + TW) % TW);
+            hl.w1[rr][w] = 2 * ((q + 1 + TW) % TW);
+            hl.n[rr][w] = (uint32_t)(s & 31);
+        }
+    return hl;
+}
+
+template <int K, int NG>
+__device__ __forceinline__ void tile_pair_hyb_k(const uint32_t* pw, const uint32_t (&bf)[2][NG][4], float (&acc)[NG][4],
+                                                const HybFastLaneK<K>& hl, uint32_t lut_lane) {
+    uint32_t z[2][2][2];                                       // [tile][row rr][pair: tig, tig + 4]
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const uint2 A = *reinterpret_cast<const uint2*>(pw + hl.w0[rr][w]);
+            const uint2 Bw = *reinterpret_cast<const uint2*>(pw + hl.w1[rr][w]);
+            z[0][rr][w] = hyb_fast_word(__funnelshift_l(Bw.x, A.x, hl.n[rr][w]), lut_lane);
+            z[1][rr][w] = hyb_fast_word(__funnelshift_l(Bw.y, A.y, hl.n[rr][w]), lut_lane);
+        }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int ng = 0; ng < NG; ++ng)
+            hmma_16816(acc[ng], z[t][0][0], z[t][1][0], z[t][0][1], z[t][1][1], bf[t][ng][0], bf[t][ng][1]);
+}
+
 }  // namespace mma
 }  // namespace qtip
