@@ -672,8 +672,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         pok[e] = b < B;
         poff[e] = (uint32_t)(r * B + (b < B ? b : 0)) * 4u;
     }
-    auto run = [&](auto kPartSmem) {
+    auto run = [&](auto kPartSmem, auto kTwoSign) {
         constexpr bool kSmemPart = decltype(kPartSmem)::value;
+        constexpr bool kTwo = decltype(kTwoSign)::value;
         float* const gpart = args.gpart;
         const int64_t row0 = args.tile_row0 * kTile;
         int st = 0;
@@ -712,8 +713,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             } else {
 #pragma unroll
                 for (int pp = 0; pp < 4; ++pp) {
-                    if constexpr (kHybFast && K == 4) tile_pair_hyb4<1>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hl, lut_lane);
-                    else if constexpr (kHybFast) tile_pair_hyb_k<K, 1>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hlk, lut_lane);
+                    if constexpr (kHybFast && K == 4) tile_pair_hyb4<1, kTwo>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hl, lut_lane);
+                    else if constexpr (kHybFast) tile_pair_hyb_k<K, 1, kTwo>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], hlk, lut_lane);
                     else tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf[pp], acc[pp & 1], g, tig, lcg, ca, lut);
                 }
             }
@@ -739,8 +740,13 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             }
         }
     };
-    if (args.part_smem) run(std::true_type{});
-    else run(std::false_type{});
+    if (kHyb && ca.two_sign) {
+        if (args.part_smem) run(std::true_type{}, std::integral_constant<bool, kHyb>{});
+        else run(std::false_type{}, std::integral_constant<bool, kHyb>{});
+    } else {
+        if (args.part_smem) run(std::true_type{}, std::false_type{});
+        else run(std::false_type{}, std::false_type{});
+    }
     __syncthreads();
     trace_mark(tr, 5);
 
@@ -1033,7 +1039,6 @@ cudaError_t set_cta_trace_layer(unsigned long long* buf, int cap) {
 bool layer_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int64_t tile_rows, bool rht_in,
                      bool rht_out) {
     if (B < 1 || B > 4 || lay.k < 2 || lay.k > 4) return false;
-    if (code == QTIP_CODE_HYB && ca.two_sign) return false;
     if (code == QTIP_CODE_HYB && ca.Q != 9) return false;   // fast path: 2^9-entry shared-memory LUT
     if (lay.n > (1 << 24) / 4 || lay.m > (1 << 24) / 4 || num_sms() > 256) return false;
     int nb = 1, na = 0, mb = 1, ma = 0;

@@ -224,18 +224,23 @@ __device__ __forceinline__ HybFastLane hyb_fast_lane(int g, int tig) {
     return hl;
 }
 
+// kTwo: the two-sign variant: bit 31 of x^2 + x also flips c0 (bit 31 of the word);
+// that bit depends on all of x, so the window is zero-filled first (one more LOP3).
+template <bool kTwo = false>
 __device__ __forceinline__ uint32_t hyb_fast_word(uint32_t x, uint32_t lut_lane) {
+    if constexpr (kTwo) x &= 0xFFFFu;
     const uint32_t h = x * x + x;
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut_lane + ((h + h) & 0xFF80u)));
     uint32_t w;
-    asm("lop3.b32 %0, %1, %2, 0x8000, 0x78;" : "=r"(w) : "r"(v), "r"(h));      // v ^ (h & 0x8000)
+    if constexpr (kTwo) asm("lop3.b32 %0, %1, %2, 0x80008000, 0x78;" : "=r"(w) : "r"(v), "r"(h));
+    else asm("lop3.b32 %0, %1, %2, 0x8000, 0x78;" : "=r"(w) : "r"(v), "r"(h));      // v ^ (h & 0x8000)
     return w;
 }
 
 // acc += W~(tiles t = 0, 1 of a pair) x~ for the HYB k = 4 fast path; pw = the pair's words,
 // lut_lane = shared-memory address of this lane's LUT replica, bf[t] from x~ mode 5.
-template <int NG>
+template <int NG, bool kTwo = false>
 __device__ __forceinline__ void tile_pair_hyb4(const uint32_t* pw, const uint32_t (&bf)[2][NG][4], float (&acc)[NG][4],
                                                const HybFastLane& hl, uint32_t lut_lane) {
     uint32_t z[2][2][2];                                       // [tile][row rr][pair: tig, tig + 4]
@@ -247,8 +252,8 @@ __device__ __forceinline__ void tile_pair_hyb4(const uint32_t* pw, const uint32_
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const uint32_t a = t ? A.y : A.x, b = t ? Bw.y : Bw.x, c = t ? C.y : C.x;
-            z[t][rr][0] = hyb_fast_word(__funnelshift_l(b, a, hl.n), lut_lane);
-            z[t][rr][1] = hyb_fast_word(__funnelshift_l(c, b, hl.n), lut_lane);
+            z[t][rr][0] = hyb_fast_word<kTwo>(__funnelshift_l(b, a, hl.n), lut_lane);
+            z[t][rr][1] = hyb_fast_word<kTwo>(__funnelshift_l(c, b, hl.n), lut_lane);
         }
     }
 #pragma unroll
@@ -285,7 +290,7 @@ __device__ __forceinline__ HybFastLaneK<K> hyb_fast_lane_k(int g, int tig) {
     return hl;
 }
 
-template <int K, int NG>
+template <int K, int NG, bool kTwo = false>
 __device__ __forceinline__ void tile_pair_hyb_k(const uint32_t* pw, const uint32_t (&bf)[2][NG][4], float (&acc)[NG][4],
                                                 const HybFastLaneK<K>& hl, uint32_t lut_lane) {
     uint32_t z[2][2][2];                                       // [tile][row rr][pair: tig, tig + 4]
@@ -295,8 +300,8 @@ __device__ __forceinline__ void tile_pair_hyb_k(const uint32_t* pw, const uint32
         for (int w = 0; w < 2; ++w) {
             const uint2 A = *reinterpret_cast<const uint2*>(pw + hl.w0[rr][w]);
             const uint2 Bw = *reinterpret_cast<const uint2*>(pw + hl.w1[rr][w]);
-            z[0][rr][w] = hyb_fast_word(__funnelshift_l(Bw.x, A.x, hl.n[rr][w]), lut_lane);
-            z[1][rr][w] = hyb_fast_word(__funnelshift_l(Bw.y, A.y, hl.n[rr][w]), lut_lane);
+            z[0][rr][w] = hyb_fast_word<kTwo>(__funnelshift_l(Bw.x, A.x, hl.n[rr][w]), lut_lane);
+            z[1][rr][w] = hyb_fast_word<kTwo>(__funnelshift_l(Bw.y, A.y, hl.n[rr][w]), lut_lane);
         }
 #pragma unroll
     for (int t = 0; t < 2; ++t)

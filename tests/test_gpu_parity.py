@@ -295,3 +295,26 @@ def test_sharded_layer_world1_nccl_equals_unsharded(cuda_lib, B):
     # the gathered y~ rows are the full call's rows bit for bit (fixed per-row association); the
     # replicated inverse RHT may run in a different kernel than the full call's (fp32 rounding order)
     assert rel_l2(y_sh, y) <= 1e-6
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("impl", [0, 5, 6])
+def test_hyb_two_sign_matvec(cuda_lib, k, impl):
+    """HYB two-sign variant (bit 31 of x^2 + x also flips the first entry) through the
+    shared-memory LUT fast path: matvec within 1e-3 of the float64 oracle."""
+    from paper_2406_11235_b200.layer import QTIPLinear
+    m, n = 384, 768
+    tiles = synth.random_tiles(m, n, k, seed=90 + k)
+    lut = lut_for("hyb")
+    layer = QTIPLinear(m, n, code="hyb", k=k, two_sign=True)
+    layer.load_tiles(tiles, synth.random_sign_bytes(m, 3001 + 7), synth.random_sign_bytes(n, 3000 + 7), scale=0.6, lut=lut)
+    x = synth.random_x(1, n, seed=91)
+    cuda_lib.set_matvec_impl(impl)
+    try:
+        y = layer(torch.from_numpy(x).cuda()).cpu().numpy()
+    finally:
+        cuda_lib.set_matvec_impl(0)
+    p = gemv.Params(k=k, V=2, code="hyb", lut=lut, two_sign=True)
+    ref = gemv.matvec(gemv.dense_decode(tiles, p), x.astype(np.float64), synth.random_sign_bytes(n, 3000 + 7),
+                      synth.random_sign_bytes(m, 3001 + 7), scale=0.6)
+    assert rel_l2(y, ref) <= MATVEC_TOL
