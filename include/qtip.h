@@ -136,22 +136,25 @@ qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a);
 /* Tail-biting trellis quantizer (P:127-141 Viterbi DP; Algorithm 4): for each of nseq
  * independent length-T source sequences, the walk returned by Algorithm 4 -- rotate the sequence
  * right by floor(T/2), run the unconstrained Viterbi, take the L-kV bit overlap O at the seam
- * (reading R3: bottom L-kV bits of the rotated walk's state at 1-indexed position floor(T/2)),
+ * (reading R3: bottom L-kV bits of the rotated walk's state at 1-indexed group floor(T/(2V))),
  * then run the Viterbi on the original sequence with the first state's top and the last state's
  * bottom L-kV bits both equal to O (a tail-biting walk).
- *   p: L = 16, V = 1, k in {2, 3}, code 3INST or 1MAD (else QTIP_ERR_UNSUPPORTED).
+ *   p: L = 16 and either 3INST/1MAD with V = 1, k in {2, 3}, or HYB with V = 2, k in {2, 3, 4},
+ *     Q = 9, one-sign (else QTIP_ERR_UNSUPPORTED).  T % V == 0.
  *   d_source: DEVICE float32 [nseq][T], already in code units (the caller scales the source by
- *     the code's state standard deviation, reading R9); d_states: DEVICE uint32 [nseq][T] walk
+ *     the code's state standard deviation, reading R9); d_lut: HYB table as for qtip_decode (DEVICE
+ *     binary16 pairs (c0, c1) [2^Q][2]), NULL otherwise; d_states: DEVICE uint32 [nseq][T/V] walk
  *     (feed to qtip_pack_states after copying to the host); d_cost: DEVICE float32 [nseq], the
  *     walk's squared error sum.
- *   Arithmetic: code values C_y are the binary16 codes of qtip_decode widened to binary32; the DP
- *     is binary32 with each operation rounded separately, ties to the smallest predecessor index
- *     and the smallest final state (reading R4), as oracle/viterbi.c qo_viterbi_f32 (R17).
+ *   Arithmetic: code values are the binary16 codes of qtip_decode widened to binary32; the DP
+ *     is binary32 with each operation rounded separately (per step sum_v (c_v - s_v)^2 left to
+ *     right), ties to the smallest predecessor index and the smallest final state (reading R4), as
+ *     oracle/viterbi.c qo_viterbi_f32 (R17).
  *   d_workspace: qtip_viterbi_workspace_bytes(p, T) bytes, caller-owned (backpointers). */
 size_t qtip_viterbi_workspace_bytes(const qtip_params* p, int64_t T);
 qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T, const float* d_source,
-                                  uint32_t* d_states, float* d_cost, void* d_workspace, size_t workspace_bytes,
-                                  void* stream);
+                                  const uint16_t* d_lut, uint32_t* d_states, float* d_cost, void* d_workspace,
+                                  size_t workspace_bytes, void* stream);
 
 /* Selects the matvec kernel: 0 = auto (the measured-fastest supported kernel), 1 = CUDA-core
  * reference kernel, 2 = tcgen05 kernel (A in TMEM), 3 = register-fed mma.sync kernel with

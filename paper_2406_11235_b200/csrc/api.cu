@@ -397,16 +397,18 @@ size_t qtip_viterbi_workspace_bytes(const qtip_params* p, int64_t T) {
 }
 
 qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T, const float* d_source,
-                                  uint32_t* d_states, float* d_cost, void* d_workspace, size_t workspace_bytes,
-                                  void* stream) {
+                                  const uint16_t* d_lut, uint32_t* d_states, float* d_cost, void* d_workspace,
+                                  size_t workspace_bytes, void* stream) {
     qtip_status st = qtip_params_check(p);
     if (st != QTIP_OK) return st;
-    if (!viterbi_supported(p->code, p->k, p->V, p->L))
-        return fail(QTIP_ERR_UNSUPPORTED, "GPU quantizer: L = 16, V = 1, k in {2, 3}, 3INST or 1MAD");
-    if (nseq < 1 || T < 2 || T > 4096 || nseq > (1 << 30)) return fail(QTIP_ERR_SHAPE, "need nseq >= 1, 2 <= T <= 4096");
-    if (!d_source || !d_states || !d_cost || !d_workspace) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (!viterbi_supported(p->code, p->k, p->V, p->L, p->Q, p->hyb_two_sign))
+        return fail(QTIP_ERR_UNSUPPORTED,
+                    "GPU quantizer: L = 16; 3INST/1MAD V = 1, k in {2, 3}; HYB V = 2, k in {2, 3, 4}, Q = 9, one sign");
+    if (nseq < 1 || T < 2 || T > 4096 || nseq > (1 << 30) || T % p->V) return fail(QTIP_ERR_SHAPE, "need nseq >= 1, 2 <= T <= 4096, V | T");
+    if (!d_source || !d_states || !d_cost || !d_workspace || (p->code == QTIP_CODE_HYB && !d_lut))
+        return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
     if (workspace_bytes < viterbi_workspace_bytes((int)T)) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
-    const cudaError_t e = launch_viterbi(p->code, p->k * p->V, code_args(p), d_source, (int)nseq, (int)T, d_states,
+    const cudaError_t e = launch_viterbi(p->code, p->k * p->V, code_args(p), d_source, d_lut, (int)nseq, (int)T, d_states,
                                          d_cost, d_workspace, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_viterbi_tailbite");
     return QTIP_OK;

@@ -120,10 +120,10 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
 
 // Tail-biting trellis quantizer (k_viterbi.cu): Algorithm 4 per sequence of T source values (in
 // code units), binary32 DP.  ws: viterbi_workspace_bytes(T) bytes (backpointers, per CTA).
-bool viterbi_supported(int code, int k, int V, int L);
+bool viterbi_supported(int code, int k, int V, int L, int Q, int two_sign);
 size_t viterbi_workspace_bytes(int T);
-cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, int nseq, int T, uint32_t* states,
-                           float* cost, void* ws, cudaStream_t s);
+cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, const uint16_t* lut, int nseq, int T,
+                           uint32_t* states, float* cost, void* ws, cudaStream_t s);
 
 // Debug CTA timelines (trace.cuh), per translation unit.
 cudaError_t set_cta_trace_rht(unsigned long long* buf, int cap);

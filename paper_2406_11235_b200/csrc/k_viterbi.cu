@@ -34,8 +34,9 @@ struct ViterbiArgs {
     CodeArgs ca;
     int code;
     const float* src;                          // [nseq][T], in code units
+    const uint32_t* lut;                       // HYB: 2^9 words (c0 | c1 << 16)
     int nseq, T;
-    uint32_t* states;                          // [nseq][T]
+    uint32_t* states;                          // [nseq][T / V]
     float* cost;                               // [nseq]
     uint32_t* bp;                              // per CTA: [T][kVThreads] words
 };
@@ -219,17 +220,183 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
     }
 }
 
-}  // namespace
 
-size_t viterbi_workspace_bytes(int T) { return (size_t)num_sms() * T * kVThreads * 4; }
+// ---------------------------------------------------------------------------------------------
+// V = 2 (HYB): kV = 2k in {4, 6, 8}; a step consumes a pair of source values and the
+// state's code is the LUT pair (c0, c1) of h = y^2 + y with the sign of c1 from bit 15 of h (one
+// sign).  2^kV predecessors per group are too many to keep a base's states in one thread, so each
+// thread holds JT of the base's j and CT of its c (JT CT BPT = 64 states); for kV = 8 four adjacent
+// lanes split the c of one j and combine their minima with two shuffles (smaller c wins ties).
+// The code is evaluated on the fly from a 2^(Q+1) = 1024-entry table with the sign folded in
+// (entries 512..1023 carry -c1), replicated 32-fold in shared memory (index bits 6..15 of h).
+// Group minima live in two swapped shared-memory arrays, base-major (position b 2^kV + c) so a
+// thread's c run is contiguous; backpointers are one byte per group per step.
+template <int KV>
+__global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArgs args) {
+    constexpr int L = 16;
+    constexpr int SH = L - KV;
+    constexpr int NB = 1 << (L - 2 * KV);              // bases
+    constexpr int NC = 1 << KV;
+    constexpr int NG = 1 << SH;                        // groups
+    constexpr int TPB = kVThreads / NB;                // threads per base (>= 4 here)
+    constexpr int CSPLIT = TPB > NC ? TPB / NC : 1;    // lanes sharing one j (kV = 8: 4)
+    constexpr int JT = TPB > NC ? 1 : NC / TPB;        // j per thread
+    constexpr int CT = NC / CSPLIT;                    // c per thread
+    static_assert(JT * CT == kVStates, "64 states per thread");
+    extern __shared__ __align__(16) float sm[];
+    float* Mbuf = sm;                                                  // [2][NG], position b NC + c
+    uint32_t* lut = reinterpret_cast<uint32_t*>(sm + 2 * NG);          // [1024][32] words (c0 | c1 << 16)
+    float* s_src = sm + 2 * NG + 1024 * 32;                            // [T]
+    __shared__ float red_v[32];
+    __shared__ uint32_t red_i[32];
+    __shared__ uint32_t s_state;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int T = args.T, nsteps = T / 2;
+    uint8_t* bp = reinterpret_cast<uint8_t*>(args.bp) + (size_t)blockIdx.x * nsteps * NG;
+    const int b = tid / TPB;
+    const int jbase = TPB > NC ? (tid % TPB) / CSPLIT : (tid % TPB) * JT;
+    const int cbase = TPB > NC ? (tid % CSPLIT) * CT : 0;
+    for (int i = tid; i < 1024 * 32; i += kVThreads) {
+        const int e = i >> 5;
+        uint32_t w = args.lut[e & 511];
+        if (e & 512) w ^= 0x80000000u;                                 // c1 negated (Alg. 3 bit 15)
+        lut[i] = w;
+    }
+    const uint32_t lut_lane = (uint32_t)__cvta_generic_to_shared(lut) + 4u * lane;
+    auto pos = [](int q) { return (q % NB) * NC + q / NB; };            // base-major group position
 
-bool viterbi_supported(int code, int k, int V, int L) {
-    return L == 16 && V == 1 && (k == 2 || k == 3) && (code == QTIP_CODE_3INST || code == QTIP_CODE_1MAD);
+    for (int seq = blockIdx.x; seq < args.nseq; seq += gridDim.x) {
+        const float* s = args.src + (size_t)seq * T;
+        uint32_t O = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            __syncthreads();
+            for (int t = tid; t < T; t += kVThreads) s_src[t] = pass ? s[t] : s[(t - T / 2 + T) % T];
+            __syncthreads();
+            int cur = 0;
+            // V_{t-1}(y) = m_{t-1}(q(y)) + d(y, t-1) folded into m_t((b << KV) | j)
+            auto step = [&](int t, auto kFirst, auto kLast, float& fbest, uint32_t& fy) {
+                constexpr bool first = decltype(kFirst)::value, last = decltype(kLast)::value;
+                const float s0 = s_src[2 * (t - 1)], s1 = s_src[2 * (t - 1) + 1];
+                const float* M = Mbuf + cur * NG;
+                float* Mn = Mbuf + (cur ^ 1) * NG;
+#pragma unroll 1
+                for (int jj = 0; jj < JT; ++jj) {
+                    const int j = jbase + jj;
+                    float best = INFINITY;
+                    uint32_t bc = 0;
+#pragma unroll 4
+                    for (int cc = 0; cc < CT; ++cc) {
+                        const int c = cbase + cc;
+                        const uint32_t y = ((uint32_t)(c * NB + b) << KV) | (uint32_t)j;
+                        const uint32_t h2 = y * (y + y + 2u);            // 2 (y^2 + y) mod 2^32
+                        uint32_t v;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut_lane + (h2 & 0x1FF80u)));
+                        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&v));
+                        const float e0 = __fsub_rn(f.x, s0), e1 = __fsub_rn(f.y, s1);
+                        const float d = __fadd_rn(__fmul_rn(e0, e0), __fmul_rn(e1, e1));
+                        float x;
+                        if constexpr (first) x = (pass == 0 || (uint32_t)(c * NB + b) == O) ? d : INFINITY;
+                        else x = __fadd_rn(M[b * NC + c], d);
+                        if constexpr (last) {
+                            const bool ok = pass == 0 || (y & ((1u << SH) - 1u)) == O;
+                            if (ok && (x < fbest || (x == fbest && y < fy))) { fbest = x; fy = y; }
+                        } else if (x < best) {
+                            best = x;
+                            bc = c;
+                        }
+                    }
+                    if constexpr (!last) {
+                        if constexpr (CSPLIT > 1) {
+#pragma unroll
+                            for (int o = 1; o < CSPLIT; o <<= 1) {
+                                const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                                const uint32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                                if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
+                            }
+                        }
+                        if (cbase == 0) {
+                            const int q = (b << KV) | j;
+                            Mn[pos(q)] = best;
+                            bp[(size_t)t * NG + q] = (uint8_t)bc;
+                        }
+                    }
+                }
+                if constexpr (!last) {
+                    __syncthreads();
+                    cur ^= 1;
+                }
+            };
+            float fbest = INFINITY;
+            uint32_t fy = 0xFFFFFFFFu;
+            if (nsteps == 1) {
+                step(1, std::true_type{}, std::true_type{}, fbest, fy);
+            } else {
+                step(1, std::true_type{}, std::false_type{}, fbest, fy);
+                for (int t = 2; t < nsteps; ++t) step(t, std::false_type{}, std::false_type{}, fbest, fy);
+                step(nsteps, std::false_type{}, std::true_type{}, fbest, fy);
+            }
+            float best = fbest;
+            uint32_t by = fy;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const uint32_t oy = __shfl_xor_sync(0xffffffffu, by, o);
+                if (ob < best || (ob == best && oy < by)) { best = ob; by = oy; }
+            }
+            if (lane == 0) { red_v[warp] = best; red_i[warp] = by; }
+            __syncthreads();
+            if (warp == 0) {
+                best = red_v[lane];
+                by = red_i[lane];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const uint32_t oy = __shfl_xor_sync(0xffffffffu, by, o);
+                    if (ob < best || (ob == best && oy < by)) { best = ob; by = oy; }
+                }
+                if (lane == 0) {
+                    if (!(best < INFINITY)) by = 0;
+                    uint32_t y = by;
+                    // Alg. 4 seam: 1-indexed group floor(T/(2V)) (R3); for T = 2 that is index -1, which the
+                    // oracle (Python indexing) reads as the last state
+                    const int g = T / 4, gi = g >= 1 ? g - 1 : nsteps - 1;
+                    if (pass == 1) {
+                        args.states[(size_t)seq * nsteps + nsteps - 1] = y;
+                        args.cost[seq] = best;
+                    }
+                    if (pass == 0 && gi == nsteps - 1) s_state = y & ((1u << SH) - 1u);
+                    for (int t = nsteps - 1; t >= 1; --t) {
+                        const uint32_t q = y >> KV;
+                        const uint32_t c = __ldcg(bp + (size_t)t * NG + q);
+                        y = (c << SH) | q;
+                        if (pass == 1) args.states[(size_t)seq * nsteps + t - 1] = y;
+                        if (pass == 0 && t - 1 == gi) {
+                            s_state = y & ((1u << SH) - 1u);
+                            break;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            O = s_state;
+        }
+    }
 }
 
-cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, int nseq, int T, uint32_t* states,
-                           float* cost, void* ws, cudaStream_t s) {
+}  // namespace
+
+size_t viterbi_workspace_bytes(int T) { return (size_t)num_sms() * T * kVThreads * 4; }   // >= V = 2 needs
+
+bool viterbi_supported(int code, int k, int V, int L, int Q, int two_sign) {
+    if (L != 16) return false;
+    if (code == QTIP_CODE_HYB) return V == 2 && Q == 9 && !two_sign && (k == 2 || k == 3 || k == 4);
+    return V == 1 && (k == 2 || k == 3) && (code == QTIP_CODE_3INST || code == QTIP_CODE_1MAD);
+}
+
+cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, const uint16_t* lut, int nseq, int T,
+                           uint32_t* states, float* cost, void* ws, cudaStream_t s) {
     ViterbiArgs a;
+    a.lut = reinterpret_cast<const uint32_t*>(lut);
     a.ca = ca;
     a.code = code;
     a.src = src;
@@ -247,7 +414,18 @@ cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* sr
         kern<<<grid, kVThreads, smem, s>>>(a);
         return cudaGetLastError();
     };
-    if (kv == 2) e = go(viterbi_kernel<2>, 14);
+    auto go2 = [&](auto kern, int sh) {
+        const size_t smem = 2 * ((size_t)1 << sh) * 4 + (size_t)1024 * 32 * 4 + (size_t)T * 4;
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) return r;
+        kern<<<grid, kVThreads, smem, s>>>(a);
+        return cudaGetLastError();
+    };
+    if (code == QTIP_CODE_HYB) {
+        if (kv == 4) e = go2(viterbi2_kernel<4>, 12);
+        else if (kv == 6) e = go2(viterbi2_kernel<6>, 10);
+        else if (kv == 8) e = go2(viterbi2_kernel<8>, 8);
+    } else if (kv == 2) e = go(viterbi_kernel<2>, 14);
     else if (kv == 3) e = go(viterbi_kernel<3>, 13);
     count_launch(1);
     return e;

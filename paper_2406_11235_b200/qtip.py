@@ -80,7 +80,7 @@ def load(path=LIB_PATH):
     lib.qtip_hadamard_order.restype = ctypes.c_int
     lib.qtip_viterbi_workspace_bytes.argtypes = [P, i64]
     lib.qtip_viterbi_workspace_bytes.restype = ctypes.c_size_t
-    lib.qtip_viterbi_tailbite.argtypes = [P, i64, i64, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.qtip_viterbi_tailbite.argtypes = [P, i64, i64, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.qtip_viterbi_tailbite.restype = ctypes.c_int
     lib.qtip_set_matvec_impl.argtypes = [ctypes.c_int]
     lib.qtip_set_matvec_impl.restype = None
@@ -179,11 +179,11 @@ def viterbi_workspace_bytes(p, T):
     return int(load().qtip_viterbi_workspace_bytes(ctypes.byref(p), T))
 
 
-def qtip_viterbi_tailbite(p, nseq, T, d_source, d_states, d_cost, d_workspace, stream=None):
+def qtip_viterbi_tailbite(p, nseq, T, d_source, d_states, d_cost, d_workspace, d_lut=None, stream=None):
     """Algorithm 4 on nseq device sequences (float32 [nseq][T], code units) -> device walks
-    (uint32 [nseq][T]) and costs (float32 [nseq])."""
+    (uint32 [nseq][T/V]) and costs (float32 [nseq]); d_lut: HYB binary16 pairs."""
     _check("qtip_viterbi_tailbite", load().qtip_viterbi_tailbite(
-        ctypes.byref(p), nseq, T, _ptr(d_source), _ptr(d_states), _ptr(d_cost), _ptr(d_workspace),
+        ctypes.byref(p), nseq, T, _ptr(d_source), _ptr(d_lut), _ptr(d_states), _ptr(d_cost), _ptr(d_workspace),
         d_workspace.numel() * d_workspace.element_size(), _stream(stream)))
 
 

@@ -13,10 +13,17 @@ from . import qtip
 
 
 class QTIPQuantizer:
-    def __init__(self, code="3inst", k=2, device="cuda"):
+    def __init__(self, code="3inst", k=2, device="cuda", lut=None):
+        """lut: HYB only, numpy uint16 (2^9, 2) binary16 pairs (the table the layer decodes with)."""
         self.code, self.k = code, k
         self.p = qtip.params_default(code, k)
+        self.V = 2 if code == "hyb" else 1
         self.device = torch.device(device)
+        self.lut = None
+        if code == "hyb":
+            if lut is None:
+                raise ValueError("HYB needs a LUT")
+            self.lut = torch.from_numpy(np.ascontiguousarray(lut, dtype=np.uint16).view(np.int16)).to(self.device)
         self._ws = {}
 
     def workspace(self, T):
@@ -29,9 +36,9 @@ class QTIPQuantizer:
         Returns (walks uint32 CUDA [nseq][T], costs float32 CUDA [nseq])."""
         assert src_code_units.dtype == torch.float32 and src_code_units.is_cuda and src_code_units.is_contiguous()
         nseq, T = src_code_units.shape
-        states = torch.empty((nseq, T), dtype=torch.int32, device=self.device)
+        states = torch.empty((nseq, T // self.V), dtype=torch.int32, device=self.device)
         cost = torch.empty(nseq, dtype=torch.float32, device=self.device)
-        qtip.qtip_viterbi_tailbite(self.p, nseq, T, src_code_units, states, cost, self.workspace(T))
+        qtip.qtip_viterbi_tailbite(self.p, nseq, T, src_code_units, states, cost, self.workspace(T), d_lut=self.lut)
         return states, cost
 
     def quantize_tiles(self, W_tilde, code_std):
@@ -42,4 +49,4 @@ class QTIPQuantizer:
         tiles = (W_tilde.reshape(m // 16, 16, n // 16, 16).permute(0, 2, 1, 3).reshape(-1, 256)
                  .to(torch.float32) * np.float32(code_std)).contiguous()
         states, cost = self.encode(tiles.to(self.device))
-        return states.cpu().numpy().astype(np.uint32).reshape(m // 16, n // 16, 256), cost
+        return states.cpu().numpy().astype(np.uint32).reshape(m // 16, n // 16, 256 // self.V), cost

@@ -17,9 +17,11 @@ code = sys.argv[1] if len(sys.argv) > 1 else "3inst"
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 nseq = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
 T = int(sys.argv[4]) if len(sys.argv) > 4 else 256
-tab = codes.code_table(code, 16)
+V = 2 if code == "hyb" else 1
+lut = synth.gaussian_lut(9, 4000) if code == "hyb" else None
+tab = codes.code_table(code, 16, lut=lut, Q=9) if code == "hyb" else codes.code_table(code, 16)
 src = (synth.gaussian_source(nseq, T, seed=5000).astype(np.float32) * np.float32(tab.std())).astype(np.float32)
-q = QTIPQuantizer(code, k)
+q = QTIPQuantizer(code, k, lut=lut)
 d = torch.from_numpy(src).cuda()
 q.encode(d[:8].contiguous())
 torch.cuda.synchronize()
@@ -29,10 +31,10 @@ st, cost = q.encode(d)
 e1.record()
 torch.cuda.synchronize()
 gpu_s = e0.elapsed_time(e1) / 1e3
-ncpu = 4
+ncpu = 4 if k * V <= 4 else 1
 os.environ.setdefault("OMP_NUM_THREADS", "1")
 t0 = time.perf_counter()
-viterbi.tailbite_encode_f32_batch(src[:ncpu], 16, k, 1, tab.astype(np.float32))
+viterbi.tailbite_encode_f32_batch(src[:ncpu], 16, k, V, tab.astype(np.float32))
 cpu_s = (time.perf_counter() - t0) / ncpu
 print(f"{code} k={k} T={T}: GPU {nseq} sequences in {gpu_s * 1e3:.1f} ms = {gpu_s / nseq * 1e6:.1f} us/sequence "
       f"({nseq / gpu_s:.0f} seq/s, {nseq * T / gpu_s / 1e6:.2f} M weights/s); CPU oracle (binary32 DP, OMP threads="

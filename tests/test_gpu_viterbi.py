@@ -50,3 +50,38 @@ def test_c1_quantize_pack_decode_roundtrip(cuda_lib):
     np.testing.assert_allclose((err.astype(np.float64) ** 2).sum(axis=1), c, rtol=1e-4)
     mse = float(((dec / sd - W) ** 2).mean())
     assert 0.060 < mse < 0.080                                                # Table 1, 3INST tail-biting ~0.068
+
+
+@pytest.mark.parametrize("k,nseq,T", [(2, 8, 256), (3, 6, 128), (4, 4, 32), (2, 130, 16), (4, 3, 2)])
+def test_viterbi_hyb_matches_oracle_bit_exact(cuda_lib, k, nseq, T):
+    """HYB (V = 2) through the GPU quantizer: 2^(2k) predecessors per group, LUT code
+    with the bit-15 sign, walks and costs bit-exact vs the oracle's binary32 Algorithm 4."""
+    from paper_2406_11235_b200.quantize import QTIPQuantizer
+    lut = synth.gaussian_lut(9, 4000)
+    tab = codes.code_table("hyb", 16, lut=lut, Q=9)
+    S = synth.gaussian_source(nseq, T, seed=6000 + k + T)
+    src = (S.astype(np.float32) * np.float32(tab.std())).astype(np.float32)
+    st, cost = QTIPQuantizer("hyb", k, lut=lut).encode(torch.from_numpy(src).cuda())
+    ref_st, ref_cost = viterbi.tailbite_encode_f32_batch(src, 16, k, 2, tab.astype(np.float32))
+    assert np.array_equal(st.cpu().numpy().view(np.uint32), ref_st)
+    assert np.array_equal(cost.cpu().numpy(), ref_cost)
+
+
+def test_hyb_quantize_pack_decode_roundtrip(cuda_lib):
+    """HYB k=2 tiles -> GPU walks -> pack -> decode reproduces the reported squared errors."""
+    from paper_2406_11235_b200 import qtip
+    from paper_2406_11235_b200.layer import QTIPLinear
+    from paper_2406_11235_b200.quantize import QTIPQuantizer
+    m, n, k = 64, 128, 2
+    lut = synth.gaussian_lut(9, 4000)
+    tab = codes.code_table("hyb", 16, lut=lut, Q=9)
+    sd = np.float32(tab.std())
+    W = synth.gaussian_source(m, n, seed=6100).astype(np.float32)
+    walks, cost = QTIPQuantizer("hyb", k, lut=lut).quantize_tiles(torch.from_numpy(W), sd)
+    layer = QTIPLinear(m, n, code="hyb", k=k)
+    layer.load_tiles(synth.random_tiles(m, n, k, seed=1), synth.random_sign_bytes(m, 1), synth.random_sign_bytes(n, 2),
+                     lut=lut)
+    qtip.qtip_pack_states(layer.p, m, n, walks, layer.packed)
+    dec = layer.decode(out_f32=True).cpu().numpy()
+    err = (dec - W * sd).reshape(m // 16, 16, n // 16, 16).transpose(0, 2, 1, 3).reshape(-1, 256)
+    np.testing.assert_allclose((err.astype(np.float64) ** 2).sum(axis=1), cost.cpu().numpy(), rtol=1e-4)
