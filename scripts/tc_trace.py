@@ -5,6 +5,7 @@ import numpy as np, torch, synth
 from paper_2406_11235_b200 import qtip
 from paper_2406_11235_b200.layer import QTIPLinear
 lib = qtip.load()
+qtip.set_matvec_impl(int(os.environ.get("QTIP_IMPL", "0")))
 m, n = int(sys.argv[1]) if len(sys.argv) > 1 else 11008, 4096
 lay = QTIPLinear(m, n).load_tiles(synth.random_tiles(m, n, 2), synth.random_sign_bytes(m, 1), synth.random_sign_bytes(n, 2))
 x = torch.from_numpy(synth.random_x(1, n)).cuda()
