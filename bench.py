@@ -6,8 +6,11 @@ Step (default workload `llama2-7b`, BASELINE configs[1]): one batch-1 decode tok
 linear layers of all 32 Llama-2-7B decoder blocks -- q, k, v, o (4096x4096), gate, up
 (11008x4096), down (4096x11008) -- each layer = RHT-in -> fused decode-GEMV -> RHT-out, k=2 3INST,
 L=16, V=1, T=256 tail-biting, every layer its own weights (1.62 GB of packed stream > 126 MB L2,
-so no layer is L2-resident when it is read again next step).  value = compressed bytes / step
-time (GB/s), whole job.  With torchrun (N>1) every layer is row-sharded across ranks and the
+so no layer is L2-resident when it is read again next step).  Within a block the model's data
+dependencies hold: q, k, v (same input) run concurrently, then o, then gate and up concurrently,
+then down (fork/join streams inside the CUDA graph); config.step_serial_ms is the same step with
+every layer strictly after the previous one.  value = compressed bytes / step time (GB/s), whole
+job.  With torchrun (N>1) every layer is row-sharded across ranks and the
 y~ shards are all-gathered over NCCL before the replicated RHT-out (strong scaling).
 
 `--impl reference` times the CPU oracle (the tier's reference arm) on a bounded sample.
@@ -33,6 +36,14 @@ WORKLOADS = {
     "llama2-70b": (80, [(8192, 8192), (1024, 8192), (1024, 8192), (8192, 8192), (28672, 8192), (28672, 8192),
                         (8192, 28672)], "hyb", 3),
     "c4-70b": (8, [(8192, 28672), (28672, 8192)], "3inst", 2),
+}
+# Data dependencies inside a block (the model's): q, k, v read the same normalised input, as do
+# gate and up, so each group runs concurrently (fork/join streams inside the graph); the groups
+# themselves are sequential (o needs attention over q, k, v; down needs silu(gate) * up).
+GROUPS = {
+    "llama2-7b": [[0, 1, 2], [3], [4, 5], [6]],
+    "llama2-70b": [[0, 1, 2], [3], [4, 5], [6]],
+    "c4-70b": [[0], [1]],
 }
 
 
@@ -220,12 +231,33 @@ def run_ours(args):
     outs = [torch.empty((B, lay.m), dtype=torch.float32, device=dev) for lay in layers]
     step_bytes = sum(m * n * k // 8 for (m, n) in shapes) * nblocks
 
-    def step():
-        for lay, o in zip(layers, outs):
-            if world == 1:
-                lay.forward(xs[lay.n], out=o)
-            else:
-                o.copy_(lay.forward(xs[lay.n]))
+    groups = GROUPS[args.workload]
+    side = [torch.cuda.Stream(device=dev) for _ in range(max(len(g) for g in groups) - 1)]
+
+    def run_layer(i):
+        lay, o = layers[i], outs[i]
+        if world == 1:
+            lay.forward(xs[lay.n], out=o)
+        else:
+            o.copy_(lay.forward(xs[lay.n]))
+
+    def step(serial=False):
+        nl = len(shapes)
+        for blk in range(nblocks):
+            for grp in groups:
+                if serial or len(grp) == 1:
+                    for i in grp:
+                        run_layer(blk * nl + i)
+                    continue
+                cur = torch.cuda.current_stream()
+                for si in range(len(grp) - 1):                  # fork after the previous group
+                    side[si].wait_stream(cur)
+                run_layer(blk * nl + grp[0])
+                for si, i in enumerate(grp[1:]):
+                    with torch.cuda.stream(side[si]):
+                        run_layer(blk * nl + i)
+                for si in range(len(grp) - 1):                  # join
+                    cur.wait_stream(side[si])
 
     # eager warm-up (Hadamard tables, workspaces, NCCL communicators), then capture one step
     for _ in range(2):
@@ -267,6 +299,24 @@ def run_ours(args):
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     value = step_bytes / (ms * 1e-3) / 1e9
+
+    # the same step with every layer strictly after the previous one (no group concurrency)
+    gs = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(gs, stream=s):
+            step(serial=True)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        gs.replay()
+    barrier()
+    es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es0.record()
+    for _ in range(args.steps):
+        gs.replay()
+    es1.record()
+    torch.cuda.synchronize()
+    ms_serial = max_over_ranks(es0.elapsed_time(es1) / args.steps)
+    del gs
 
     # ---- per-shape layer latency (graph of one layer, replayed) for us/layer reporting
     per_layer = {}
@@ -367,6 +417,9 @@ def run_ours(args):
                        "code": code, "k": k, "L": 16, "V": 2 if code == "hyb" else 1, "T": 256, "batch": B,
                        "stream_bytes_per_step": step_bytes, "tokens_per_s_equiv": round(B * 1e3 / ms, 2),
                        "per_layer": per_layer, "parallelism": f"rows{world}" if world > 1 else "single",
+                       "dependency": "block: q|k|v and gate|up concurrent, groups sequential",
+                       "step_serial_ms": round(ms_serial, 5),
+                       "serial_GBps": round(step_bytes / (ms_serial * 1e-3) / 1e9, 2),
                        "l2": "inputs > L2: 1.62 GB of distinct packed weights per step (126 MB L2)"
                        if args.workload == "llama2-7b" else "distinct weights per layer",
                        "matvec_impl": qtip.get_matvec_impl(),
