@@ -36,6 +36,7 @@
 // order (deterministic and independent of the grid or of row sharding).
 #include "decode.cuh"
 #include "internal.h"
+#include "mma_tile.cuh"
 #include "tc.cuh"
 
 namespace qtip {
@@ -63,8 +64,35 @@ namespace {
 constexpr int kGroups = 4;
 constexpr int kDecWarps = 4 * kGroups;
 constexpr int kThreads = 32 * (1 + kDecWarps + kGroups);   // 672: producer + 16 decoders + 4 issuers
-constexpr int kSlots = 8;
+#ifndef QTIP_TC_SLOTS
+#define QTIP_TC_SLOTS 8
+#endif
+constexpr int kSlots = QTIP_TC_SLOTS;
 constexpr int kABufs = 3;
+// Ablation switches (compile-time, all off in the product build; scripts/tc_ablation.sh builds the
+// variants, profiles/r1b_tc_ablation.txt holds the rates).  QTIP_TC_PIPE=1 selects the
+// software-pipelined 3INST/1MAD k = 2 hand-off (decode into registers, then hand off the previous
+// stores); the others act on that branch: NODECODE stores raw words, NOMMA makes the issuer commit
+// without MMAs, NOST skips the TMEM stores, NOSYNC drops the decoder <-> issuer mbarrier protocol
+// (results are then wrong: rate experiments only).  QTIP_TC_EPI_H = hand-off index of the epilogue.
+#ifndef QTIP_TC_NODECODE
+#define QTIP_TC_NODECODE 0
+#endif
+#ifndef QTIP_TC_NOMMA
+#define QTIP_TC_NOMMA 0
+#endif
+#ifndef QTIP_TC_NOST
+#define QTIP_TC_NOST 0
+#endif
+#ifndef QTIP_TC_NOSYNC
+#define QTIP_TC_NOSYNC 0
+#endif
+#ifndef QTIP_TC_PIPE
+#define QTIP_TC_PIPE 0
+#endif
+#ifndef QTIP_TC_EPI_H
+#define QTIP_TC_EPI_H 3
+#endif
 constexpr int kHybLutQ = 9;
 constexpr uint32_t kLutBytes = (1u << (kHybLutQ + 1)) * 128u;   // 2^(Q+1) entries x 32 replicas x 4 B
 constexpr int kN = 16;                                          // UMMA N (batch padded)
@@ -167,6 +195,34 @@ __device__ __forceinline__ void decode_handoff(const uint32_t* __restrict__ pw, 
     }
 }
 
+// 3INST / 1MAD k = 2: this thread's row of the two tiles of a hand-off into registers, windows
+// paired (q, q + 8) out of one funnel word F_q = bits [2q, 2q + 32) of the row (mma_tile.cuh
+// lcg_pair: 1.94 ALU + 1.5 FMA ops per weight instead of 2.44 + 1 for the byte-permute windows).
+template <int CODE>
+__device__ __forceinline__ void decode_k2_regs(const uint32_t* __restrict__ pw, int r, const CodeArgs& ca,
+                                               uint32_t (&z)[2][16]) {
+    const uint2 A = *reinterpret_cast<const uint2*>(pw + 2 * r);
+    const uint2 Bw = *reinterpret_cast<const uint2*>(pw + 2 * ((r + 1) & 15));
+    const mma::Lcg<CODE, false> lcg(ca);
+#pragma unroll
+    for (int tt = 0; tt < 2; ++tt) {
+        const uint32_t a = tt ? A.y : A.x, b = tt ? Bw.y : Bw.x;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t F = q ? __funnelshift_l(b, a, 2 * q) : a;
+            mma::lcg_pair<CODE, CODE == QTIP_CODE_3INST, false>(F, lcg, ca.magic, z[tt][q], z[tt][q + 8]);
+        }
+    }
+}
+
+// One mbarrier arrival per warp instead of 32 (the barriers count warps): the warp's own
+// completed work (tcgen05.wait::st, finished shared-memory reads) is ordered before lane 0's
+// release-arrive by the __syncwarp.
+__device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(bar);
+}
+
 template <int K, int CODE>
 __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args) {
     using C = Cfg<K, CODE>;
@@ -214,12 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
         if (lane == 0) {
             for (int s = 0; s < kSlots; ++s) {
                 ptx::mbar_init(full(s), 1);
-                ptx::mbar_init(empty(s), 128);
+                ptx::mbar_init(empty(s), 4);                 // one arrival per decoder warp
             }
             for (int g = 0; g < kGroups; ++g) {
                 for (int b = 0; b < kABufs; ++b) {
                     ptx::mbar_init(aempty(g, b), 1);
-                    ptx::mbar_init(afull(g, b), 128);
+                    ptx::mbar_init(afull(g, b), 4);
                 }
                 for (int b = 0; b < 2; ++b) ptx::mbar_init(dfull(g, b), 1);
             }
@@ -256,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
         const uint32_t bdesc_lo0 = (ptx::smem_u32(bbuf + 2 * g * C::kBGroup) >> 4) | ((128u >> 4) << 16);
         constexpr uint32_t kBDescHi = (256u >> 4) | (1u << 14);
         const int my_unit_count = (nunits > g) ? (nunits - g + kGroups - 1) / kGroups : 0;
-        for (int lu = 0; lu < my_unit_count; ++lu) {
+        for (int lu = 0; lu < (QTIP_TC_NOSYNC ? 0 : my_unit_count); ++lu) {
             const uint32_t db = lu & 1;
             const uint32_t bdesc_lo = bdesc_lo0 + db * (C::kBGroup >> 4);
             const uint32_t dcol = tgrp + 16u * db;
@@ -267,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
                 ptx::mbar_wait(afull(g, b), (hc / kABufs) & 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
+#if !QTIP_TC_NOMMA
                     const uint32_t acol = tgrp + 32u + 32u * (uint32_t)b;
 #pragma unroll
                     for (int tt = 0; tt < 2; ++tt) {
@@ -278,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
                                              (h | tt | half) != 0);
                         }
                     }
+#endif
                     ptx::umma_commit(aempty(g, b));
                     if (h == 3) ptx::umma_commit(dfull(g, db));
                     QTIP_TRACE(g * 64 + hc, 4);
@@ -312,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
             const int j = g + kGroups * lp;
             const int64_t u = u0 + j;
             const int64_t RB = args.rb0 + u / n_kc, KC = u % n_kc;
-            ptx::mbar_wait(dfull(g, lp & 1), (lp >> 1) & 1);
+            if (!QTIP_TC_NOSYNC) ptx::mbar_wait(dfull(g, lp & 1), (lp >> 1) & 1);
             ptx::tc_fence_after();
             uint32_t d[16];
             ptx::tmem_ld16(taddr_lane + 16u * (lp & 1), d);
@@ -356,19 +414,57 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
                 const uint32_t use = hc / kABufs;                      // earlier uses of A buffer b
                 const bool tr = (lane == 0 && wg == 0);
                 if (tr) QTIP_TRACE(g * 64 + hc, 0);
-                if (use > 0) ptx::mbar_wait(aempty(g, b), (use - 1) & 1);
-                if (tr) QTIP_TRACE(g * 64 + hc, 1);
-                ptx::tc_fence_after();
-                decode_handoff<K, CODE>(slot + (I * 4 + h) * (8 * K) * 2, r, args.ca, lane4, lut_base,
-                                        taddr_lane + 32u + 32u * b);
-                if (h == 3) ptx::mbar_arrive(empty(s));               // all reads of this slot done
-                if (tr) QTIP_TRACE(g * 64 + hc, 2);
+                if constexpr (K == 2 && !C::kHyb && QTIP_TC_PIPE) {
+                    // software-pipelined hand-off: decode into registers first, then complete and
+                    // hand off the previous hand-off's stores (issued a whole decode earlier, so the
+                    // wait is short), then claim this buffer and store
+                    uint32_t z[2][16];
+#if QTIP_TC_NODECODE
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) { z[0][i] = slot[i] ^ r; z[1][i] = slot[i] + r; }
+#else
+                    decode_k2_regs<CODE>(slot + (I * 4 + h) * (8 * K) * 2, r, args.ca, z);
+#endif
+                    if (h == 3) warp_arrive(empty(s), lane);           // all reads of this slot done
+                    if (tr) QTIP_TRACE(g * 64 + hc, 2);
+                    if (hc > 0) {
+                        ptx::tc_wait_st();
+                        ptx::tc_fence_before();
+                        if (!QTIP_TC_NOSYNC) warp_arrive(afull(g, (int)((hc - 1) % kABufs)), lane);
+                    }
+                    if (use > 0 && !QTIP_TC_NOSYNC) ptx::mbar_wait(aempty(g, b), (use - 1) & 1);
+                    if (tr) QTIP_TRACE(g * 64 + hc, 1);
+                    ptx::tc_fence_after();
+                    if (!QTIP_TC_NOST) {
+                        ptx::tmem_st16(taddr_lane + 32u + 32u * b, z[0]);
+                        ptx::tmem_st16(taddr_lane + 32u + 32u * b + 16u, z[1]);
+                    } else if ((z[0][3] ^ z[1][7]) == 0x12345u) {
+                        args.partial[r] = 0.f;
+                    }
+                    if (tr) QTIP_TRACE(g * 64 + hc, 3);
+                    if (h == QTIP_TC_EPI_H && lu > 0) epilogue(lu - 1);  // previous cell's MMAs are long issued
+                } else {
+                    if (use > 0) ptx::mbar_wait(aempty(g, b), (use - 1) & 1);
+                    if (tr) QTIP_TRACE(g * 64 + hc, 1);
+                    ptx::tc_fence_after();
+                    decode_handoff<K, CODE>(slot + (I * 4 + h) * (8 * K) * 2, r, args.ca, lane4, lut_base,
+                                            taddr_lane + 32u + 32u * b);
+                    if (h == 3) warp_arrive(empty(s), lane);           // all reads of this slot done
+                    if (tr) QTIP_TRACE(g * 64 + hc, 2);
+                    ptx::tc_wait_st();
+                    ptx::tc_fence_before();
+                    warp_arrive(afull(g, b), lane);                     // hand-off to the group's issuer
+                    if (tr) QTIP_TRACE(g * 64 + hc, 3);
+                    if (h == 0 && lu > 0) epilogue(lu - 1);           // drain the previous cell's D
+                }
+                if (tr) QTIP_TRACE(g * 64 + hc, 5);
+            }
+        }
+        if constexpr (K == 2 && !C::kHyb && QTIP_TC_PIPE) {
+            if (my_unit_count > 0) {                                   // hand off the last hand-off
                 ptx::tc_wait_st();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(afull(g, b));                         // hand-off to the group's issuer
-                if (tr) QTIP_TRACE(g * 64 + hc, 3);
-                if (h == 0 && lu > 0) epilogue(lu - 1);               // drain the previous cell's D
-                if (tr) QTIP_TRACE(g * 64 + hc, 5);
+                if (!QTIP_TC_NOSYNC) warp_arrive(afull(g, (int)((4u * my_unit_count - 1) % kABufs)), lane);
             }
         }
         if (my_unit_count > 0) epilogue(my_unit_count - 1);

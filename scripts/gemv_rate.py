@@ -21,7 +21,7 @@ k = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 m = int(sys.argv[4]) if len(sys.argv) > 4 else 37888
 n = int(sys.argv[5]) if len(sys.argv) > 5 else 4096
 B = int(sys.argv[6]) if len(sys.argv) > 6 else 1
-qtip.load()
+qtip.load(os.environ.get("QTIP_LIB", qtip.LIB_PATH))
 qtip.set_matvec_impl(impl)
 lut = synth.gaussian_lut(9) if code == "hyb" else None
 sms = torch.cuda.get_device_properties(0).multi_processor_count
