@@ -36,6 +36,9 @@ WORKLOADS = {
     "llama2-70b": (80, [(8192, 8192), (1024, 8192), (1024, 8192), (8192, 8192), (28672, 8192), (28672, 8192),
                         (8192, 28672)], "hyb", 3),
     "c4-70b": (8, [(8192, 28672), (28672, 8192)], "3inst", 2),
+    # the 7B block with q,k,v and gate,up stacked into one matrix each (one RHT over the stacked
+    # output): the same weight bytes in 4 layers per block
+    "llama2-7b-stacked": (32, [(12288, 4096), (4096, 4096), (22016, 4096), (4096, 11008)], "3inst", 2),
 }
 # Data dependencies inside a block (the model's): q, k, v read the same normalised input, as do
 # gate and up, so each group runs concurrently (fork/join streams inside the graph); the groups
@@ -44,6 +47,7 @@ GROUPS = {
     "llama2-7b": [[0, 1, 2], [3], [4, 5], [6]],
     "llama2-70b": [[0, 1, 2], [3], [4, 5], [6]],
     "c4-70b": [[0], [1]],
+    "llama2-7b-stacked": [[0], [1], [2], [3]],
 }
 
 

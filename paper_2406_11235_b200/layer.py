@@ -53,6 +53,8 @@ class QTIPLinear:
         r0, r1 = rows if rows is not None else (0, self.m)
         if out is None:
             out = torch.empty((B, r1 - r0), dtype=torch.float32, device=self.device)
+        if B == 0:                                  # empty batch: nothing to compute, no launch
+            return out
         qtip.qtip_matvec(self.p, self.m, self.n, B, self.packed, self.lut, self.sign_n, self.sign_m, self.scale,
                          x, out, r0, r1, flags, self.workspace(B), stream)
         return out

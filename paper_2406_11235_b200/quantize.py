@@ -38,6 +38,8 @@ class QTIPQuantizer:
         nseq, T = src_code_units.shape
         states = torch.empty((nseq, T // self.V), dtype=torch.int32, device=self.device)
         cost = torch.empty(nseq, dtype=torch.float32, device=self.device)
+        if nseq == 0:                               # no sequences: nothing to encode, no launch
+            return states, cost
         qtip.qtip_viterbi_tailbite(self.p, nseq, T, src_code_units, states, cost, self.workspace(T), d_lut=self.lut)
         return states, cost
 

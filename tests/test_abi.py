@@ -114,3 +114,32 @@ def test_host_validation_before_any_launch(lib):
     states = np.zeros((1, 1, 256), dtype=np.uint32)
     states[0, 0, 5] = 0xFFFF
     assert lib.qtip_pack_states(ctypes.byref(p), 16, 16, states.ctypes.data_as(vp), vp(256), None) == -3
+
+
+def test_degenerate_arguments_are_refused(lib):
+    """Empty and out-of-range sizes return a status (include/qtip.h) before any device access;
+    the Python layers map an empty batch / no sequences to an empty result without a call."""
+    p = qtip.params_default("3inst", 2)
+    vp, f1, ws = ctypes.c_void_p, ctypes.c_float(1.0), 1 << 20
+
+    def mv(m=256, n=256, B=1, r0=0, r1=256, flags=3, sn=vp(256), sm=vp(256)):
+        return lib.qtip_matvec(ctypes.byref(p), m, n, B, vp(256), None, sn, sm, f1, vp(256), vp(512), r0, r1,
+                               flags, vp(256), ws, None)
+    assert mv(B=0) == -1 and mv(B=65) == -1                        # batch 1..64
+    assert mv(r0=128, r1=128, flags=0) == -2                       # empty row range
+    assert mv(m=0, r1=0) == -2 and mv(n=0) == -2 and mv(m=250, r1=250) == -2   # multiples of 16
+    assert mv(flags=8) == -1                                       # unknown flag
+    assert mv(sn=None) == -1 and mv(sm=None) == -1                 # RHT without its signs
+    assert lib.qtip_rht(256, 0, vp(16), vp(16), vp(32), 0, None) == -2
+    assert lib.qtip_rht(0, 1, vp(16), vp(16), vp(32), 0, None) == -2
+    pv = qtip.params_default("3inst", 2)
+
+    def vt(nseq=1, T=256, pp=pv):
+        return lib.qtip_viterbi_tailbite(ctypes.byref(pp), nseq, T, vp(256), None, vp(256), vp(256), vp(256),
+                                         1 << 30, None)
+    assert vt(nseq=0) == -2 and vt(T=1) == -2 and vt(T=4097) == -2
+    ph = qtip.params_default("hyb", 2)
+    assert vt(T=255, pp=ph) == -2                                  # V = 2 must divide T
+    p4 = qtip.params_default("3inst", 4)
+    assert vt(pp=p4) == -5                                         # V = 1 Viterbi: k in {2, 3}
+

@@ -318,3 +318,53 @@ def test_hyb_two_sign_matvec(cuda_lib, k, impl):
     ref = gemv.matvec(gemv.dense_decode(tiles, p), x.astype(np.float64), synth.random_sign_bytes(n, 3000 + 7),
                       synth.random_sign_bytes(m, 3001 + 7), scale=0.6)
     assert rel_l2(y, ref) <= MATVEC_TOL
+
+
+def test_empty_batch_is_a_no_op(cuda_lib):
+    """B = 0: an empty (0, m) result and no kernel launch (the ABI itself refuses B < 1)."""
+    layer = make_layer(cuda_lib, 256, 256, "3inst", 2, synth.random_tiles(256, 256, 2, seed=3))
+    c0 = cuda_lib.launch_count()
+    y = layer(torch.empty((0, 256), dtype=torch.float32, device="cuda"))
+    assert tuple(y.shape) == (0, 256) and cuda_lib.launch_count() == c0
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_zero_input_gives_exact_zero(cuda_lib, impl):
+    """x = 0: every path returns exact zeros (no NaN from the fp16 x~ or the scale)."""
+    m, n = 384, 768
+    layer = make_layer(cuda_lib, m, n, "hyb", 3, synth.random_tiles(m, n, 3, seed=4), lut_for("hyb"), scale=3.0)
+    cuda_lib.set_matvec_impl(impl)
+    try:
+        y = layer(torch.zeros((2, n), dtype=torch.float32, device="cuda")).cpu().numpy()
+    finally:
+        cuda_lib.set_matvec_impl(0)
+    assert np.array_equal(y, np.zeros_like(y))
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("m,n", [(16, 16), (16, 48), (48, 16)])
+def test_smallest_layers(cuda_lib, impl, m, n):
+    """One-tile-high / one-tile-wide layers (less than one 128-row block, one K-chunk)."""
+    tiles = synth.random_tiles(m, n, 2, seed=m + n)
+    layer = make_layer(cuda_lib, m, n, "3inst", 2, tiles, None, seed=6, scale=0.5)
+    x = synth.random_x(1, n, seed=7)
+    cuda_lib.set_matvec_impl(impl)
+    try:
+        y = layer(torch.from_numpy(x).cuda()).cpu().numpy()
+    finally:
+        cuda_lib.set_matvec_impl(0)
+    ref = _oracle_matvec(tiles, "3inst", 2, None, m, n, x, 6, 0.5)
+    assert rel_l2(y, ref) <= (1e-5 if impl == 1 else MATVEC_TOL)
+
+
+@pytest.mark.parametrize("code,k", [("3inst", 2), ("hyb", 4)])
+def test_maximum_batch(cuda_lib, code, k):
+    """B = 64, the largest batch the ABI accepts (auto kernel choice)."""
+    m, n = 256, 512
+    tiles = synth.random_tiles(m, n, k, seed=21)
+    lut = lut_for(code)
+    layer = make_layer(cuda_lib, m, n, code, k, tiles, lut, seed=8)
+    x = synth.random_x(64, n, seed=22)
+    y = layer(torch.from_numpy(x).cuda()).cpu().numpy()
+    ref = _oracle_matvec(tiles, code, k, lut, m, n, x, 8, 1.0)
+    assert rel_l2(y, ref) <= MATVEC_TOL

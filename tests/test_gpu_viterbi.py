@@ -85,3 +85,13 @@ def test_hyb_quantize_pack_decode_roundtrip(cuda_lib):
     dec = layer.decode(out_f32=True).cpu().numpy()
     err = (dec - W * sd).reshape(m // 16, 16, n // 16, 16).transpose(0, 2, 1, 3).reshape(-1, 256)
     np.testing.assert_allclose((err.astype(np.float64) ** 2).sum(axis=1), cost.cpu().numpy(), rtol=1e-4)
+
+
+def test_no_sequences_is_a_no_op(cuda_lib):
+    """nseq = 0: empty walks and costs, no launch (the ABI itself refuses nseq < 1)."""
+    import torch
+    from paper_2406_11235_b200.quantize import QTIPQuantizer
+    q = QTIPQuantizer("3inst", 2)
+    c0 = cuda_lib.launch_count()
+    w, c = q.encode(torch.empty((0, 256), dtype=torch.float32, device="cuda"))
+    assert tuple(w.shape) == (0, 256) and tuple(c.shape) == (0,) and cuda_lib.launch_count() == c0
