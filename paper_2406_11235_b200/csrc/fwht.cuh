@@ -28,13 +28,15 @@ __device__ __forceinline__ int fwht_fast(float (&v)[E], int a, float* scr) {
                 v[e] = x0 + x1;
                 v[e | h] = x0 - x1;
             }
+    // shuffle butterflies: (lane & h) ? o - v : v + o  ==  fma(v, +-1, o), one rounding either way
     const int lb = a - s < 5 ? a - s : 5;
-    for (int j = 0; j < lb; ++j) {
-        const int h = 1 << j;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const float o = __shfl_xor_sync(0xffffffffu, v[e], h);
-            v[e] = (lane & h) ? o - v[e] : v[e] + o;
+    for (int j = 0; j < 5; ++j) {
+        if (j < lb) {
+            const int h = 1 << j;
+            const float sg = (lane & h) ? -1.0f : 1.0f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = fmaf(v[e], sg, __shfl_xor_sync(0xffffffffu, v[e], h));
         }
     }
     const int wb = a - s - 5;
@@ -57,12 +59,13 @@ __device__ __forceinline__ int fwht_fast(float (&v)[E], int a, float* scr) {
             v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
         }
     }
-    for (int j = 0; j < wb; ++j) {
-        const int h = 1 << (5 - wb + j);
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const float o = __shfl_xor_sync(0xffffffffu, v[e], h);
-            v[e] = (lane & h) ? o - v[e] : v[e] + o;
+    for (int j = 0; j < 5; ++j) {
+        if (j < wb) {
+            const int h = 1 << (5 - wb + j);
+            const float sg = (lane & h) ? -1.0f : 1.0f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = fmaf(v[e], sg, __shfl_xor_sync(0xffffffffu, v[e], h));
         }
     }
     __syncthreads();                                                // scr may be reused
@@ -102,13 +105,17 @@ __device__ __forceinline__ void tile_read(const float* scr, int tile, float (&o)
 // consecutive tiles, 64 B apart: rotation spreads a store instruction over 8 bank groups)
 template <bool kHyb, bool kSwap = false>
 __device__ __forceinline__ void put_tile(uint32_t* dst, const float (&v)[16]) {
-    auto h = [&](int c) { return (uint32_t)__half_as_ushort(__float2half_rn(v[c])); };
+    // one packed f32x2 -> f16x2 conversion (round to nearest) per word; low half = first argument
+    auto h2 = [&](float lo, float hi) {
+        const __half2 q = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<const uint32_t*>(&q);
+    };
     if constexpr (!kHyb) {
         uint4 w[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {                               // words 4j..4j+3 = cols 2j, 2j+8, 2j+1, 2j+9
-            const uint32_t a = h(2 * j), b = h(2 * j + 8), c = h(2 * j + 1), d = h(2 * j + 9);
-            w[j] = make_uint4(a | (a << 16), b | (b << 16), c | (c << 16), d | (d << 16));
+            w[j] = make_uint4(h2(v[2 * j], v[2 * j]), h2(v[2 * j + 8], v[2 * j + 8]), h2(v[2 * j + 1], v[2 * j + 1]),
+                              h2(v[2 * j + 9], v[2 * j + 9]));
         }
         const int r = (threadIdx.x >> 1) & 3;
 #pragma unroll
@@ -125,7 +132,7 @@ __device__ __forceinline__ void put_tile(uint32_t* dst, const float (&v)[16]) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int ww = 4 * j + k, pr = 4 * (ww & 1) + (ww >> 1);
-                u[k] = kSwap ? (h(2 * pr + 1) | (h(2 * pr) << 16)) : (h(2 * pr) | (h(2 * pr + 1) << 16));
+                u[k] = kSwap ? h2(v[2 * pr + 1], v[2 * pr]) : h2(v[2 * pr], v[2 * pr + 1]);
             }
             w[j] = make_uint4(u[0], u[1], u[2], u[3]);
         }

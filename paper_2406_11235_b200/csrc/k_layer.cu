@@ -84,10 +84,12 @@ __device__ int g_layer_trace_cap = 0;
 // {tag 5, blockIdx, t0..t11} after a u64 record counter.
 constexpr int kMarks = 12;
 __shared__ unsigned long long g_trs[kMarks];
+__shared__ int g_trclk;                      // debug bit 4: SM clock64 marks (phase durations in cycles)
 __device__ __forceinline__ void trace_mark(bool on, int i) {
     if (on && threadIdx.x == 0) {
         unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (g_trclk) t = clock64();
+        else asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_trs[i] = t;
     }
 }
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     const int n_pairs = (int)(n_kc * 4);
 
     const bool tr = g_layer_trace != nullptr;
+    if (tr && threadIdx.x == 0) g_trclk = (args.debug & 4) != 0;
     if (tr && threadIdx.x == 0)
         for (int q = 0; q < kMarks; ++q) g_trs[q] = 0;
     trace_mark(tr, 0);

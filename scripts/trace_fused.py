@@ -73,6 +73,14 @@ t = t[order]
 P = 148
 t0 = t[:, 0].min()
 names = ["entry", "pdl", "staged", "fwht", "x~", "gemv", "red", "prol/sh", "bar2", "ystg", "fwho", "exit"]
+if debug & 4:                                   # SM clock64 marks: per-CTA cycles since its PDL release
+    raw = rec[:, 2:].astype(np.float64)
+    for j, nm in enumerate(names):
+        ok = (raw[:, j] > 0) & (raw[:, 1] > 0)
+        if ok.any():
+            d = raw[ok, j] - raw[ok, 1]
+            print(f"  {nm:8s} cycles after pdl release: median {np.median(d):8.0f}  max {np.max(d):8.0f}")
+    sys.exit(0)
 for li in range(NL):
     tl = (t[li * P:(li + 1) * P] - t0) / 1e3
     cols = []
