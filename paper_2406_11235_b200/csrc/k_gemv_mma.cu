@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : 6) g
         const uint32_t bar = ptx::smem_u32(full + st);
         const int64_t RB = args.rb0 + u / n_kc, KC = u % n_kc;
         ptx::mbar_arrive_expect_tx(bar, kCellBytes + kXRowBytes * (uint32_t)args.B);
-        ptx::bulk_g2s(ptx::smem_u32(stages + st * stage_bytes),
+        ptx::bulk_g2s_stream(ptx::smem_u32(stages + st * stage_bytes),
                       args.packed + (RB * n_kc + KC) * (int64_t)(kCellBytes / 4), kCellBytes, bar);
     };
     // the packed weights never depend on the previous kernel: start streaming them before the

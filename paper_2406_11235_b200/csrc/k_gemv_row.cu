@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
         const int64_t kc = warp + (int64_t)j * W;
         const uint32_t bar = ptx::smem_u32(full + st);
         ptx::mbar_arrive_expect_tx(bar, stage_bytes);
-        ptx::bulk_g2s(ptx::smem_u32(ring + st * stage_bytes),
+        ptx::bulk_g2s_stream(ptx::smem_u32(ring + st * stage_bytes),
                       args.packed + (RB * n_kc + kc) * (int64_t)(512 * K) + Il * (kChunkBytes / 4), kChunkBytes, bar);
     };
     auto issue_x = [&](int j) {                                      // lane 0: x~ columns of cell j

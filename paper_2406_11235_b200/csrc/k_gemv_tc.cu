@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_kernel(const TcArgs args)
                 const int64_t RB = args.rb0 + u / n_kc, KC = u % n_kc;
                 const uint32_t* src = args.packed + (RB * n_kc + KC) * args.lay.cell_words;
                 ptx::mbar_arrive_expect_tx(full(s), C::kUnitBytes);
-                ptx::bulk_g2s(ptx::smem_u32(stream + s * C::kUnitBytes), src, C::kUnitBytes, full(s));
+                ptx::bulk_g2s_stream(ptx::smem_u32(stream + s * C::kUnitBytes), src, C::kUnitBytes, full(s));
             }
         }
     } else if (warp > kDecWarps) {

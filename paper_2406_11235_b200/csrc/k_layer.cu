@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     // each lane arriving on the stage's mbarrier when its copies land.  Measured: one
     // cp.async.bulk per 512-B chunk (lane 0) capped the steady state at 8.6 weights/clk/SM
     // (scripts/gemv_rate.py); per-lane copies keep many more requests in flight.
+    const uint64_t wpol = ptx::l2_evict_first_policy();
     auto issue = [&](const UnitIt& it, int st) {
         const int I = (int)args.tile_row0 + it.Ir;
         const uint32_t bar = ptx::smem_u32(full + st);
@@ -366,9 +367,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
 #pragma unroll
         for (int q = 0; q < (16 * K + 31) / 32; ++q) {               // 16 K pieces of 16 B
             const int piece = lane + 32 * q;
-            if (piece < 16 * K)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * piece), "l"(src + 16 * piece)
-                             : "memory");
+            if (piece < 16 * K) ptx::cp_async16_stream(dst + 16 * piece, src + 16 * piece, wpol);
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
     };
@@ -512,7 +511,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     }
     __syncthreads();
     trace_mark(tr, 4);
-    ptx::pdl_launch_dependents();
+    const int pdl_at = (args.debug >> 3) & 3;                        // debug: 0 here, 1 after GEMV, 2 after reduction
+    if (pdl_at == 0) ptx::pdl_launch_dependents();
 
     // ---------------------------------------------------------------- GEMV over the warp's units
     const CodeArgs ca = args.ca;
@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     }
     __syncthreads();
     trace_mark(tr, 5);
+    if (pdl_at == 1) ptx::pdl_launch_dependents();
 
     // ---------------------------------------------------------------- reduction (warp per row)
     const bool rht_out = args.rht_out != 0;
@@ -632,7 +633,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         nrow_items = ((L1i - 1) / n_units - Ia + 1) * kTile * B;
     }
     const int tile_row0 = (int)args.tile_row0;
+    trace_mark(tr && rows_mode && !rht_out, 9);
     for (int t = warp; t < nrow_items; t += kLWarps) {
+        if (t == 0) trace_mark(tr && rows_mode && !rht_out, 10);
         const int tb = t / B, b = t - tb * B;
         const int Ir = Ia + (tb >> 4), r = tb & 15;
         const int i = (tile_row0 + Ir) * kTile + r;
@@ -641,7 +644,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             const float s = args.part_smem
                 ? warp_row_sum<false>(part + ((u0 - L0i) * kTile + r) * B + b, kTile * B, n_units)
                 : warp_row_sum<true>(args.gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
+            if (t == 0) trace_mark(tr && rows_mode && !rht_out, 7);       // debug: first row's sum
             if (lane == 0) finish(b, i, s);
+            if (t == 0) trace_mark(tr && rows_mode && !rht_out, 8);
         } else if (args.part_smem) {                                  // shared row: publish this CTA's units
             const int s_lo = L0i - u0 > 0 ? L0i - u0 : 0, s_hi = L1i - u0 < n_units ? L1i - u0 : n_units;
             for (int u = s_lo + lane; u < s_hi; u += 32)
@@ -649,6 +654,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         }
     }
     trace_mark(tr, 6);
+    if (pdl_at == 2) ptx::pdl_launch_dependents();
     if (rows_mode) {
         // no shared rows.  RHT-out: every CTA takes a ticket after publishing its y~ rows; the last
         // `finishers` arrivals run the RHT-out (the very last one alone when m = 2^a), the others
@@ -706,7 +712,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         if (slot < (unsigned long long)g_layer_trace_cap) {
             unsigned long long* r = g_layer_trace + 1 + (kMarks + 2) * slot;
             r[0] = 5;
-            r[1] = blockIdx.x;
+            r[1] = blockIdx.x | ((unsigned long long)args.part_smem << 32) | ((unsigned long long)args.stages << 40);
             for (int q = 0; q < kMarks; ++q) r[2 + q] = g_trs[q];
         }
     }

@@ -83,6 +83,33 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
+// Streamed-once data (the packed weights): L2 evict-first, so a step's 1.6 GB of weights does not
+// push the small reused lines (x~, partial sums, kernel code and tables) out of L2.
+#ifndef QTIP_EVICT_FIRST
+#define QTIP_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_stream(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+#if QTIP_EVICT_FIRST
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(l2_evict_first_policy())
+        : "memory");
+#else
+    bulk_g2s(dst, src, bytes, bar);
+#endif
+}
+__device__ __forceinline__ void cp_async16_stream(uint32_t dst, const void* src, uint64_t pol) {
+#if QTIP_EVICT_FIRST
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+#else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

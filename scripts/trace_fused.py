@@ -75,6 +75,7 @@ t0 = t[:, 0].min()
 names = ["entry", "pdl", "staged", "fwht", "x~", "gemv", "red", "prol/sh", "bar2", "ystg", "fwho", "exit"]
 if debug & 4:                                   # SM clock64 marks: per-CTA cycles since its PDL release
     raw = rec[:, 2:].astype(np.float64)
+    print(f"  part_smem {int(rec[0, 1]) >> 32 & 0xff}  ring stages {int(rec[0, 1]) >> 40}")
     for j, nm in enumerate(names):
         ok = (raw[:, j] > 0) & (raw[:, 1] > 0)
         if ok.any():
