@@ -139,10 +139,31 @@ template <bool kGlobal>
 __device__ __forceinline__ float warp_row_sum(const float* p, int64_t st, int nu) {
     const int lane = threadIdx.x & 31;
     float t = 0.0f;
-    for (int u = lane; u < nu; u += 32) t += kGlobal ? __ldcg(p + u * st) : p[u * st];
+#pragma unroll 1
+    for (int u = lane; u < nu; u += 32) t += kGlobal ? __ldcg(p + u * st) : p[u * st];   // compact: cold code
 #pragma unroll
     for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     return t;
+}
+
+// The same canonical sum (bit for bit: lane-strided partial sums, then the xor-butterfly tree seen
+// from lane 0) computed by ONE thread, so a CTA reduces many rows in parallel (one thread per row)
+// instead of one warp per row.
+__device__ __forceinline__ float thread_row_sum(const float* p, int st, int nu) {
+    float s[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) s[l] = 0.0f;
+#pragma unroll 1
+    for (int u0 = 0; u0 < nu; u0 += 32) {
+#pragma unroll
+        for (int l = 0; l < 32; ++l)
+            if (u0 + l < nu) s[l] += p[(u0 + l) * st];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int l = 0; l < o; ++l) s[l] += s[l + o];
+    return s[0];
 }
 
 // One radix-2^R pass of the Walsh-Hadamard butterflies on index bits [p, p + R) of v (swizzled).
@@ -634,6 +655,17 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     }
     const int tile_row0 = (int)args.tile_row0;
     trace_mark(tr && rows_mode && !rht_out, 9);
+    if (rows_mode && args.part_smem) {
+        // every row of this CTA is complete here: one thread per (row, batch) item
+        for (int t = threadIdx.x; t < nrow_items; t += kLThreads) {
+            const int tb = t / B, b = t - tb * B;
+            const int Ir = Ia + (tb >> 4), r = tb & 15;
+            const int i = (tile_row0 + Ir) * kTile + r;
+            const int u0 = Ir * n_units;
+            finish(b, i, thread_row_sum(part + ((u0 - L0i) * kTile + r) * B + b, kTile * B, n_units));
+        }
+        nrow_items = 0;                                               // nothing left for the warp loop
+    }
     for (int t = warp; t < nrow_items; t += kLWarps) {
         if (t == 0) trace_mark(tr && rows_mode && !rht_out, 10);
         const int tb = t / B, b = t - tb * B;
