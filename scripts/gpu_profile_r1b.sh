@@ -1,10 +1,13 @@
 # Round-1 (second session) measurement pass, run on the GPU box from the repo root: bench lines of
 # the default and other configs, the ncu launch list of the bench command, ncu --set full of the
 # step's GEMV launches, microbenchmarks, steady-state GEMV rates, phase traces, quantizer timing.
-# Everything lands in gpurun_out/r1b/; scripts/summarize_r1b.py copies the summaries to profiles/.
+# Everything lands in gpurun_out/<tag>/ (bash scripts/gpu_profile_r1b.sh <tag>, default r1b);
+# python scripts/summarize_r1b.py <tag> copies the summaries to profiles/<tag>_*.
 set -x
-O=gpurun_out/r1b
+O=gpurun_out/${1:-r1b}
 mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1
 timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
 for B in 1 2 4 8 16; do timeout 400 python bench.py --no-cpu-baseline --code hyb --k 4 --batch $B --steps 10 > $O/c3_hyb4_b$B.json 2> $O/c3_hyb4_b$B.err; done

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Copy the round-1b measurement pass (scripts/gpu_profile_r1b.sh, gpurun_out/r1b/) into profiles/:
+"""Copy a measurement pass (scripts/gpu_profile_r1b.sh [tag], gpurun_out/<tag>/, default r1b) into profiles/:
 bench lines, text outputs of the microbenchmarks / rates / traces, ncu summaries (JSON) of the
 GEMV launches, the decode-loop microbenchmark and the persistent GEMV, the launch-list share table
 and profiles/traffic.json (read by bench.py as roofline.traffic)."""
@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "gpurun_out", "r1b")
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r1b"                 # measurement pass label
+SRC = os.path.join(ROOT, "gpurun_out", TAG)
 DST = os.path.join(ROOT, "profiles")
 
 
@@ -96,13 +97,13 @@ def launch_share(path):
 
 def main():
     os.makedirs(DST, exist_ok=True)
-    copies = {"bench.json": "r1b_bench.json", "bench_reference.json": "r1b_bench_reference.json",
-              "c2_1mad.json": "r1b_c2_1mad.json", "c4_70b_1gpu.json": "r1b_c4_70b_1gpu.json",
-              "c5_70b_hyb3_1gpu.json": "r1b_c5_70b_hyb3_1gpu.json", "pipe_mix.txt": "r1b_pipe_mix.txt",
-              "decode_microbench.txt": "r1b_decode_microbench.txt", "gridbar.txt": "r1b_gridbar.txt",
-              "gemv_rate.txt": "r1b_gemv_rate.txt", "trace_fused_impl5.txt": "r1b_trace_fused_impl5.txt",
-              "trace_fused_impl6.txt": "r1b_trace_fused_impl6.txt", "viterbi.txt": "r1b_viterbi.txt",
-              "gpu.txt": "r1b_gpu.txt"}
+    copies = {"bench.json": f"{TAG}_bench.json", "bench_reference.json": f"{TAG}_bench_reference.json",
+              "c2_1mad.json": f"{TAG}_c2_1mad.json", "c4_70b_1gpu.json": f"{TAG}_c4_70b_1gpu.json",
+              "c5_70b_hyb3_1gpu.json": f"{TAG}_c5_70b_hyb3_1gpu.json", "pipe_mix.txt": f"{TAG}_pipe_mix.txt",
+              "decode_microbench.txt": f"{TAG}_decode_microbench.txt", "gridbar.txt": f"{TAG}_gridbar.txt",
+              "gemv_rate.txt": f"{TAG}_gemv_rate.txt", "trace_fused_impl5.txt": f"{TAG}_trace_fused_impl5.txt",
+              "trace_fused_impl6.txt": f"{TAG}_trace_fused_impl6.txt", "viterbi.txt": f"{TAG}_viterbi.txt",
+              "gpu.txt": f"{TAG}_gpu.txt", "pytest_gpu.txt": f"{TAG}_pytest_gpu.txt", "smoke.txt": f"{TAG}_smoke.txt"}
     for a, b in copies.items():
         p = os.path.join(SRC, a)
         if os.path.exists(p):
@@ -116,21 +117,21 @@ def main():
             if ln:
                 c3.append(json.loads(ln[-1]))
     if c3:
-        with open(os.path.join(DST, "r1b_c3_hyb4_batch_sweep.json"), "w") as f:
+        with open(os.path.join(DST, f"{TAG}_c3_hyb4_batch_sweep.json"), "w") as f:
             json.dump(c3, f, indent=1)
-    for rep, out in (("prof_gemv", "r1b_ncu_gemv.json"), ("prof_decode_loop", "r1b_ncu_decode_loop.json"),
-                     ("prof_gemv6", "r1b_ncu_gemv6.json")):
+    for rep, out in (("prof_gemv", f"{TAG}_ncu_gemv.json"), ("prof_decode_loop", f"{TAG}_ncu_decode_loop.json"),
+                     ("prof_gemv6", f"{TAG}_ncu_gemv6.json")):
         p = os.path.join(SRC, rep + ".ncu-rep")
         if os.path.exists(p):
             with open(os.path.join(DST, out), "w") as f:
                 json.dump(ncu_summary(p), f, indent=1)
     lp = os.path.join(SRC, "launches.csv")
     if os.path.exists(lp):
-        shutil.copy(lp, os.path.join(DST, "r1b_launches.csv"))
-        with open(os.path.join(DST, "r1b_launches_summary.txt"), "w") as f:
+        shutil.copy(lp, os.path.join(DST, f"{TAG}_launches.csv"))
+        with open(os.path.join(DST, f"{TAG}_launches_summary.txt"), "w") as f:
             f.write(launch_share(lp) + "\n")
     # traffic.json for bench.py: mean DRAM bytes per GEMV launch of the 7B step
-    gp = os.path.join(DST, "r1b_ncu_gemv.json")
+    gp = os.path.join(DST, f"{TAG}_ncu_gemv.json")
     if os.path.exists(gp):
         with open(gp) as f:
             g = json.load(f)
@@ -144,7 +145,7 @@ def main():
             tp = os.path.join(DST, "traffic.json")
             t = json.load(open(tp)) if os.path.exists(tp) else {}
             t["llama2-7b/3inst/k2"] = {"dram_bytes_per_launch": tot_b / tot_n, "launches": tot_n, "kernels": names,
-                                      "report": "gpurun_out/r1b/prof_gemv.ncu-rep (profiles/r1b_ncu_gemv.json)"}
+                                      "report": f"gpurun_out/{TAG}/prof_gemv.ncu-rep (profiles/{TAG}_ncu_gemv.json)"}
             with open(tp, "w") as f:
                 json.dump(t, f, indent=1)
     print("ok")
