@@ -155,9 +155,14 @@ __device__ __forceinline__ float thread_row_sum(const float* p, int st, int nu) 
     for (int l = 0; l < 32; ++l) s[l] = 0.0f;
 #pragma unroll 1
     for (int u0 = 0; u0 < nu; u0 += 32) {
+        // all loads first (clamped in range, branch-free): one latency per chunk, not 32
+        const float* q = p + u0 * st;
+        const int last = nu - 1 - u0;
+        float v[32];
 #pragma unroll
-        for (int l = 0; l < 32; ++l)
-            if (u0 + l < nu) s[l] += p[(u0 + l) * st];
+        for (int l = 0; l < 32; ++l) v[l] = q[(l < last ? l : last) * st];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) s[l] = l <= last ? s[l] + v[l] : s[l];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1)
