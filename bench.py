@@ -61,12 +61,13 @@ def peaks():
 
 
 def traffic(workload, code, k, impl):
-    """DRAM bytes (read + write) per GEMV launch from the committed `ncu --set full` capture
-    (profiles/traffic.json, written by scripts/ncu_traffic.py), or None if not captured."""
+    """DRAM bytes (read + write) per layer of the step's GEMV launches from the committed
+    `ncu --set full` capture of one block (profiles/traffic.json, written by
+    scripts/summarize_r1b.py), or None if not captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             d = json.load(f)
-        return d[f"{workload}/{code}/k{k}"]["dram_bytes_per_launch"]
+        return d[f"{workload}/{code}/k{k}"]["dram_bytes_per_layer"]
     except Exception:
         return None
 
@@ -178,7 +179,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2406_11235_b200 import qtip
-    from paper_2406_11235_b200.layer import QTIPLinear
+    from paper_2406_11235_b200.layer import QTIPLinear, forward_group
     from paper_2406_11235_b200.sharded import ShardedQTIPLinear
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -249,7 +250,33 @@ def run_ours(args):
         nl = len(shapes)
         for blk in range(nblocks):
             for grp in groups:
-                if serial or len(grp) == 1:
+                if not serial and len(grp) > 1 and args.grouping == "launch" and world == 1:
+                    # same-shape layers on one input: one grouped call (qtip_matvec_group) per shape;
+                    # differently shaped members (70B: q vs k, v) run concurrently on side streams
+                    by_shape = {}
+                    for i in grp:
+                        by_shape.setdefault(shapes[i], []).append(blk * nl + i)
+                    parts = list(by_shape.values())
+
+                    def run_part(idx):
+                        if len(idx) == 1:
+                            run_layer(idx[0])
+                        else:
+                            forward_group([layers[i] for i in idx], xs[layers[idx[0]].n], outs=[outs[i] for i in idx])
+                    if len(parts) == 1:
+                        run_part(parts[0])
+                        continue
+                    cur = torch.cuda.current_stream()
+                    for si in range(len(parts) - 1):
+                        side[si].wait_stream(cur)
+                    run_part(parts[0])
+                    for si, idx in enumerate(parts[1:]):
+                        with torch.cuda.stream(side[si]):
+                            run_part(idx)
+                    for si in range(len(parts) - 1):
+                        cur.wait_stream(side[si])
+                    continue
+                if serial or len(grp) == 1 or args.grouping == "serial":
                     for i in grp:
                         run_layer(blk * nl + i)
                     continue
@@ -353,13 +380,30 @@ def run_ours(args):
     #      RHT-out off; PDL on), timed with CUDA events around the replays
     locs = [(lay if world == 1 else lay.local) for lay in layers]
     gouts = [torch.empty((B, t.m), dtype=torch.float32, device=dev) for t in locs]
+    gflags = qtip.QTIP_RHT_IN | qtip.QTIP_XT_READY
+
+    def gemv_launches():
+        # the step's decode-GEMV launches in step order (grouped layers as one grouped launch)
+        nl = len(shapes)
+        for blk in range(nblocks):
+            for grp in groups:
+                parts = {}
+                for i in grp:
+                    parts.setdefault(shapes[i], []).append(blk * nl + i)
+                for idx in parts.values():
+                    if len(idx) > 1 and args.grouping == "launch" and world == 1:
+                        forward_group([locs[i] for i in idx], xs[locs[idx[0]].n], outs=[gouts[i] for i in idx],
+                                      flags=gflags)
+                    else:
+                        for i in idx:
+                            locs[i].forward(xs[locs[i].n], out=gouts[i], flags=gflags)
+
     gk = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
-        for t, o in zip(locs, gouts):                           # eager pass (workspaces exist)
-            t.forward(xs[t.n], out=o, flags=qtip.QTIP_RHT_IN | qtip.QTIP_XT_READY)
+        step()                                                  # x~ of every layer in its workspace
+        gemv_launches()                                         # eager pass
         with torch.cuda.graph(gk, stream=s):
-            for t, o in zip(locs, gouts):
-                t.forward(xs[t.n], out=o, flags=qtip.QTIP_RHT_IN | qtip.QTIP_XT_READY)
+            gemv_launches()
     torch.cuda.current_stream().wait_stream(s)
     for _ in range(3):
         gk.replay()
@@ -421,7 +465,8 @@ def run_ours(args):
                        "code": code, "k": k, "L": 16, "V": 2 if code == "hyb" else 1, "T": 256, "batch": B,
                        "stream_bytes_per_step": step_bytes, "tokens_per_s_equiv": round(B * 1e3 / ms, 2),
                        "per_layer": per_layer, "parallelism": f"rows{world}" if world > 1 else "single",
-                       "dependency": "block: q|k|v and gate|up concurrent, groups sequential",
+                       "dependency": "block: q,k,v and gate,up share an input (one grouped launch per shape, or concurrent streams), groups sequential",
+                       "grouping": args.grouping,
                        "step_serial_ms": round(ms_serial, 5),
                        "serial_GBps": round(step_bytes / (ms_serial * 1e-3) / 1e9, 2),
                        "l2": "inputs > L2: 1.62 GB of distinct packed weights per step (126 MB L2)"
@@ -430,9 +475,9 @@ def run_ours(args):
                        "arith": "decoded weights and RHT'd x in binary16, fp32 accumulation"},
             "roofline": {"bound": "hbm", "achieved": round(gemv_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gemv_gbs / peak, 4), "traffic": traffic(args.workload, code, k, qtip.get_matvec_impl()),
-                         "kernel": "fused decode-GEMV (+ split-K reduce where used), back-to-back graph",
+                         "kernel": "fused decode-GEMV launches of the step (grouped where the step groups), back-to-back graph",
                          "peak_kind": peak_kind,
-                         "avg_launch_us": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3),
+                         "us_per_layer": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3),
                          # context: the measured decode-MMA loop ceiling of 3INST k=2
                          # (scripts/decode_microbench.cu, 19.2 weights/clk/SM), the practical bound
                          # below HBM for this code
@@ -463,6 +508,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=None)
     ap.add_argument("--matvec-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grouping", default="launch", choices=["streams", "launch", "serial"],
+                    help="layers of a block that share an input: concurrent streams, one grouped launch, or serial")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -122,6 +122,24 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B,
 
 size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B);
 
+/* G (1..4) layers of the SAME shape (m, n) and parameters applied to the SAME input x, e.g. the
+ * q, k, v projections or gate, up of a transformer block (QTIP quantizes q, k, v, o, up,
+ * gate, down as 7 separate matrices, each with its own RHT signs):
+ *     d_y[g] = qtip_matvec(p, m, n, B, d_packed[g], d_lut[g], d_sign_n[g], d_sign_m[g], scale[g],
+ *                          d_x, d_y[g], 0, m, flags, d_workspace[g], ...)
+ *   Arrays of G HOST pointers to DEVICE buffers (d_packed, d_lut (NULL array unless HYB),
+ *   d_sign_n, d_sign_m, d_y, d_workspace); scale: HOST float[G]; each workspace >= qtip_matvec_workspace_bytes(p, m, n, B)
+ *   (workspace_bytes is the size of each), 256-B aligned.  Full row range only.
+ *   When the persistent kernel fits (B <= 4, every layer keeps >= 1 tile row per CTA) the G
+ *   layers run as ONE grouped RHT-in launch, ONE persistent decode-GEMV launch (the SMs split
+ *   between the layers) and ONE grouped RHT-out launch; otherwise G qtip_matvec calls.  Results
+ *   equal G qtip_matvec calls with qtip_set_matvec_impl(6) bit for bit (canonical row sums, R18).
+ *   Errors as qtip_matvec, plus QTIP_ERR_INVALID_PARAMS for G outside 1..4 or NULL arrays. */
+qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B,
+                              const void* const* d_packed, const uint16_t* const* d_lut, const uint8_t* const* d_sign_n,
+                              const uint8_t* const* d_sign_m, const float* scale, const float* d_x, float* const* d_y,
+                              int flags, void* const* d_workspace, size_t workspace_bytes, void* stream);
+
 /* Random Hadamard transform of B vectors of length n:
  *   inverse = 0:  out = H_n (S . in) / sqrt(n)
  *   inverse = 1:  out = S . (H_n^T in) / sqrt(n)

@@ -209,6 +209,98 @@ static void record_event(cudaEvent_t ev, cudaStream_t s) {
         cudaEventRecord(ev, s);
 }
 
+qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B,
+                              const void* const* d_packed, const uint16_t* const* d_lut, const uint8_t* const* d_sign_n,
+                              const uint8_t* const* d_sign_m, const float* scale, const float* d_x, float* const* d_y,
+                              int flags, void* const* d_workspace, size_t workspace_bytes, void* stream) {
+    if (G < 1 || G > kMaxGroup) return fail(QTIP_ERR_INVALID_PARAMS, "group size must be in 1..4");
+    if (!d_packed || !d_y || !d_workspace || !scale || !d_sign_n || !d_sign_m)
+        return fail(QTIP_ERR_INVALID_PARAMS, "NULL pointer array");
+    // every member's arguments are validated by the per-layer entry point's rules
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if ((st = check_shape(m, n)) != QTIP_OK) return st;
+    if (B < 1 || B > 64) return fail(QTIP_ERR_INVALID_PARAMS, "batch must be in 1..64");
+    if (flags & ~(QTIP_RHT_IN | QTIP_RHT_OUT | QTIP_XT_READY)) return fail(QTIP_ERR_INVALID_PARAMS, "unknown flags");
+    const size_t need = qtip_matvec_workspace_bytes(p, m, n, B);
+    for (int g = 0; g < G; ++g) {
+        if (!d_packed[g] || !d_y[g] || !d_workspace[g] || !d_x || (p->code == QTIP_CODE_HYB && (!d_lut || !d_lut[g])))
+            return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+        if (((flags & QTIP_RHT_IN) && !(flags & QTIP_XT_READY) && !d_sign_n[g]) || ((flags & QTIP_RHT_OUT) && !d_sign_m[g]))
+            return fail(QTIP_ERR_INVALID_PARAMS, "NULL sign vector");
+        if (!aligned16(d_packed[g]) || (reinterpret_cast<uintptr_t>(d_workspace[g]) & 255u))
+            return fail(QTIP_ERR_ALIGNMENT, "d_packed 16-B and d_workspace 256-B aligned");
+        if (workspace_bytes < need) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
+    }
+    const Layout l = make_layout(m, n, p->k);
+    const CodeArgs ca = code_args(p);
+    const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
+    const bool xready = (flags & QTIP_XT_READY) != 0;
+    const int64_t tile_rows = (m + kTile - 1) / kTile;
+    const bool grouped = G > 1 && (g_impl == 0 || g_impl == 6) &&
+                         layer_supported(l, p->code, ca, B, tile_rows, false, false) &&
+                         tile_rows >= (num_sms() + G - 1) / G;
+    if (!grouped) {                                              // one layer at a time (same results)
+        for (int g = 0; g < G; ++g) {
+            st = qtip_matvec(p, m, n, B, d_packed[g], d_lut ? d_lut[g] : nullptr, d_sign_n[g], d_sign_m[g], scale[g], d_x, d_y[g], 0, m,
+                             flags, d_workspace[g], workspace_bytes, stream);
+            if (st != QTIP_OK) return st;
+        }
+        return QTIP_OK;
+    }
+    RhtPlan pn{}, pm{};
+    if (rin && !xready && make_rht_plan(n, &pn) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
+    if (rout && make_rht_plan(m, &pm) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);
+    const int xmode = gemv_mma_xt_mode(p->code);
+    const int xmode6 = p->code == QTIP_CODE_HYB ? 5 : xmode;        // HYB fast path: swapped pairs
+    const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
+    void* xt[kMaxGroup];
+    float* yt[kMaxGroup];
+    float* lws[kMaxGroup];
+    unsigned* bar[kMaxGroup];
+    float* ydst[kMaxGroup];
+    float sc[kMaxGroup];
+    const float* xin[kMaxGroup];
+    for (int g = 0; g < G; ++g) {                                 // the impl 6 workspace layout
+        char* ws = (char*)d_workspace[g];
+        xt[g] = ws;
+        yt[g] = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
+        lws[g] = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad) +
+                          align256(4 * (l.m_pad / kCellRows + 2)));
+        bar[g] = (unsigned*)((char*)lws[g] + align256(4 * layer_workspace_floats(l, B, 0)));
+        ydst[g] = rout ? yt[g] : d_y[g];
+        sc[g] = rout ? 1.0f : scale[g];
+        xin[g] = d_x;
+    }
+    cudaError_t e = cudaSuccess;
+    if (!xready) {
+        if (rin) {
+            e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, l.n_pad, 0, std::vector<float>(G, 1.0f).data(), s,
+                                 xmode6, l.n_pad);
+        } else {
+            for (int g = 0; g < G && e == cudaSuccess; ++g) e = launch_convert(d_x, n, n, B, xt[g], l.n_pad, xmode6, l.n_pad, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group rht_in");
+    }
+    const uint16_t* luts[kMaxGroup];
+    for (int g = 0; g < G; ++g) luts[g] = d_lut ? d_lut[g] : nullptr;
+    e = launch_layer_group(l, p->code, ca, G, d_packed, luts, sc, ydst, B, (uint32_t* const*)xt, row_words, lws, bar, s);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group gemv");
+    if (rout) {
+        const float* yin[kMaxGroup];
+        void* yout[kMaxGroup];
+        for (int g = 0; g < G; ++g) {
+            yin[g] = yt[g];
+            yout[g] = d_y[g];
+        }
+        e = launch_rht_group(pm, G, B, d_sign_m, yin, m, yout, m, 1, scale, s);
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group rht_out");
+    }
+    return QTIP_OK;
+}
+
 size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B) {
     if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1) return 0;
     const Layout l = make_layout(m, n, p->k);

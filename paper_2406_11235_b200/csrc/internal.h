@@ -42,6 +42,9 @@ const uint32_t* hadamard_table_device(int b, bool transpose, cudaError_t* err);
 cudaError_t launch_decode(const Layout& lay, int code, int V, const CodeArgs& ca, const void* packed,
                           const uint16_t* lut, int out_f32, void* out, cudaStream_t s);
 
+// Largest number of same-shape layers one grouped launch serves (q, k, v / gate, up).
+constexpr int kMaxGroup = 4;
+
 struct RhtPlan {
     int64_t n;
     int b, a;          // n = b * 2^a
@@ -61,6 +64,10 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan);
 cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
                        void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode = 0,
                        int64_t pad_to = 0, int* zero_ptr = nullptr, int zero_n = 0);
+// G transforms of the same plan in one launch (grid.z = g): sign[g], in[g], out[g], scale[g].
+cudaError_t launch_rht_group(const RhtPlan& plan, int G, int64_t B, const uint8_t* const* sign, const float* const* in,
+                             int64_t in_stride, void* const* out, int64_t out_stride, int inverse, const float* scale,
+                             cudaStream_t s, int out_mode = 0, int64_t pad_to = 0);
 // x (float32) -> out_mode encoding, zero padded to pad_to (used when RHT-in is off).
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
                            int out_mode, int64_t pad_to, cudaStream_t s, int* zero_ptr = nullptr, int zero_n = 0);
@@ -117,6 +124,13 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
                          const float* x, const uint8_t* sign_n, const uint8_t* sign_m, float scale, float* y,
                          int64_t B, int64_t row_begin, int64_t row_end, bool rht_in, bool rht_out, bool xt_ready,
                          uint32_t* xt_g, int64_t row_words, float* ws_f, unsigned* bar, cudaStream_t s);
+// G same-shape layers in one persistent launch (x~ already in each layer's workspace, no RHT
+// phases): CTAs [g P / G, (g+1) P / G) run layer g in rows mode.  cudaErrorInvalidConfiguration
+// when a layer has fewer tile rows than its CTAs or the shared memory does not fit.
+cudaError_t launch_layer_group(const Layout& lay, int code, const CodeArgs& ca, int G, const void* const* packed,
+                               const uint16_t* const* lut, const float* scale, float* const* y, int64_t B,
+                               uint32_t* const* xt_g, int64_t row_words, float* const* ws_f, unsigned* const* bar,
+                               cudaStream_t s);
 
 // Tail-biting trellis quantizer (k_viterbi.cu): Algorithm 4 per sequence of T source values (in
 // code units), binary32 DP.  ws: viterbi_workspace_bytes(T) bytes (backpointers, per CTA).

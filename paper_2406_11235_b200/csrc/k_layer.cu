@@ -73,6 +73,17 @@ struct LayerArgs {
     uint32_t off_ring, off_x, off_v, off_red, off_out, off_outred, off_scr, off_lut;
     int finishers;                           // rows mode: CTAs (last arrivals) that run the RHT-out
     int debug;                               // knob 2: bit 0 = run the fast x~ phase twice (cold/warm probe)
+    // grouped launch (G > 1): G layers of identical shape, CTAs [gcta0[g], gcta0[g+1]) run layer g
+    // (rows mode, x~ ready, no RHT phases); the per-layer pointers replace the fields above
+    int G;
+    int gcta0[kMaxGroup + 1];
+    const uint32_t* gpacked[kMaxGroup];
+    uint32_t* gxt[kMaxGroup];
+    float* gy[kMaxGroup];
+    float gscale[kMaxGroup];
+    float* ggpart[kMaxGroup];
+    unsigned* gbar[kMaxGroup];
+    const uint32_t* glut[kMaxGroup];
 };
 
 __device__ unsigned long long* g_layer_trace = nullptr;
@@ -107,7 +118,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 // with relaxed loads and fence once.  The counter is 0 between barriers (zero-initialised
 // workspace); a 4 s watchdog traps instead of hanging if a CTA is missing.
 // Measured variants: scripts/gridbar_microbench.cu.
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned P) {
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned* cnt = bar;
@@ -115,7 +126,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
         unsigned g, old;
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-        if (old == gridDim.x - 1) {
+        if (old == P - 1) {
             asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(cnt) : "memory");
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
         } else {
@@ -338,7 +349,18 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tig = lane & 3;
     const int B = args.B, S = args.stages;
-    const int64_t P = gridDim.x, c = blockIdx.x;
+    int grp = 0;                                                    // layer of a grouped launch
+    while (grp + 1 < args.G && (int)blockIdx.x >= args.gcta0[grp + 1]) ++grp;
+    const bool grouped = args.G > 1;
+    const int64_t P = grouped ? args.gcta0[grp + 1] - args.gcta0[grp] : (int64_t)gridDim.x;
+    const int64_t c = grouped ? (int64_t)blockIdx.x - args.gcta0[grp] : (int64_t)blockIdx.x;
+    const uint32_t* const a_packed = grouped ? args.gpacked[grp] : args.packed;
+    uint32_t* const a_xt = grouped ? args.gxt[grp] : args.xt_g;
+    float* const a_y = grouped ? args.gy[grp] : args.y;
+    const float a_scale = grouped ? args.gscale[grp] : args.scale;
+    float* const a_gpart = grouped ? args.ggpart[grp] : args.gpart;
+    unsigned* const a_bar = grouped ? args.gbar[grp] : args.bar;
+    const uint32_t* const a_lut = grouped ? args.glut[grp] : args.lut;
     const int64_t n = args.lay.n, m = args.lay.m, n_kc = args.lay.n_kc, m_pad = args.lay.m_pad;
     const int n_units = args.n_units, U = args.U, CP = args.CP;
     const int64_t T = args.T;
@@ -388,7 +410,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         const int I = (int)args.tile_row0 + it.Ir;
         const uint32_t bar = ptx::smem_u32(full + st);
         const uint8_t* src = reinterpret_cast<const uint8_t*>(
-            args.packed + ((int64_t)(I >> 3) * n_kc + it.u) * (512 * K) + (I & 7) * (64 * K));
+            a_packed + ((int64_t)(I >> 3) * n_kc + it.u) * (512 * K) + (I & 7) * (64 * K));
         const uint32_t dst = ptx::smem_u32(ring + (size_t)st * chunk_bytes);
 #pragma unroll
         for (int q = 0; q < (16 * K + 31) / 32; ++q) {               // 16 K pieces of 16 B
@@ -417,7 +439,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     if constexpr (kHybFast) {                                       // 32-way replicated LUT, words (c0 << 16) | c1
         uint32_t* lsm = reinterpret_cast<uint32_t*>(smem + args.off_lut);
         for (int i = threadIdx.x; i < (512 << 5); i += kLThreads) {
-            const uint32_t v = __ldg(args.lut + (i >> 5));
+            const uint32_t v = __ldg(a_lut + (i >> 5));
             lsm[i] = (v << 16) | (v >> 16);
         }
     }
@@ -436,19 +458,19 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             cta_fwht(vb, B * len, args.na);
             const float rs = rsqrtf((float)n);
             const int64_t F = (int64_t)B * len;
-            uint32_t* xg = args.xt_g;
+            uint32_t* xg = a_xt;
             dense_mix(vb, len, args.nb, args.na, args.hb_n, (int)(c * F / P), (int)((c + 1) * F / P), red,
                       [=](int f, float s) { put_xt<kHyb, kHybFast>(xg, rw, f / len, f % len, s * rs); });
             if (c == 0) {                                           // zero padding columns [n, n_pad)
                 const int pad = (int)(n_pad - n);
                 for (int i = threadIdx.x; i < B * pad; i += kLThreads)
-                    put_xt<kHyb, kHybFast>(args.xt_g, rw, i / pad, n + i % pad, 0.0f);
+                    put_xt<kHyb, kHybFast>(a_xt, rw, i / pad, n + i % pad, 0.0f);
             }
-            grid_sync(args.bar);
+            grid_sync(a_bar, (unsigned)P);
         }
         const int words = (int)(B * rw);
         for (int i = threadIdx.x; i < words / 4; i += kLThreads)
-            reinterpret_cast<uint4*>(xs)[i] = __ldcg(reinterpret_cast<const uint4*>(args.xt_g) + i);
+            reinterpret_cast<uint4*>(xs)[i] = __ldcg(reinterpret_cast<const uint4*>(a_xt) + i);
     } else {
         const int len = (int)n, np = (int)n_pad;
         const int Ef = args.rht_in ? fwht_fast_E(n, args.na, kLThreads) : 0;
@@ -489,7 +511,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
 #pragma unroll
                         for (int q = 0; q < 16; ++q) o[q] *= rs;
                         put_tile<kHyb, kHybFast>(xs + bt * rw + tile * wpt, o);
-                        if (c == 0 && args.xt_g) put_tile<kHyb, kHybFast>(args.xt_g + bt * rw + tile * wpt, o);
+                        if (c == 0 && a_xt) put_tile<kHyb, kHybFast>(a_xt + bt * rw + tile * wpt, o);
                     }
                     __syncthreads();                                // scr reused by the next batch row
                 };
@@ -528,7 +550,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
                     put_xt<kHyb, kHybFast>(xs, rw, bt, e0 + q, v[q]);
-                    if (c == 0 && args.xt_g) put_xt<kHyb, kHybFast>(args.xt_g, rw, bt, e0 + q, v[q]);   // QTIP_XT_READY reuse
+                    if (c == 0 && a_xt) put_xt<kHyb, kHybFast>(a_xt, rw, bt, e0 + q, v[q]);   // QTIP_XT_READY reuse
                 }
             }
             __syncthreads();
@@ -551,7 +573,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     const bool bval = g < B;
     const uint32_t* xsl = bval ? xs + g * rw + (kHyb ? 2 : 4) * tig : zero_b + (kHyb ? 2 : 4) * tig;
     const int ustride = bval ? (kHyb ? 64 : 128) : 0;
-    const uint32_t* lut = args.lut;
+    const uint32_t* lut = a_lut;
     const uint32_t lut_lane = ptx::smem_u32(smem + args.off_lut) + 4u * lane;
     const mma::HybFastLane hl = mma::hyb_fast_lane(g, tig);
     const mma::HybFastLaneK<K> hlk = mma::hyb_fast_lane_k<K>(g, tig);
@@ -569,7 +591,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     auto run = [&](auto kPartSmem, auto kTwoSign) {
         constexpr bool kSmemPart = decltype(kPartSmem)::value;
         constexpr bool kTwo = decltype(kTwoSign)::value;
-        float* const gpart = args.gpart;
+        float* const gpart = a_gpart;
         const int64_t row0 = args.tile_row0 * kTile;
         int st = 0;
         uint32_t phase = 0;
@@ -651,7 +673,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     auto finish = [&](int b, int64_t i, float s) {                    // s = the row's canonical sum
         s *= args.code_factor;
         if (rht_out) args.ybuf[b * m_pad + i] = s;
-        else if (i >= args.row_lo && i < args.row_hi) args.y[b * args.y_stride + (i - args.row_lo)] = args.scale * s;
+        else if (i >= args.row_lo && i < args.row_hi) a_y[b * args.y_stride + (i - args.row_lo)] = a_scale * s;
     };
     int Ia = 0, nrow_items = 0;
     if (L1 > L0) {
@@ -680,14 +702,14 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         if (u0 >= L0i && u0 + n_units <= L1i) {                       // every unit in this CTA
             const float s = args.part_smem
                 ? warp_row_sum<false>(part + ((u0 - L0i) * kTile + r) * B + b, kTile * B, n_units)
-                : warp_row_sum<true>(args.gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
+                : warp_row_sum<true>(a_gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
             if (t == 0) trace_mark(tr && rows_mode && !rht_out, 7);       // debug: first row's sum
             if (lane == 0) finish(b, i, s);
             if (t == 0) trace_mark(tr && rows_mode && !rht_out, 8);
         } else if (args.part_smem) {                                  // shared row: publish this CTA's units
             const int s_lo = L0i - u0 > 0 ? L0i - u0 : 0, s_hi = L1i - u0 < n_units ? L1i - u0 : n_units;
             for (int u = s_lo + lane; u < s_hi; u += 32)
-                args.gpart[((int64_t)b * m_pad + i) * n_units + u] = part[((u0 + u - L0i) * kTile + r) * B + b];
+                a_gpart[((int64_t)b * m_pad + i) * n_units + u] = part[((u0 + u - L0i) * kTile + r) * B + b];
         }
     }
     trace_mark(tr, 6);
@@ -701,7 +723,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             const int G = args.finishers;
             __syncthreads();
             if (threadIdx.x == 0) {
-                unsigned long long* cnt = reinterpret_cast<unsigned long long*>(args.bar + 64);
+                unsigned long long* cnt = reinterpret_cast<unsigned long long*>(a_bar + 64);
                 unsigned long long old;
                 __threadfence();
                 asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(cnt) : "memory");
@@ -725,7 +747,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             if (tk >= P - G) rht_out_phase(args, smem, tk - (P - G), G, tr);
         }
     } else {
-        grid_sync(args.bar);
+        grid_sync(a_bar, (unsigned)P);
         trace_mark(tr, 7);
         // shared rows: finished by the owner of their last unit
         for (int t = warp; t < nrow_items; t += kLWarps) {
@@ -734,11 +756,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             const int u0 = Ir * n_units;
             if ((u0 >= L0i && u0 + n_units <= L1i) || owner(u0 + n_units - 1) != c) continue;
             const int i = (tile_row0 + Ir) * kTile + r;
-            const float s = warp_row_sum<true>(args.gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
+            const float s = warp_row_sum<true>(a_gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units);
             if (lane == 0) finish(b, i, s);
         }
         if (rht_out) {
-            grid_sync(args.bar);
+            grid_sync(a_bar, (unsigned)P);
             trace_mark(tr, 8);
             rht_out_phase(args, smem, c, P, tr);
         }
@@ -869,8 +891,8 @@ struct LayerPlan {
 };
 
 bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool coop, bool rht_out, int mb,
-                LayerPlan* pl) {
-    const int P = num_sms();
+                LayerPlan* pl, int P_cta = 0) {
+    const int P = P_cta > 0 ? P_cta : num_sms();                     // CTAs sharing the layer's tile rows
     const bool hyb = code == QTIP_CODE_HYB;
     const int n_pairs = (int)(lay.n_kc * 4);
     // unit = one cell's tile row (4 tile pairs, 128 columns) for every shape: the association of
@@ -1030,6 +1052,87 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
     const bool imm = code != QTIP_CODE_HYB && ca.a == (code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&
                      ca.b == (code == QTIP_CODE_1MAD ? 76625530u : 64248484u);
     e = cudaErrorInvalidValue;
+#define QTIP_LAYER_CASE(KK, CC)                                                           \
+    if (lay.k == KK && code == CC) e = imm ? launch_layer_t<KK, CC, true>(a, pl.smem, s) \
+                                           : launch_layer_t<KK, CC, false>(a, pl.smem, s);
+    QTIP_LAYER_CASE(2, QTIP_CODE_3INST)
+    QTIP_LAYER_CASE(3, QTIP_CODE_3INST)
+    QTIP_LAYER_CASE(4, QTIP_CODE_3INST)
+    QTIP_LAYER_CASE(2, QTIP_CODE_1MAD)
+    QTIP_LAYER_CASE(3, QTIP_CODE_1MAD)
+    QTIP_LAYER_CASE(4, QTIP_CODE_1MAD)
+    QTIP_LAYER_CASE(2, QTIP_CODE_HYB)
+    QTIP_LAYER_CASE(3, QTIP_CODE_HYB)
+    QTIP_LAYER_CASE(4, QTIP_CODE_HYB)
+#undef QTIP_LAYER_CASE
+    count_launch(1);
+    return e;
+}
+
+cudaError_t launch_layer_group(const Layout& lay, int code, const CodeArgs& ca, int G, const void* const* packed,
+                               const uint16_t* const* lut, const float* scale, float* const* y, int64_t B,
+                               uint32_t* const* xt_g, int64_t row_words, float* const* ws_f, unsigned* const* bar,
+                               cudaStream_t s) {
+    if (G < 2 || G > kMaxGroup) return cudaErrorInvalidValue;
+    const int P = num_sms();
+    const int64_t tile_rows = (lay.m + kTile - 1) / kTile;
+    const int Pmin = P / G;
+    if (tile_rows < (P + G - 1) / G) return cudaErrorInvalidConfiguration;   // rows mode for every layer
+    LayerArgs a{};
+    a.packed = (const uint32_t*)packed[0];
+    a.lay = lay;
+    a.ca = ca;
+    a.lut = (const uint32_t*)lut[0];
+    a.scale = scale[0];
+    a.code_factor = (code == QTIP_CODE_1MAD) ? 5.0f / 739.0f : 1.0f;
+    a.y = y[0];
+    a.row_lo = 0;
+    a.row_hi = lay.m;
+    a.y_stride = lay.m;
+    a.B = (int)B;
+    a.rht_in = a.rht_out = 0;
+    a.xt_ready = 1;
+    a.nb = a.mb = 1;
+    a.coop = 0;
+    a.xt_g = xt_g[0];
+    a.row_words = row_words;
+    a.ybuf = ws_f[0];
+    a.gpart = ws_f[0] + B * lay.m_pad;
+    a.bar = bar[0];
+    a.tile_row0 = 0;
+    LayerPlan pl;
+    if (!plan_layer(lay, code, B, tile_rows, false, false, 1, &pl, Pmin)) return cudaErrorInvalidConfiguration;
+    a.T = pl.T;
+    a.n_units = pl.n_units;
+    a.U = pl.U;
+    a.CP = pl.CP;
+    a.stages = pl.S;
+    a.max_units_cta = pl.max_units;
+    a.part_smem = pl.part_smem;
+    a.off_ring = pl.off_ring;
+    a.off_x = pl.off_x;
+    a.off_v = pl.off_v;
+    a.off_red = pl.off_red;
+    a.off_out = pl.off_out;
+    a.off_outred = pl.off_outred;
+    a.off_scr = pl.off_scr;
+    a.off_lut = pl.off_lut;
+    a.debug = g_layer_debug;
+    a.finishers = 1;
+    a.G = G;
+    for (int g = 0; g <= G; ++g) a.gcta0[g] = (int)((int64_t)g * P / G);
+    for (int g = 0; g < G; ++g) {
+        a.gpacked[g] = (const uint32_t*)packed[g];
+        a.gxt[g] = xt_g[g];
+        a.gy[g] = y[g];
+        a.gscale[g] = scale[g];
+        a.ggpart[g] = ws_f[g] + B * lay.m_pad;
+        a.gbar[g] = bar[g];
+        a.glut[g] = (const uint32_t*)lut[g];
+    }
+    const bool imm = code != QTIP_CODE_HYB && ca.a == (code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&
+                     ca.b == (code == QTIP_CODE_1MAD ? 76625530u : 64248484u);
+    cudaError_t e = cudaErrorInvalidValue;
 #define QTIP_LAYER_CASE(KK, CC)                                                           \
     if (lay.k == KK && code == CC) e = imm ? launch_layer_t<KK, CC, true>(a, pl.smem, s) \
                                            : launch_layer_t<KK, CC, false>(a, pl.smem, s);

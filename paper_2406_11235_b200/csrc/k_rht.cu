@@ -62,13 +62,25 @@ constexpr int kRhtWarps = kRhtThreads / 32;
 __device__ unsigned long long* g_rht_trace = nullptr;
 __device__ int g_rht_trace_cap = 0;
 
+// Per-transform pointers of a (grouped) launch: transform z = blockIdx.z uses entry z.
+struct RhtIO {
+    const uint8_t* sign[kMaxGroup];
+    const float* in[kMaxGroup];
+    void* out[kMaxGroup];
+    float out_scale[kMaxGroup];
+};
+
 template <int E, int RA>
-__global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const uint8_t* __restrict__ sign,
-                                                           const float* __restrict__ in, int64_t in_stride,
-                                                           void* __restrict__ out, int64_t out_stride, int inverse,
-                                                           float out_scale, int out_mode, int64_t pad_to,
+__global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __grid_constant__ RhtIO io,
+                                                           int64_t in_stride, int64_t out_stride, int inverse,
+                                                           int out_mode, int64_t pad_to,
                                                            int* __restrict__ zero_ptr, int zero_n) {
     extern __shared__ __align__(16) float sm[];
+    const int z = blockIdx.z;
+    const uint8_t* __restrict__ sign = io.sign[z];
+    const float* __restrict__ in = io.in[z];
+    void* __restrict__ out = io.out[z];
+    const float out_scale = io.out_scale[z];
     const int L2 = 1 << plan.a2;
     const int CL = L2 < 32 ? L2 : 32;                        // lanes per row
     const int rpw = 32 / CL;                                 // rows side by side in a warp
@@ -108,7 +120,7 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const ui
     ptx::pdl_wait();                                         // the input may be the previous kernel's output
     ptx::pdl_launch_dependents();
     trace.waited(g_rht_trace);
-    if (blockIdx.x == 0 && blockIdx.y == 0)
+    if (blockIdx.x == 0 && blockIdx.y == 0 && z == 0)
         for (int i = tid; i < zero_n; i += kRhtThreads) zero_ptr[i] = 0;
     __syncthreads();
 
@@ -264,9 +276,9 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
 }
 
 template <int E, int RA>
-static cudaError_t launch_rht_t(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in,
-                                int64_t in_stride, void* out, int64_t out_stride, int inverse, float out_scale,
-                                cudaStream_t s, int out_mode, int64_t pad, int* zero_ptr, int zero_n) {
+static cudaError_t launch_rht_t(const RhtPlan& plan, int G, int64_t B, const RhtIO& io, int64_t in_stride,
+                                int64_t out_stride, int inverse, cudaStream_t s, int out_mode, int64_t pad,
+                                int* zero_ptr, int zero_n) {
     const int L2 = 1 << plan.a2;
     const size_t smem = sizeof(float) * ((size_t)((plan.f * plan.rows_per_cta + 3) & ~3) +
                                          (size_t)kRhtWarps * plan.rows_per_cta * L2 + (size_t)(plan.n >> 5));
@@ -277,24 +289,48 @@ static cudaError_t launch_rht_t(const RhtPlan& plan, int64_t B, const uint8_t* s
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B);
-    return launch_pdl(kern, grid, dim3(kRhtThreads), smem, s, plan, sign, in, in_stride, out, out_stride, inverse,
-                      out_scale, out_mode, pad, zero_ptr, zero_n);
+    dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B, (unsigned)G);
+    return launch_pdl(kern, grid, dim3(kRhtThreads), smem, s, plan, io, in_stride, out_stride, inverse, out_mode, pad,
+                      zero_ptr, zero_n);
 }
 
-cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
-                       void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode,
-                       int64_t pad_to, int* zero_ptr, int zero_n) {
-    const float out_scale = (float)(scale / std::sqrt((double)plan.n));
+static cudaError_t launch_rht_io(const RhtPlan& plan, int G, int64_t B, const RhtIO& io, int64_t in_stride,
+                                 int64_t out_stride, int inverse, cudaStream_t s, int out_mode, int64_t pad_to,
+                                 int* zero_ptr, int zero_n) {
     const int64_t pad = pad_to < plan.n ? plan.n : pad_to;
     cudaError_t e = cudaErrorInvalidValue;
 #define QTIP_RHT_CASE(EE, RR) \
-    if (plan.E == EE && plan.RA == RR) e = launch_rht_t<EE, RR>(plan, B, sign, in, in_stride, out, out_stride, inverse, out_scale, s, out_mode, pad, zero_ptr, zero_n);
+    if (plan.E == EE && plan.RA == RR) e = launch_rht_t<EE, RR>(plan, G, B, io, in_stride, out_stride, inverse, s, out_mode, pad, zero_ptr, zero_n);
     QTIP_RHT_CASE(1, 1) QTIP_RHT_CASE(1, 2) QTIP_RHT_CASE(1, 4) QTIP_RHT_CASE(2, 1) QTIP_RHT_CASE(2, 2)
     QTIP_RHT_CASE(2, 4) QTIP_RHT_CASE(4, 1) QTIP_RHT_CASE(8, 1)
 #undef QTIP_RHT_CASE
     count_launch(1);
     return e;
+}
+
+cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
+                       void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode,
+                       int64_t pad_to, int* zero_ptr, int zero_n) {
+    RhtIO io{};
+    io.sign[0] = sign;
+    io.in[0] = in;
+    io.out[0] = out;
+    io.out_scale[0] = (float)(scale / std::sqrt((double)plan.n));
+    return launch_rht_io(plan, 1, B, io, in_stride, out_stride, inverse, s, out_mode, pad_to, zero_ptr, zero_n);
+}
+
+cudaError_t launch_rht_group(const RhtPlan& plan, int G, int64_t B, const uint8_t* const* sign, const float* const* in,
+                             int64_t in_stride, void* const* out, int64_t out_stride, int inverse, const float* scale,
+                             cudaStream_t s, int out_mode, int64_t pad_to) {
+    if (G < 1 || G > kMaxGroup) return cudaErrorInvalidValue;
+    RhtIO io{};
+    for (int g = 0; g < G; ++g) {
+        io.sign[g] = sign[g];
+        io.in[g] = in[g];
+        io.out[g] = out[g];
+        io.out_scale[g] = (float)(scale[g] / std::sqrt((double)plan.n));
+    }
+    return launch_rht_io(plan, G, B, io, in_stride, out_stride, inverse, s, out_mode, pad_to, nullptr, 0);
 }
 
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,

@@ -70,3 +70,24 @@ class QTIPLinear:
     def stream_bytes(self):
         """Algorithmic compressed bytes m n k / 8 (the metric's numerator)."""
         return self.m * self.n * self.k // 8
+
+
+def forward_group(layers, x, outs=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_OUT, stream=None):
+    """Same-shape QTIPLinear layers applied to one input x (e.g. q, k, v): one qtip_matvec_group
+    call (grouped RHT-in, one persistent decode-GEMV launch over all layers, grouped RHT-out)."""
+    l0 = layers[0]
+    for l in layers[1:]:
+        if (l.m, l.n, l.code, l.k) != (l0.m, l0.n, l0.code, l0.k) or bytes(l.p) != bytes(l0.p):
+            raise ValueError("forward_group: layers must share shape and QTIP parameters")
+    assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.shape[1] == l0.n
+    B = x.shape[0]
+    if outs is None:
+        outs = [torch.empty((B, l.m), dtype=torch.float32, device=l.device) for l in layers]
+    if B == 0:                                      # empty batch: nothing to compute, no launch
+        return outs
+    qtip.qtip_matvec_group(l0.p, l0.m, l0.n, B, [l.packed for l in layers],
+                           [l.lut for l in layers] if l0.code == "hyb" else None,
+                           [l.sign_n for l in layers], [l.sign_m for l in layers], [l.scale for l in layers], x, outs,
+                           flags, [l.workspace(B) for l in layers], stream)
+    return outs
+

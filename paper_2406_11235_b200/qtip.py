@@ -24,7 +24,7 @@ STATUS = {0: "QTIP_OK", -1: "QTIP_ERR_INVALID_PARAMS", -2: "QTIP_ERR_SHAPE", -3:
           -4: "QTIP_ERR_ALIGNMENT", -5: "QTIP_ERR_UNSUPPORTED", -6: "QTIP_ERR_CUDA", -7: "QTIP_ERR_WORKSPACE"}
 
 EXPORTS = ["qtip_params_default", "qtip_params_check", "qtip_packed_bytes", "qtip_pack", "qtip_pack_states",
-           "qtip_decode", "qtip_matvec", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
+           "qtip_decode", "qtip_matvec", "qtip_matvec_group", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
            "qtip_set_matvec_impl", "qtip_get_matvec_impl", "qtip_status_string", "qtip_last_error",
            "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl", "qtip_viterbi_workspace_bytes",
            "qtip_viterbi_tailbite"]
@@ -72,6 +72,10 @@ def load(path=LIB_PATH):
     lib.qtip_matvec.argtypes = [P, i64, i64, i64, vp, vp, vp, vp, ctypes.c_float, vp, vp, i64, i64, ctypes.c_int,
                                 vp, ctypes.c_size_t, vp]
     lib.qtip_matvec.restype = ctypes.c_int
+    PP = ctypes.POINTER(vp)
+    lib.qtip_matvec_group.argtypes = [P, ctypes.c_int, i64, i64, i64, PP, PP, PP, PP, ctypes.POINTER(ctypes.c_float),
+                                      vp, PP, ctypes.c_int, PP, ctypes.c_size_t, vp]
+    lib.qtip_matvec_group.restype = ctypes.c_int
     lib.qtip_matvec_workspace_bytes.argtypes = [P, i64, i64, i64]
     lib.qtip_matvec_workspace_bytes.restype = ctypes.c_size_t
     lib.qtip_rht.argtypes = [i64, i64, vp, vp, vp, ctypes.c_int, vp]
@@ -173,6 +177,18 @@ def qtip_matvec(p, m, n, B, d_packed, d_lut, d_sign_n, d_sign_m, scale, d_x, d_y
     _check("qtip_matvec", load().qtip_matvec(ctypes.byref(p), m, n, B, _ptr(d_packed), _ptr(d_lut), _ptr(d_sign_n),
                                              _ptr(d_sign_m), float(scale), _ptr(d_x), _ptr(d_y), row_begin, row_end,
                                              flags, _ptr(d_workspace), ws_bytes, _stream(stream)))
+
+
+def qtip_matvec_group(p, m, n, B, d_packed, d_lut, d_sign_n, d_sign_m, scales, d_x, d_y,
+                      flags=QTIP_RHT_IN | QTIP_RHT_OUT, d_workspace=None, stream=None):
+    """G same-shape layers on one input (lists of device tensors, one entry per layer)."""
+    G = len(d_packed)
+    arr = lambda ts: (ctypes.c_void_p * G)(*[_ptr(t) for t in ts])
+    ws_bytes = min(w.numel() * w.element_size() for w in d_workspace)
+    _check("qtip_matvec_group", load().qtip_matvec_group(
+        ctypes.byref(p), G, m, n, B, arr(d_packed), None if d_lut is None else arr(d_lut), arr(d_sign_n), arr(d_sign_m),
+        (ctypes.c_float * G)(*[float(v) for v in scales]), _ptr(d_x), arr(d_y), flags, arr(d_workspace), ws_bytes,
+        _stream(stream)))
 
 
 def viterbi_workspace_bytes(p, T):

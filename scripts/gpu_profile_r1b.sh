@@ -15,7 +15,7 @@ timeout 400 python bench.py --no-cpu-baseline --code 1mad --k 2 --steps 10 > $O/
 timeout 600 python bench.py --no-cpu-baseline --workload c4-70b --steps 10 > $O/c4_70b_1gpu.json 2> $O/c4_70b_1gpu.err
 timeout 900 python bench.py --no-cpu-baseline --workload llama2-70b --steps 3 --warmup 3 > $O/c5_70b_hyb3_1gpu.json 2> $O/c5_70b_hyb3_1gpu.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemv -s 700 -c 7 -o $O/prof_gemv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/prof_gemv.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemv|layer_kernel" -s 700 -c 4 -o $O/prof_gemv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/prof_gemv.log 2>&1
 timeout 120 ./scripts/pipe_mix_microbench > $O/pipe_mix.txt 2>&1
 timeout 120 ./scripts/decode_microbench > $O/decode_microbench.txt 2>&1
 timeout 300 ncu --set full --clock-control none -k regex:loop -c 1 -o $O/prof_decode_loop ./scripts/decode_microbench > $O/prof_decode_loop.log 2>&1

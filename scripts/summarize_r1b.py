@@ -144,7 +144,8 @@ def main():
         if tot_n:
             tp = os.path.join(DST, "traffic.json")
             t = json.load(open(tp)) if os.path.exists(tp) else {}
-            t["llama2-7b/3inst/k2"] = {"dram_bytes_per_launch": tot_b / tot_n, "launches": tot_n, "kernels": names,
+            # one block's GEMV launches (grouped q,k,v / gate,up count once): bytes per LAYER (7)
+            t["llama2-7b/3inst/k2"] = {"dram_bytes_per_layer": tot_b / 7, "launches": tot_n, "kernels": names,
                                       "report": f"gpurun_out/{TAG}/prof_gemv.ncu-rep (profiles/{TAG}_ncu_gemv.json)"}
             with open(tp, "w") as f:
                 json.dump(t, f, indent=1)
