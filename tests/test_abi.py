@@ -143,3 +143,29 @@ def test_degenerate_arguments_are_refused(lib):
     p4 = qtip.params_default("3inst", 4)
     assert vt(pp=p4) == -5                                         # V = 1 Viterbi: k in {2, 3}
 
+
+
+def test_group_call_validation(lib):
+    """qtip_matvec_group refuses bad group sizes, NULL arrays and per-member errors before any launch."""
+    p = qtip.params_default("3inst", 2)
+    vp = ctypes.c_void_p
+    lib.qtip_matvec_group.argtypes = [ctypes.POINTER(qtip.QtipParams), ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                      ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_float), vp, ctypes.POINTER(vp),
+                                      ctypes.c_int, ctypes.POINTER(vp), ctypes.c_size_t, vp]
+    lib.qtip_matvec_group.restype = ctypes.c_int
+    G = 3
+    arr = lambda v: (vp * G)(*([vp(v)] * G))
+    sc = (ctypes.c_float * G)(1.0, 1.0, 1.0)
+    ws = 1 << 20
+
+    def call(G=3, m=256, n=256, B=1, flags=3, packed=None, sn=None, wsb=ws):
+        return lib.qtip_matvec_group(ctypes.byref(p), G, m, n, B, packed or arr(256), None, sn or arr(256), arr(256), sc,
+                                     vp(256), arr(512), flags, arr(256), wsb, None)
+    assert call(G=0) == -1 and call(G=5) == -1                     # group size 1..4
+    assert call(B=0) == -1 and call(m=250) == -2 and call(flags=8) == -1
+    assert call(packed=(vp * G)(vp(256), None, vp(256))) == -1   # NULL member buffer
+    assert call(packed=arr(8)) == -4                               # misaligned member stream
+    assert call(wsb=16) == -7                                      # workspace too small
+    assert lib.qtip_matvec_group(ctypes.byref(p), 3, 256, 256, 1, None, None, arr(256), arr(256), sc, vp(256), arr(512),
+                                 3, arr(256), ws, None) == -1
