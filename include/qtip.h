@@ -135,6 +135,10 @@ size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, i
  *   between the layers) and ONE grouped RHT-out launch; otherwise G qtip_matvec calls.  Results
  *   equal G qtip_matvec calls with qtip_set_matvec_impl(6) bit for bit (canonical row sums, R18).
  *   Errors as qtip_matvec, plus QTIP_ERR_INVALID_PARAMS for G outside 1..4 or NULL arrays. */
+/* 1 if qtip_matvec_group with these arguments runs as the grouped launches (else G per-layer calls,
+ * which a caller may prefer to run concurrently on its own streams), 0 otherwise. */
+int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B);
+
 qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B,
                               const void* const* d_packed, const uint16_t* const* d_lut, const uint8_t* const* d_sign_n,
                               const uint8_t* const* d_sign_m, const float* scale, const float* d_x, float* const* d_y,

@@ -209,6 +209,15 @@ static void record_event(cudaEvent_t ev, cudaStream_t s) {
         cudaEventRecord(ev, s);
 }
 
+int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B) {
+    if (G < 2 || G > kMaxGroup || qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1 || B > 64)
+        return 0;
+    if (!(g_impl == 0 || g_impl == 6)) return 0;
+    // measured: HYB at B >= 4 runs faster as concurrent per-layer row-tile kernels
+    if (g_impl == 0 && p->code == QTIP_CODE_HYB && B >= 4) return 0;
+    return layer_group_supported(make_layout(m, n, p->k), p->code, code_args(p), B, G) ? 1 : 0;
+}
+
 qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B,
                               const void* const* d_packed, const uint16_t* const* d_lut, const uint8_t* const* d_sign_n,
                               const uint8_t* const* d_sign_m, const float* scale, const float* d_x, float* const* d_y,
@@ -236,10 +245,7 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
     const CodeArgs ca = code_args(p);
     const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
     const bool xready = (flags & QTIP_XT_READY) != 0;
-    const int64_t tile_rows = (m + kTile - 1) / kTile;
-    const bool grouped = G > 1 && (g_impl == 0 || g_impl == 6) &&
-                         layer_supported(l, p->code, ca, B, tile_rows, false, false) &&
-                         tile_rows >= (num_sms() + G - 1) / G;
+    const bool grouped = qtip_matvec_group_fused(p, G, m, n, B) != 0;
     if (!grouped) {                                              // one layer at a time (same results)
         for (int g = 0; g < G; ++g) {
             st = qtip_matvec(p, m, n, B, d_packed[g], d_lut ? d_lut[g] : nullptr, d_sign_n[g], d_sign_m[g], scale[g], d_x, d_y[g], 0, m,

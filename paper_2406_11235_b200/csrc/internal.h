@@ -127,6 +127,7 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
 // G same-shape layers in one persistent launch (x~ already in each layer's workspace, no RHT
 // phases): CTAs [g P / G, (g+1) P / G) run layer g in rows mode.  cudaErrorInvalidConfiguration
 // when a layer has fewer tile rows than its CTAs or the shared memory does not fit.
+bool layer_group_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int G);
 cudaError_t launch_layer_group(const Layout& lay, int code, const CodeArgs& ca, int G, const void* const* packed,
                                const uint16_t* const* lut, const float* scale, float* const* y, int64_t B,
                                uint32_t* const* xt_g, int64_t row_words, float* const* ws_f, unsigned* const* bar,

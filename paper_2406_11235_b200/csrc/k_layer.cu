@@ -682,14 +682,15 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     }
     const int tile_row0 = (int)args.tile_row0;
     trace_mark(tr && rows_mode && !rht_out, 9);
-    if (rows_mode && args.part_smem) {
+    if (rows_mode) {
         // every row of this CTA is complete here: one thread per (row, batch) item
         for (int t = threadIdx.x; t < nrow_items; t += kLThreads) {
             const int tb = t / B, b = t - tb * B;
             const int Ir = Ia + (tb >> 4), r = tb & 15;
             const int i = (tile_row0 + Ir) * kTile + r;
             const int u0 = Ir * n_units;
-            finish(b, i, thread_row_sum(part + ((u0 - L0i) * kTile + r) * B + b, kTile * B, n_units));
+            finish(b, i, args.part_smem ? thread_row_sum(part + ((u0 - L0i) * kTile + r) * B + b, kTile * B, n_units)
+                                        : thread_row_sum(a_gpart + ((int64_t)b * m_pad + i) * n_units, 1, n_units));
         }
         nrow_items = 0;                                               // nothing left for the warp loop
     }
@@ -906,9 +907,10 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
                                    : (int)((pl->T + P - 1) / P);
     const size_t chunk = (size_t)pl->CP * 64 * lay.k;
     const size_t head = 8 * kLWarps * kLMaxStages;
-    size_t part = align128((size_t)pl->max_units * kTile * B * 4);
-    pl->part_smem = part <= 48 * 1024;
-    if (!pl->part_smem) part = 0;
+    // unit partials in shared memory whenever the whole plan still fits (else in the workspace)
+    const size_t part_bytes = align128((size_t)pl->max_units * kTile * B * 4);
+    size_t part = part_bytes;
+    pl->part_smem = 1;
     const size_t xs = align128((size_t)B * lay.n_pad * (hyb ? 2 : 4));
     const size_t vin = align128(((size_t)B * lay.n + 31) / 32 * 32 * 4);
     const size_t vin_pad = align128((size_t)B * lay.n_pad * 4);
@@ -949,10 +951,16 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
     // the deepest ring that still lets a second CTA (the next layer's, under PDL) share the SM,
     // else the deepest that fits one CTA per SM
     int pick = 0;
-    for (int S = kLMaxStages; S >= 2 && !pick; --S)
-        if (layout(S) <= 113 * 1024) pick = S;
-    for (int S = kLMaxStages; S >= 2 && !pick; --S)
-        if (layout(S) <= 225 * 1024) pick = S;                         // + static shared memory
+    for (int pass = 0; pass < 2 && !pick; ++pass) {
+        if (pass == 1) {                                              // partials to the workspace instead
+            pl->part_smem = 0;
+            part = 0;
+        }
+        for (int S = kLMaxStages; S >= 2 && !pick; --S)
+            if (layout(S) <= 113 * 1024) pick = S;
+        for (int S = kLMaxStages; S >= 2 && !pick; --S)
+            if (layout(S) <= 225 * 1024) pick = S;                     // + static shared memory
+    }
     if (!pick) return false;
     pl->S = pick;
     pl->smem = layout(pick);
@@ -1067,6 +1075,16 @@ cudaError_t launch_layer(const Layout& lay, int code, const CodeArgs& ca, const 
 #undef QTIP_LAYER_CASE
     count_launch(1);
     return e;
+}
+
+bool layer_group_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int G) {
+    if (G < 2 || G > kMaxGroup) return false;
+    const int64_t tile_rows = (lay.m + kTile - 1) / kTile;
+    if (!layer_supported(lay, code, ca, B, tile_rows, false, false)) return false;
+    const int P = num_sms();
+    if (tile_rows < (P + G - 1) / G) return false;                    // rows mode for every layer
+    LayerPlan pl;
+    return plan_layer(lay, code, B, tile_rows, false, false, 1, &pl, P / G);
 }
 
 cudaError_t launch_layer_group(const Layout& lay, int code, const CodeArgs& ca, int G, const void* const* packed,

@@ -72,6 +72,16 @@ class QTIPLinear:
         return self.m * self.n * self.k // 8
 
 
+_SIDE = {}
+
+
+def _side_streams(device, count):
+    lst = _SIDE.setdefault(str(device), [])
+    while len(lst) < count:
+        lst.append(torch.cuda.Stream(device=device))
+    return lst[:count]
+
+
 def forward_group(layers, x, outs=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_OUT, stream=None):
     """Same-shape QTIPLinear layers applied to one input x (e.g. q, k, v): one qtip_matvec_group
     call (grouped RHT-in, one persistent decode-GEMV launch over all layers, grouped RHT-out)."""
@@ -84,6 +94,19 @@ def forward_group(layers, x, outs=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_O
     if outs is None:
         outs = [torch.empty((B, l.m), dtype=torch.float32, device=l.device) for l in layers]
     if B == 0:                                      # empty batch: nothing to compute, no launch
+        return outs
+    if len(layers) > 1 and stream is None and not qtip.group_fused(l0.p, len(layers), l0.m, l0.n, B):
+        # no grouped launch for this shape / batch: the layers run concurrently on side streams
+        cur = torch.cuda.current_stream(l0.device)
+        side = _side_streams(l0.device, len(layers) - 1)
+        for s in side:
+            s.wait_stream(cur)
+        layers[0].forward(x, out=outs[0], flags=flags)
+        for s, l, o in zip(side, layers[1:], outs[1:]):
+            with torch.cuda.stream(s):
+                l.forward(x, out=o, flags=flags)
+        for s in side:
+            cur.wait_stream(s)
         return outs
     qtip.qtip_matvec_group(l0.p, l0.m, l0.n, B, [l.packed for l in layers],
                            [l.lut for l in layers] if l0.code == "hyb" else None,

@@ -24,7 +24,7 @@ STATUS = {0: "QTIP_OK", -1: "QTIP_ERR_INVALID_PARAMS", -2: "QTIP_ERR_SHAPE", -3:
           -4: "QTIP_ERR_ALIGNMENT", -5: "QTIP_ERR_UNSUPPORTED", -6: "QTIP_ERR_CUDA", -7: "QTIP_ERR_WORKSPACE"}
 
 EXPORTS = ["qtip_params_default", "qtip_params_check", "qtip_packed_bytes", "qtip_pack", "qtip_pack_states",
-           "qtip_decode", "qtip_matvec", "qtip_matvec_group", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
+           "qtip_decode", "qtip_matvec", "qtip_matvec_group", "qtip_matvec_group_fused", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
            "qtip_set_matvec_impl", "qtip_get_matvec_impl", "qtip_status_string", "qtip_last_error",
            "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl", "qtip_viterbi_workspace_bytes",
            "qtip_viterbi_tailbite"]
@@ -76,6 +76,8 @@ def load(path=LIB_PATH):
     lib.qtip_matvec_group.argtypes = [P, ctypes.c_int, i64, i64, i64, PP, PP, PP, PP, ctypes.POINTER(ctypes.c_float),
                                       vp, PP, ctypes.c_int, PP, ctypes.c_size_t, vp]
     lib.qtip_matvec_group.restype = ctypes.c_int
+    lib.qtip_matvec_group_fused.argtypes = [P, ctypes.c_int, i64, i64, i64]
+    lib.qtip_matvec_group_fused.restype = ctypes.c_int
     lib.qtip_matvec_workspace_bytes.argtypes = [P, i64, i64, i64]
     lib.qtip_matvec_workspace_bytes.restype = ctypes.c_size_t
     lib.qtip_rht.argtypes = [i64, i64, vp, vp, vp, ctypes.c_int, vp]
@@ -189,6 +191,11 @@ def qtip_matvec_group(p, m, n, B, d_packed, d_lut, d_sign_n, d_sign_m, scales, d
         ctypes.byref(p), G, m, n, B, arr(d_packed), None if d_lut is None else arr(d_lut), arr(d_sign_n), arr(d_sign_m),
         (ctypes.c_float * G)(*[float(v) for v in scales]), _ptr(d_x), arr(d_y), flags, arr(d_workspace), ws_bytes,
         _stream(stream)))
+
+
+def group_fused(p, G, m, n, B):
+    """True if qtip_matvec_group runs these G layers as the grouped launches."""
+    return bool(load().qtip_matvec_group_fused(ctypes.byref(p), G, m, n, B))
 
 
 def viterbi_workspace_bytes(p, T):

@@ -370,31 +370,35 @@ def test_maximum_batch(cuda_lib, code, k):
     assert rel_l2(y, ref) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("code,k,G,m,n,B", [("3inst", 2, 3, 1024, 512, 1), ("hyb", 4, 2, 1280, 256, 2),
-                                            ("1mad", 3, 4, 688, 256, 4), ("3inst", 2, 3, 256, 256, 1)])
-def test_grouped_matvec_equals_per_layer_calls(cuda_lib, code, k, G, m, n, B):
-    """qtip_matvec_group == G qtip_matvec calls with the persistent kernel (impl 6), bit for bit, for
-    every flag combination (grouped launch when every layer keeps a tile row per CTA; the
-    256-row case exercises the per-layer path); member 0 also against the oracle."""
+@pytest.mark.parametrize("code,k,G,m,n,B,grouped", [("3inst", 2, 3, 1024, 512, 1, True), ("hyb", 4, 2, 1280, 256, 2, True),
+                                                    ("1mad", 3, 4, 688, 256, 4, True), ("3inst", 2, 3, 256, 256, 1, False),
+                                                    ("hyb", 4, 2, 11008, 4096, 4, False)])
+def test_grouped_matvec_equals_per_layer_calls(cuda_lib, code, k, G, m, n, B, grouped):
+    """qtip_matvec_group == G qtip_matvec calls, bit for bit, for every flag combination: against the
+    persistent kernel (impl 6) when the group ran as one launch (one RHT-in + one GEMV (+ one
+    RHT-out) launch), else against the auto per-layer calls (256 rows: too few tile rows per CTA;
+    11008 x 4096 at B = 4: the grouped plan does not fit shared memory); member 0 also against
+    the oracle on the small shapes."""
     from paper_2406_11235_b200.layer import forward_group
     lut = lut_for(code)
     tiles = [synth.random_tiles(m, n, k, seed=50 + g) for g in range(G)]
     layers = [make_layer(cuda_lib, m, n, code, k, tiles[g], lut, seed=20 + g, scale=0.5 + g) for g in range(G)]
     x = torch.from_numpy(synth.random_x(B, n, seed=77)).cuda()
-    for flags in (0, 1, 2, 3):
+    for flags in (1, 3, 0, 2):
         c0 = cuda_lib.launch_count()
         outs = [o.cpu().numpy() for o in forward_group(layers, x, flags=flags)]
         launches = cuda_lib.launch_count() - c0
-        sms = torch.cuda.get_device_properties(0).multi_processor_count
-        grouped = m // 16 >= -(-sms // G)
-        cuda_lib.set_matvec_impl(6 if grouped else 0)
+        if flags & 1:
+            ran_grouped = launches == 2 + bool(flags & 2)
+            if grouped is not None:
+                assert ran_grouped == grouped, (flags, launches)
+        cuda_lib.set_matvec_impl(6 if ran_grouped else 0)
         try:
             ref = [l(x, flags=flags).cpu().numpy() for l in layers]
         finally:
             cuda_lib.set_matvec_impl(0)
         for g in range(G):
             assert np.array_equal(outs[g], ref[g]), (flags, g)
-        if grouped and flags & 1:                       # one RHT-in, one GEMV (+ one RHT-out) launch
-            assert launches == 2 + bool(flags & 2), (flags, launches)
-    want = _oracle_matvec(tiles[0], code, k, lut, m, n, x.cpu().numpy(), 20, 0.5)
-    assert rel_l2(outs[0], want) <= MATVEC_TOL
+        if flags == 3 and m * n <= 1 << 20:
+            want = _oracle_matvec(tiles[0], code, k, lut, m, n, x.cpu().numpy(), 20, 0.5)
+            assert rel_l2(outs[0], want) <= MATVEC_TOL
