@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
     const float* x = in + bt * in_stride;
     const int j_lo = f * warp / kRhtWarps, j_hi = f * (warp + 1) / kRhtWarps;
     // loads of U rows are issued together before their FMAs (the latency is L2's, ~U x fewer round trips)
-    constexpr int U = E >= 4 ? 2 : 8;
+    constexpr int U = E >= 4 ? 2 : 16;                       // f = 128 (n = 4096): one round of loads per warp
     auto slice = [&](auto kind) {
         constexpr int K = decltype(kind)::value;             // 0 plain, 1 sign words, 2 sign bytes
         const float* xp = x + (int64_t)j_lo * L2 + c;
