@@ -402,3 +402,33 @@ def test_grouped_matvec_equals_per_layer_calls(cuda_lib, code, k, G, m, n, B, gr
         if flags == 3 and m * n <= 1 << 20:
             want = _oracle_matvec(tiles[0], code, k, lut, m, n, x.cpu().numpy(), 20, 0.5)
             assert rel_l2(outs[0], want) <= MATVEC_TOL
+
+
+def test_grouped_two_sign_hyb_and_distinct_luts(cuda_lib):
+    """Grouped launch with HYB two-sign and a different LUT per member: each member
+    against its own per-layer impl 6 call (bitwise) and the oracle."""
+    from paper_2406_11235_b200.layer import QTIPLinear, forward_group
+    m, n, k, G = 1280, 512, 3, 2
+    luts = [synth.gaussian_lut(9, 4100 + g) for g in range(G)]
+    tiles = [synth.random_tiles(m, n, k, seed=95 + g) for g in range(G)]
+    layers = []
+    for g in range(G):
+        l = QTIPLinear(m, n, code="hyb", k=k, two_sign=True)
+        l.load_tiles(tiles[g], synth.random_sign_bytes(m, 3101 + g), synth.random_sign_bytes(n, 3100 + g),
+                     scale=0.7 + g, lut=luts[g])
+        layers.append(l)
+    x = torch.from_numpy(synth.random_x(1, n, seed=96)).cuda()
+    c0 = cuda_lib.launch_count()
+    outs = [o.cpu().numpy() for o in forward_group(layers, x)]
+    assert cuda_lib.launch_count() - c0 == 3                     # grouped RHT-in, GEMV, RHT-out
+    cuda_lib.set_matvec_impl(6)
+    try:
+        ref = [l(x).cpu().numpy() for l in layers]
+    finally:
+        cuda_lib.set_matvec_impl(0)
+    for g in range(G):
+        assert np.array_equal(outs[g], ref[g]), g
+        p = gemv.Params(k=k, V=2, code="hyb", lut=luts[g], two_sign=True)
+        want = gemv.matvec(gemv.dense_decode(tiles[g], p), x.cpu().numpy().astype(np.float64),
+                           synth.random_sign_bytes(n, 3100 + g), synth.random_sign_bytes(m, 3101 + g), scale=0.7 + g)
+        assert rel_l2(outs[g], want) <= MATVEC_TOL
