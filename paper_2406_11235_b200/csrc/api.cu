@@ -255,8 +255,8 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
         return QTIP_OK;
     }
     RhtPlan pn{}, pm{};
-    if (rin && !xready && make_rht_plan(n, &pn) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
-    if (rout && make_rht_plan(m, &pm) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
+    if (rin && !xready && make_rht_plan(n, &pn, 128 / G) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
+    if (rout && make_rht_plan(m, &pm, 128 / G) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);
     const int xmode = gemv_mma_xt_mode(p->code);

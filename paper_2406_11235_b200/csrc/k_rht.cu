@@ -241,7 +241,7 @@ __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t 
 
 constexpr int64_t kRhtMaxN = 48 * 1024;
 
-cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
+cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas) {
     int b, a;
     if (!hadamard_factor(n, &b, &a)) return cudaErrorInvalidValue;
     if (n > kRhtMaxN) return cudaErrorInvalidValue;
@@ -260,7 +260,7 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan) {
     int RA = 1;
     if (plan->E <= 2) {
         RA = 4;
-        while (RA > 1 && (plan->f + RA * rpw - 1) / (RA * rpw) < 128) RA /= 2;
+        while (RA > 1 && (plan->f + RA * rpw - 1) / (RA * rpw) < min_ctas) RA /= 2;
     }
     plan->RA = RA;
     plan->rows_per_cta = RA * rpw;
