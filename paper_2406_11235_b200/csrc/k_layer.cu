@@ -400,6 +400,12 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         }
     };
     const int L0i = (int)L0, L1i = (int)L1;
+    // the end-of-launch reduction's row range, computed here (its integer divisions off the tail)
+    int Ia = 0, nrow_items = 0;
+    if (L1 > L0) {
+        Ia = L0i / n_units;
+        nrow_items = ((L1i - 1) / n_units - Ia + 1) * kTile * B;
+    }
     UnitIt first{L0i + warp, (L0i + warp) / n_units, (L0i + warp) % n_units};
     // Weight chunks are fetched by the whole warp with 16-byte cp.async (LDGSTS) into its ring stage,
     // each lane arriving on the stage's mbarrier when its copies land.  Measured: one
@@ -675,11 +681,6 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         if (rht_out) args.ybuf[b * m_pad + i] = s;
         else if (i >= args.row_lo && i < args.row_hi) a_y[b * args.y_stride + (i - args.row_lo)] = a_scale * s;
     };
-    int Ia = 0, nrow_items = 0;
-    if (L1 > L0) {
-        Ia = L0i / n_units;
-        nrow_items = ((L1i - 1) / n_units - Ia + 1) * kTile * B;
-    }
     const int tile_row0 = (int)args.tile_row0;
     trace_mark(tr && rows_mode && !rht_out, 9);
     if (rows_mode) {
