@@ -365,7 +365,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
     // measured: for HYB at batch 1 the persistent GEMV with the shared-memory
     // LUT fast path (impl 6) beats the row-tile and split-K kernels (at B = 4 it does not)
-    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1) impl = 6;
+    // (measured, scripts/stage_breakdown.py: except for a square 4096 layer, where the row-tile
+    // kernel's launch is 1 us shorter)
+    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1 && !(m <= 4096 && n <= 4096)) impl = 6;
     if (impl == 0) {
         // measured: the row-tile kernel wins while its CTAs (one per 16 rows,
         // 8-16 warps each) fill the GPU in one wave; beyond that the split-K kernel balances better

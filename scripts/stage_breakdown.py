@@ -2,7 +2,7 @@
 """Per-stage times of the 7B block (graph of 32 replicas of one stage, CUDA events): grouped q,k,v,
 o, grouped gate,up, down -- full (RHT-in, GEMV, RHT-out) and GEMV only (x~ ready, RHT-out off).
 
-usage: python scripts/stage_breakdown.py [code] [k] [B]
+usage: python scripts/stage_breakdown.py [code] [k] [B] [matvec impl for the single layers]
 """
 import os
 import sys
@@ -17,7 +17,9 @@ from paper_2406_11235_b200.layer import QTIPLinear, forward_group  # noqa: E402
 code = sys.argv[1] if len(sys.argv) > 1 else "3inst"
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+impl = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 qtip.load()
+qtip.set_matvec_impl(impl)
 lut = synth.gaussian_lut(9) if code == "hyb" else None
 R = 32
 
@@ -66,7 +68,7 @@ for name, shp in stages.items():
         torch.cuda.synchronize()
         res[label] = 1e3 * e0.elapsed_time(e1) / (10 * R)
     nbytes = sum(m * n * k // 8 for (m, n) in shp)
-    print(f"{code} k={k} B={B} {name:18s}: full {res['full']:7.2f} us  gemv-only {res['gemv']:7.2f} us  "
+    print(f"{code} k={k} B={B} impl={impl} {name:18s}: full {res['full']:7.2f} us  gemv-only {res['gemv']:7.2f} us  "
           f"({nbytes / res['gemv'] / 1e3:7.1f} GB/s gemv)  rht+boundaries {res['full'] - res['gemv']:6.2f} us")
     del reps
     torch.cuda.empty_cache()
