@@ -365,16 +365,13 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
     // measured: for HYB at batch 1 the persistent GEMV with the shared-memory
     // LUT fast path (impl 6) beats the row-tile and split-K kernels (at B = 4 it does not)
-    // (measured, scripts/stage_breakdown.py: except for a square 4096 layer, where the row-tile
-    // kernel's launch is 1 us shorter)
-    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1 && !(m <= 4096 && n <= 4096)) impl = 6;
-    if (impl == 0) {
-        // measured: the row-tile kernel wins while its CTAs (one per 16 rows,
-        // 8-16 warps each) fill the GPU in one wave; beyond that the split-K kernel balances better
-        const int64_t tile_rows = (row_end - row_begin + kTile - 1) / kTile;
-        if (row_ok && tile_rows <= 4 * (int64_t)num_sms()) impl = 4;
-        else impl = mma_ok ? 3 : (tc_ok ? 2 : 1);
-    }
+    // measured (scripts/stage_breakdown.py, bench C4/C5): the row-tile kernel wins
+    // while its CTAs (one per 16 rows, two per SM) fill the GPU in one wave and K is short
+    // (4096 x 4096 and 1024 x 8192 HYB layers: ~1-2 us shorter launches than the persistent GEMV);
+    // past one wave the split-K kernel balances better (8192 x 28672 3INST: 68.9 vs 85.4 us)
+    const bool one_wave = launch_tile_rows <= 2 * (int64_t)num_sms();
+    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1 && !(one_wave && n <= 8192)) impl = 6;
+    if (impl == 0) impl = (row_ok && one_wave) ? 4 : (mma_ok ? 3 : (tc_ok ? 2 : 1));
     const bool use_tc = impl == 2, use_mma = impl == 3, use_row = impl == 4;
     cudaStream_t s = (cudaStream_t)stream;
     char* ws = (char*)d_workspace;
