@@ -82,7 +82,7 @@ __device__ __forceinline__ void reduce_row_block(const MmaArgs& args, int64_t RB
 }
 
 template <int K, int CODE, int NG, bool kImm>   // NG = batch groups of 8 (1 or 2); kImm = paper LCG constants
-__global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : 6) gemv_mma_kernel(const MmaArgs args) {
+__global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG == 2 ? 4 : 6)) gemv_mma_kernel(const MmaArgs args) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
     constexpr int TW = 8 * K;
