@@ -88,7 +88,10 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
     constexpr int TW = 8 * K;
     constexpr uint32_t kCellBytes = 2048u * K;                      // packed stream of one cell
     constexpr uint32_t kXRowBytes = kHyb ? 256u : 512u;              // x~ of one cell, one batch row
-    const uint32_t stage_bytes = kCellBytes + kXRowBytes * (uint32_t)args.B;   // rows >= B are not staged
+    // x~ rows padded by 16 B (3INST/1MAD) / 32 B (HYB) when B > 1: the 8 batch rows of a B-fragment
+    // load then fall in different bank groups (unpadded: 8-way conflicts at B = 8)
+    const uint32_t xstride = args.B > 1 ? (kHyb ? 288u : 528u) : kXRowBytes;
+    const uint32_t stage_bytes = kCellBytes + xstride * (uint32_t)args.B;   // rows >= B are not staged
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // kMmaStages mbarriers
     __shared__ int s_last;
     uint8_t* stages = smem + 128;
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
         const int64_t KC = u % n_kc;
         uint8_t* dst = stages + st * stage_bytes + kCellBytes;
         for (int n = 0; n < args.B; ++n)
-            ptx::bulk_g2s(ptx::smem_u32(dst + n * kXRowBytes),
+            ptx::bulk_g2s(ptx::smem_u32(dst + n * xstride),
                           reinterpret_cast<const uint8_t*>(args.xt) + n * args.xt_row_words * 4 + KC * kXRowBytes,
                           kXRowBytes, ptx::smem_u32(full + st));
     };
@@ -165,8 +168,8 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
 #pragma unroll
         for (int pp = 0; pp < kCellTileCols / 2; ++pp) {              // tile pair (2pp, 2pp+1)
             uint32_t bf[2][NG][4];                                   // shared by the warp's two tile rows
-            load_bfrag<NG, kHyb>(xs, kHyb ? 64 : 128, 2 * pp, g, tig, args.B, bf[0]);
-            load_bfrag<NG, kHyb>(xs, kHyb ? 64 : 128, 2 * pp + 1, g, tig, args.B, bf[1]);
+            load_bfrag<NG, kHyb>(xs, (int)(xstride / 4), 2 * pp, g, tig, args.B, bf[0]);
+            load_bfrag<NG, kHyb>(xs, (int)(xstride / 4), 2 * pp + 1, g, tig, args.B, bf[1]);
 #pragma unroll
             for (int tr = 0; tr < 2; ++tr) {
                 const int I = 2 * warp + tr;
@@ -234,7 +237,8 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
 template <int K, int CODE, int NG, bool kImm>
 cudaError_t launch_mma_t(const MmaArgs& a, cudaStream_t s) {
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
-    const size_t smem = 128 + (size_t)kMmaStages * (2048u * K + (kHyb ? 256u : 512u) * (size_t)a.B);
+    const size_t xstride = a.B > 1 ? (kHyb ? 288u : 528u) : (kHyb ? 256u : 512u);   // as in the kernel
+    const size_t smem = 128 + (size_t)kMmaStages * (2048u * K + xstride * (size_t)a.B);
     auto kern = gemv_mma_kernel<K, CODE, NG, kImm>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -57,7 +57,10 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
     constexpr uint32_t kChunkBytes = 256u * K;                       // one cell's 8 tiles of this tile row
     constexpr uint32_t kXRowBytes = kHyb ? 256u : 512u;              // x~ of one cell, one batch row
     const int S = args.stages;
-    const uint32_t stage_bytes = kChunkBytes + kXRowBytes * (uint32_t)args.B;
+    // x~ rows padded by 16 B (3INST/1MAD) / 32 B (HYB) when B > 1: the 8 batch rows of a B-fragment
+    // load then fall in different bank groups (unpadded: 8-way conflicts at B = 8)
+    const uint32_t xstride = args.B > 1 ? (kHyb ? 288u : 528u) : kXRowBytes;
+    const uint32_t stage_bytes = kChunkBytes + xstride * (uint32_t)args.B;   // rows >= B are not staged
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = blockDim.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
         const int st = j % S;
         const int64_t kc = warp + (int64_t)j * W;
         const uint32_t bar = ptx::smem_u32(full + st);
-        ptx::mbar_arrive_expect_tx(bar, stage_bytes);
+        ptx::mbar_arrive_expect_tx(bar, kChunkBytes + kXRowBytes * (uint32_t)args.B);   // bytes copied (not the padded stage)
         ptx::bulk_g2s_stream(ptx::smem_u32(ring + st * stage_bytes),
                       args.packed + (RB * n_kc + kc) * (int64_t)(512 * K) + Il * (kChunkBytes / 4), kChunkBytes, bar);
     };
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
         const int st = j % S;
         const int64_t kc = warp + (int64_t)j * W;
         for (int n = 0; n < args.B; ++n)
-            ptx::bulk_g2s(ptx::smem_u32(ring + st * stage_bytes + kChunkBytes + n * kXRowBytes),
+            ptx::bulk_g2s(ptx::smem_u32(ring + st * stage_bytes + kChunkBytes + n * xstride),
                           reinterpret_cast<const uint8_t*>(args.xt) + n * args.xt_row_words * 4 + kc * kXRowBytes,
                           kXRowBytes, ptx::smem_u32(full + st));
     };
@@ -113,8 +116,8 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
 #pragma unroll
         for (int pp = 0; pp < kCellTileCols / 2; ++pp) {
             uint32_t bf[2][1][4];
-            load_bfrag<1, kHyb>(xs, kHyb ? 64 : 128, 2 * pp, g, tig, args.B, bf[0]);
-            load_bfrag<1, kHyb>(xs, kHyb ? 64 : 128, 2 * pp + 1, g, tig, args.B, bf[1]);
+            load_bfrag<1, kHyb>(xs, (int)(xstride / 4), 2 * pp, g, tig, args.B, bf[0]);
+            load_bfrag<1, kHyb>(xs, (int)(xstride / 4), 2 * pp + 1, g, tig, args.B, bf[1]);
             tile_pair<K, CODE, 1, kImm>(chunk + pp * TW * 2, bf, acc, g, tig, lcg, ca, args.lut);
         }
         __syncwarp();                                                // every lane is done with stage st
@@ -147,7 +150,7 @@ template <int K, int CODE, bool kImm>
 cudaError_t launch_row_t(RowArgs a, int64_t tile_rows, cudaStream_t s) {
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
     auto kern = gemv_row_kernel<K, CODE, kImm>;
-    const size_t stage = 256u * K + (kHyb ? 256u : 512u) * (size_t)a.B;
+    const size_t stage = 256u * K + (a.B > 1 ? (kHyb ? 288u : 528u) : (kHyb ? 256u : 512u)) * (size_t)a.B;
     const size_t fixed = 8 * kRowMaxWarps * kRowMaxStages + 4 * kRowMaxWarps * kTile * (size_t)a.B;
     // widest W whose CTAs all fit in one wave (per-SM CTA count from registers / threads, and a
     // shared-memory share of 227 KB / CTAs); ring depth as deep as that share allows (2..4)
