@@ -88,9 +88,9 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
     constexpr int TW = 8 * K;
     constexpr uint32_t kCellBytes = 2048u * K;                      // packed stream of one cell
     constexpr uint32_t kXRowBytes = kHyb ? 256u : 512u;              // x~ of one cell, one batch row
-    // x~ rows padded by 16 B (3INST/1MAD) / 32 B (HYB) when B > 1: the 8 batch rows of a B-fragment
-    // load then fall in different bank groups (unpadded: 8-way conflicts at B = 8)
-    const uint32_t xstride = args.B > 1 ? (kHyb ? 288u : 528u) : kXRowBytes;
+    // x~ rows padded by 64 B (3INST/1MAD) / 32 B (HYB) when B > 1: the batch rows of a B-fragment
+    // load then spread over all bank groups (unpadded: up to 8-way conflicts at B = 8)
+    const uint32_t xstride = args.B > 1 ? (kHyb ? 288u : 576u) : kXRowBytes;
     const uint32_t stage_bytes = kCellBytes + xstride * (uint32_t)args.B;   // rows >= B are not staged
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);             // kMmaStages mbarriers
     __shared__ int s_last;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
 template <int K, int CODE, int NG, bool kImm>
 cudaError_t launch_mma_t(const MmaArgs& a, cudaStream_t s) {
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
-    const size_t xstride = a.B > 1 ? (kHyb ? 288u : 528u) : (kHyb ? 256u : 512u);   // as in the kernel
+    const size_t xstride = a.B > 1 ? (kHyb ? 288u : 576u) : (kHyb ? 256u : 512u);   // as in the kernel
     const size_t smem = 128 + (size_t)kMmaStages * (2048u * K + xstride * (size_t)a.B);
     auto kern = gemv_mma_kernel<K, CODE, NG, kImm>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

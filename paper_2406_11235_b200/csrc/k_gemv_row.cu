@@ -57,9 +57,9 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
     constexpr uint32_t kChunkBytes = 256u * K;                       // one cell's 8 tiles of this tile row
     constexpr uint32_t kXRowBytes = kHyb ? 256u : 512u;              // x~ of one cell, one batch row
     const int S = args.stages;
-    // x~ rows padded by 16 B (3INST/1MAD) / 32 B (HYB) when B > 1: the 8 batch rows of a B-fragment
-    // load then fall in different bank groups (unpadded: 8-way conflicts at B = 8)
-    const uint32_t xstride = args.B > 1 ? (kHyb ? 288u : 528u) : kXRowBytes;
+    // x~ rows padded by 64 B (3INST/1MAD) / 32 B (HYB) when B > 1: the batch rows of a B-fragment
+    // load then spread over all bank groups (unpadded: up to 8-way conflicts at B = 8)
+    const uint32_t xstride = args.B > 1 ? (kHyb ? 288u : 576u) : kXRowBytes;
     const uint32_t stage_bytes = kChunkBytes + xstride * (uint32_t)args.B;   // rows >= B are not staged
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int W = blockDim.x >> 5;
@@ -150,7 +150,7 @@ template <int K, int CODE, bool kImm>
 cudaError_t launch_row_t(RowArgs a, int64_t tile_rows, cudaStream_t s) {
     constexpr bool kHyb = CODE == QTIP_CODE_HYB;
     auto kern = gemv_row_kernel<K, CODE, kImm>;
-    const size_t stage = 256u * K + (a.B > 1 ? (kHyb ? 288u : 528u) : (kHyb ? 256u : 512u)) * (size_t)a.B;
+    const size_t stage = 256u * K + (a.B > 1 ? (kHyb ? 288u : 576u) : (kHyb ? 256u : 512u)) * (size_t)a.B;
     const size_t fixed = 8 * kRowMaxWarps * kRowMaxStages + 4 * kRowMaxWarps * kTile * (size_t)a.B;
     // widest W whose CTAs all fit in one wave (per-SM CTA count from registers / threads, and a
     // shared-memory share of 227 KB / CTAs); ring depth as deep as that share allows (2..4)

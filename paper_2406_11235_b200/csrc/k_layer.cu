@@ -454,6 +454,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
 
     // ---------------------------------------------------------------- x~
     const int64_t rw = args.row_words;
+    // x~ row stride in shared memory: padded (64 B / HYB 32 B) when x~ is copied in from the workspace
+    // and B > 1, so a B-fragment load's batch rows spread over all bank groups
+    const int xrs = ((args.xt_ready || args.coop) && B > 1) ? (int)rw + (kHyb ? 8 : 16) : (int)rw;
     const int64_t n_pad = args.lay.n_pad;
     if (args.xt_ready || args.coop) {
         if (args.coop && !args.xt_ready) {
@@ -474,9 +477,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
             }
             grid_sync(a_bar, (unsigned)P);
         }
-        const int words = (int)(B * rw);
-        for (int i = threadIdx.x; i < words / 4; i += kLThreads)
-            reinterpret_cast<uint4*>(xs)[i] = __ldcg(reinterpret_cast<const uint4*>(a_xt) + i);
+        const int words = (int)(B * rw), rq = (int)(rw / 4), xq = xrs / 4;
+        for (int i = threadIdx.x; i < words / 4; i += kLThreads) {          // rows at the padded stride
+            const int row = i / rq;
+            reinterpret_cast<uint4*>(xs)[row * xq + (i - row * rq)] = __ldcg(reinterpret_cast<const uint4*>(a_xt) + i);
+        }
     } else {
         const int len = (int)n, np = (int)n_pad;
         const int Ef = args.rht_in ? fwht_fast_E(n, args.na, kLThreads) : 0;
@@ -577,7 +582,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
     if (threadIdx.x < 128) zero_b[threadIdx.x] = 0u;
     __syncthreads();
     const bool bval = g < B;
-    const uint32_t* xsl = bval ? xs + g * rw + (kHyb ? 2 : 4) * tig : zero_b + (kHyb ? 2 : 4) * tig;
+    const uint32_t* xsl = bval ? xs + g * xrs + (kHyb ? 2 : 4) * tig : zero_b + (kHyb ? 2 : 4) * tig;
     const int ustride = bval ? (kHyb ? 64 : 128) : 0;
     const uint32_t* lut = a_lut;
     const uint32_t lut_lane = ptx::smem_u32(smem + args.off_lut) + 4u * lane;
@@ -912,7 +917,7 @@ bool plan_layer(const Layout& lay, int code, int64_t B, int64_t tile_rows, bool 
     const size_t part_bytes = align128((size_t)pl->max_units * kTile * B * 4);
     size_t part = part_bytes;
     pl->part_smem = 1;
-    const size_t xs = align128((size_t)B * lay.n_pad * (hyb ? 2 : 4));
+    const size_t xs = align128((size_t)B * (lay.n_pad * (hyb ? 2 : 4) + (B > 1 ? (hyb ? 32 : 64) : 0)));   // padded rows
     const size_t vin = align128(((size_t)B * lay.n + 31) / 32 * 32 * 4);
     const size_t vin_pad = align128((size_t)B * lay.n_pad * 4);
     const size_t red = (size_t)kLWarps * kMixChunk * 4;
