@@ -200,6 +200,32 @@ qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* 
 
 static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
+// Workspace regions (one caller buffer per layer, 256-B aligned).
+struct WsLayout {
+    size_t xt, partial, yt, cnt, lws, bar, seg, total;
+};
+static WsLayout ws_layout(const qtip_params* p, const Layout& l, int64_t B) {
+    WsLayout o;
+    const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : 64);          // x~ rows (batch pad of the kernels)
+    size_t off = 0;
+    o.xt = off;
+    off += align256(4 * Bx * l.n_pad);
+    o.partial = off;
+    off += align256(4 * l.n_kc * B * l.m_pad);
+    o.yt = off;
+    off += align256(4 * B * l.m_pad);
+    o.cnt = off;
+    off += align256(4 * (l.m_pad / kCellRows + 2));
+    o.lws = off;
+    off += align256(4 * layer_workspace_floats(l, B, 0));
+    o.bar = off;
+    off += 1024;
+    o.seg = off;
+    off += align256(4 * umma_seg_floats(l, p->code, B));
+    o.total = off;
+    return o;
+}
+
 // Profile events also work inside CUDA-graph capture (as external event-record nodes).
 static void record_event(cudaEvent_t ev, cudaStream_t s) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -209,13 +235,29 @@ static void record_event(cudaEvent_t ev, cudaStream_t s) {
         cudaEventRecord(ev, s);
 }
 
+// The auto kernel choice depends on (p, m, n, B) and the group size only -- never on the row range
+// of a call -- so QTIP_XT_READY reuses an x~ written in the same layout.
+static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
+    if (g_impl != 0 && g_impl != 7) return false;
+    if (!umma_supported(l, p->code, code_args(p), B, G)) return false;
+    if (g_impl == 7) return true;
+    // auto (measured, profiles/r2_*): the tcgen05 stream-K kernel wins for HYB at batch
+    // 1-8 once every SM has >= 10 cells of the launch (q,k,v / gate,up groups and the 11008-wide
+    // layers); short single launches keep the row-tile kernel (fixed start-up + stream-K fix-up cost),
+    // and 3INST / 1MAD stay on the register-fed kernels (their decode, not the MMA, is the bound)
+    const int64_t cells = (int64_t)G * l.n_rb * l.n_kc;
+    return p->code == QTIP_CODE_HYB && B <= 8 && cells >= 10 * (int64_t)num_sms();
+}
+
 int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B) {
     if (G < 2 || G > kMaxGroup || qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1 || B > 64)
         return 0;
+    const Layout l = make_layout(m, n, p->k);
+    if (use_umma(p, l, B, G)) return 1;
     if (!(g_impl == 0 || g_impl == 6)) return 0;
     // measured: HYB at B >= 4 runs faster as concurrent per-layer row-tile kernels
     if (g_impl == 0 && p->code == QTIP_CODE_HYB && B >= 4) return 0;
-    return layer_group_supported(make_layout(m, n, p->k), p->code, code_args(p), B, G) ? 1 : 0;
+    return layer_group_supported(l, p->code, code_args(p), B, G) ? 1 : 0;
 }
 
 qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B,
@@ -245,7 +287,11 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
     const CodeArgs ca = code_args(p);
     const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
     const bool xready = (flags & QTIP_XT_READY) != 0;
-    const bool grouped = qtip_matvec_group_fused(p, G, m, n, B) != 0;
+    bool grouped = qtip_matvec_group_fused(p, G, m, n, B) != 0;
+    const bool umma = grouped && use_umma(p, l, B, G);
+    if (umma && p->code == QTIP_CODE_HYB)                        // one shared-memory LUT per launch
+        for (int g = 1; g < G; ++g)
+            if (d_lut[g] != d_lut[0]) grouped = false;
     if (!grouped) {                                              // one layer at a time (same results)
         for (int g = 0; g < G; ++g) {
             st = qtip_matvec(p, m, n, B, d_packed[g], d_lut ? d_lut[g] : nullptr, d_sign_n[g], d_sign_m[g], scale[g], d_x, d_y[g], 0, m,
@@ -258,29 +304,77 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
     if (rin && !xready && make_rht_plan(n, &pn, 128 / G) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
     if (rout && make_rht_plan(m, &pm, 128 / G) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
     cudaStream_t s = (cudaStream_t)stream;
+    const WsLayout o = ws_layout(p, l, B);
+    const float* xin[kMaxGroup];
+    void* xt[kMaxGroup];
+    for (int g = 0; g < G; ++g) {
+        xt[g] = (char*)d_workspace[g] + o.xt;
+        xin[g] = d_x;
+    }
+    cudaError_t e = cudaSuccess;
+    if (umma) {
+        // grouped RHT-in -> one stream-K tcgen05 launch over the G layers' cells -> grouped RHT-out
+        // (or segment reduction) reading the partial-sum segments
+        const int xmode = umma_xt_mode(p->code);
+        const int64_t bp = umma_batch_pad(B);
+        if (!xready) {
+            if (rin) {
+                e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, bp, 0, std::vector<float>(G, 1.0f).data(), s, xmode,
+                                     l.n_pad);
+            } else {
+                for (int g = 0; g < G && e == cudaSuccess; ++g) e = launch_convert(d_x, n, n, B, xt[g], bp, xmode, l.n_pad, s);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group rht_in");
+        }
+        float* segs[kMaxGroup];
+        int* tks[kMaxGroup];
+        float* yo[kMaxGroup];
+        float ysc[kMaxGroup];
+        for (int g = 0; g < G; ++g) {
+            segs[g] = (float*)((char*)d_workspace[g] + o.seg);
+            tks[g] = (int*)((char*)d_workspace[g] + o.cnt);
+            yo[g] = rout ? (float*)((char*)d_workspace[g] + o.yt) : d_y[g];
+            ysc[g] = rout ? 1.0f : scale[g];
+        }
+        const bool prof = g_prof_start && g_prof_stop;
+        if (prof) record_event(g_prof_start, s);
+        e = launch_umma(l, p->code, ca, G, d_packed, d_lut ? d_lut[0] : nullptr, (const void* const*)xt, segs, tks, yo, ysc,
+                        rout ? l.m_pad : m, m, B, 0, l.n_rb, s);
+        if (prof) {
+            record_event(g_prof_stop, s);
+            g_prof_start = g_prof_stop = nullptr;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group gemv");
+        if (rout) {
+            const float* yin[kMaxGroup];
+            void* yout[kMaxGroup];
+            for (int g = 0; g < G; ++g) {
+                yin[g] = yo[g];
+                yout[g] = d_y[g];
+            }
+            e = launch_rht_group(pm, G, B, d_sign_m, yin, l.m_pad, yout, m, 1, scale, s);
+            if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group rht_out");
+        }
+        return QTIP_OK;
+    }
     const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);
+    (void)Bx;
     const int xmode = gemv_mma_xt_mode(p->code);
     const int xmode6 = p->code == QTIP_CODE_HYB ? 5 : xmode;        // HYB fast path: swapped pairs
     const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
-    void* xt[kMaxGroup];
     float* yt[kMaxGroup];
     float* lws[kMaxGroup];
     unsigned* bar[kMaxGroup];
     float* ydst[kMaxGroup];
     float sc[kMaxGroup];
-    const float* xin[kMaxGroup];
     for (int g = 0; g < G; ++g) {                                 // the impl 6 workspace layout
         char* ws = (char*)d_workspace[g];
-        xt[g] = ws;
-        yt[g] = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
-        lws[g] = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad) +
-                          align256(4 * (l.m_pad / kCellRows + 2)));
-        bar[g] = (unsigned*)((char*)lws[g] + align256(4 * layer_workspace_floats(l, B, 0)));
+        yt[g] = (float*)(ws + o.yt);
+        lws[g] = (float*)(ws + o.lws);
+        bar[g] = (unsigned*)(ws + o.bar);
         ydst[g] = rout ? yt[g] : d_y[g];
         sc[g] = rout ? 1.0f : scale[g];
-        xin[g] = d_x;
     }
-    cudaError_t e = cudaSuccess;
     if (!xready) {
         if (rin) {
             e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, l.n_pad, 0, std::vector<float>(G, 1.0f).data(), s,
@@ -309,10 +403,7 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
 
 size_t qtip_matvec_workspace_bytes(const qtip_params* p, int64_t m, int64_t n, int64_t B) {
     if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1) return 0;
-    const Layout l = make_layout(m, n, p->k);
-    const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);       // x~ rows (mma kernel pads the batch)
-    return align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad) +
-           align256(4 * (l.m_pad / kCellRows + 2)) + align256(4 * layer_workspace_floats(l, B, 0)) + 1024;
+    return ws_layout(p, make_layout(m, n, p->k), B).total;
 }
 
 qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, const void* d_packed,
@@ -345,6 +436,47 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
 
     const Layout l = make_layout(m, n, p->k);
     const CodeArgs ca = code_args(p);
+    cudaStream_t s = (cudaStream_t)stream;
+    const WsLayout o = ws_layout(p, l, B);
+    char* ws = (char*)d_workspace;
+    void* xt = ws + o.xt;
+    const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
+    const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
+    cudaError_t e;
+    const bool umma_ok = umma_supported(l, p->code, ca, B, 1);
+    if (g_impl == 7 && !umma_ok)
+        return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 stream-K kernel: needs 2 <= k <= 4, B <= 64, HYB Q = 9 one-sign");
+    if (use_umma(p, l, B, 1)) {
+        // impl 7 (auto default): RHT-in -> stream-K tcgen05 decode-GEMV (k_umma.cu) -> RHT-out reading
+        // the partial-sum segments (or the segment reduction when RHT-out is off)
+        const int xmode = umma_xt_mode(p->code);
+        const int64_t bp = umma_batch_pad(B);
+        e = cudaSuccess;
+        int* tk0 = (int*)(ws + o.cnt);                   // the GEMV's row-block tickets: cleared here
+        const int ntk = (int)(rb1 - rb0);
+        if (!(flags & QTIP_XT_READY)) {
+            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, bp, 0, 1.0f, s, xmode, l.n_pad, tk0, ntk);
+            else e = launch_convert(d_x, n, n, B, xt, bp, xmode, l.n_pad, s, tk0, ntk);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
+        float* segp = (float*)(ws + o.seg);
+        int* tk = (int*)(ws + o.cnt);
+        float* yo = rout ? (float*)(ws + o.yt) : d_y;
+        const float ysc = rout ? 1.0f : scale;
+        const int64_t rows = row_end - row_begin;
+        const bool prof = g_prof_start && g_prof_stop;
+        if (prof) record_event(g_prof_start, s);
+        e = launch_umma(l, p->code, ca, 1, &d_packed, d_lut, (const void* const*)&xt, &segp, &tk, &yo, &ysc,
+                        rout ? l.m_pad : rows, rows, B, rb0, rb1, s);
+        if (prof) {
+            record_event(g_prof_stop, s);
+            g_prof_start = g_prof_stop = nullptr;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec gemv");
+        if (rout) e = launch_rht(pm, B, d_sign_m, yo, l.m_pad, d_y, m, 1, scale, s);
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_out");
+        return QTIP_OK;
+    }
     // kernel choice: 1 CUDA-core reference, 2 tcgen05 (A in TMEM), 3 register-fed mma.sync;
     // auto picks the measured-fastest supported one
     const bool tc_ok = gemv_tc_supported(l, p->code, ca, B);
@@ -353,7 +485,6 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if (g_impl == 2 && !tc_ok) return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 kernel: needs 2 <= k <= 4, B <= 16, HYB Q = 9 one-sign");
     if (g_impl == 3 && !mma_ok) return fail(QTIP_ERR_UNSUPPORTED, "mma kernel: needs 2 <= k <= 4, B <= 16, one-sign HYB");
     if (g_impl == 4 && !row_ok) return fail(QTIP_ERR_UNSUPPORTED, "row kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB");
-    const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
     const int64_t launch_tile_rows = (row_end - row_begin + kTile - 1) / kTile;
     const bool layer_ok = layer_supported(l, p->code, ca, B, launch_tile_rows, rin && !(flags & QTIP_XT_READY), rout);
     if (g_impl == 5 && !layer_ok)
@@ -363,32 +494,26 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         return fail(QTIP_ERR_UNSUPPORTED, "persistent GEMV kernel: needs 2 <= k <= 4, B <= 4, one-sign HYB, shared memory fit");
     int impl = g_impl;
     if (impl == 0 && layer_ok && g_layer_auto) impl = 5;
+    // Fallback when impl 7 does not apply (two-sign HYB, Q != 9, B > 64 is refused anyway): the
+    // choice uses the FULL layer's tile rows, so a row shard takes the same kernel (and the same
+    // x~ layout for QTIP_XT_READY) as the full call.
     // measured: for HYB at batch 1 the persistent GEMV with the shared-memory
     // LUT fast path (impl 6) beats the row-tile and split-K kernels (at B = 4 it does not)
-    // measured (scripts/stage_breakdown.py, bench C4/C5): the row-tile kernel wins
-    // while its CTAs (one per 16 rows, two per SM) fill the GPU in one wave and K is short
-    // (4096 x 4096 and 1024 x 8192 HYB layers: ~1-2 us shorter launches than the persistent GEMV);
-    // past one wave the split-K kernel balances better (8192 x 28672 3INST: 68.9 vs 85.4 us)
-    const bool one_wave = launch_tile_rows <= 2 * (int64_t)num_sms();
-    if (impl == 0 && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1 && !(one_wave && n <= 8192)) impl = 6;
+    const bool one_wave = l.m / kTile <= 2 * (int64_t)num_sms();
+    const bool gemv6_full = layer_supported(l, p->code, ca, B, l.m / kTile, false, false);
+    if (impl == 0 && gemv6_full && gemv6_ok && p->code == QTIP_CODE_HYB && B == 1 && !(one_wave && n <= 8192)) impl = 6;
     if (impl == 0) impl = (row_ok && one_wave) ? 4 : (mma_ok ? 3 : (tc_ok ? 2 : 1));
     const bool use_tc = impl == 2, use_mma = impl == 3, use_row = impl == 4;
-    cudaStream_t s = (cudaStream_t)stream;
-    char* ws = (char*)d_workspace;
-    void* xt = ws;
-    const int64_t Bx = B <= 8 ? 8 : (B <= 16 ? 16 : B);
-    float* partial = (float*)(ws + align256(4 * Bx * l.n_pad));
-    float* yt = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad));
-    int* cnt = (int*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) + align256(4 * B * l.m_pad));
+    float* partial = (float*)(ws + o.partial);
+    float* yt = (float*)(ws + o.yt);
+    int* cnt = (int*)(ws + o.cnt);
     const int n_rb = (int)(l.m_pad / kCellRows);
     const int xmode = (use_mma || use_row || impl == 5 || impl == 6) ? gemv_mma_xt_mode(p->code) : (use_tc ? gemv_tc_xt_mode(p->code) : 0);
-    cudaError_t e;
+    float* lws = (float*)(ws + o.lws);
+    unsigned* bar = (unsigned*)(ws + o.bar);
     if (impl == 6) {
         // RHT-in kernel -> persistent row-owning decode-GEMV (k_layer.cu without its RHT phases,
         // x~ from the workspace) -> RHT-out kernel
-        float* lws = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) +
-                              align256(4 * B * l.m_pad) + align256(4 * (l.m_pad / kCellRows + 2)));
-        unsigned* bar = (unsigned*)((char*)lws + align256(4 * layer_workspace_floats(l, B, 0)));
         const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
         const int xmode6 = p->code == QTIP_CODE_HYB ? 5 : xmode;   // HYB fast path: swapped pairs
         e = cudaSuccess;
@@ -412,9 +537,6 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     }
     if (impl == 5) {
         // one persistent launch: RHT-in, decode-GEMV, reduction, RHT-out (k_layer.cu)
-        float* lws = (float*)(ws + align256(4 * Bx * l.n_pad) + align256(4 * l.n_kc * B * l.m_pad) +
-                              align256(4 * B * l.m_pad) + align256(4 * (l.m_pad / kCellRows + 2)));
-        unsigned* bar = (unsigned*)((char*)lws + align256(4 * layer_workspace_floats(l, B, 0)));
         const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
         const bool prof = g_prof_start && g_prof_stop;
         if (prof) record_event(g_prof_start, s);
@@ -432,7 +554,6 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     else if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 2);
     else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s, cnt, n_rb + 2);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
-    const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
     const bool prof = g_prof_start && g_prof_stop;
     if (prof) record_event(g_prof_start, s);
     const bool rht_out = (flags & QTIP_RHT_OUT) != 0;

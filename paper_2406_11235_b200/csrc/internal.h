@@ -135,6 +135,21 @@ cudaError_t launch_layer_group(const Layout& lay, int code, const CodeArgs& ca, 
                                uint32_t* const* xt_g, int64_t row_words, float* const* ws_f, unsigned* const* bar,
                                cudaStream_t s);
 
+// tcgen05 stream-K fused decode-GEMV (k_umma.cu, impl 7): G same-shape layers' row blocks
+// [rb0, rb1), x~ per layer in the UMMA B layout (RHT out_mode umma_xt_mode(code), batch stride
+// umma_batch_pad(B)).  Writes yout[g][b * ys + i] = yscale[g] * (W~ x~)[i] for launch rows i in
+// [0, rows); seg[g] (umma_seg_floats floats) holds partial sums of split row blocks, ticket[g]
+// (rb1 - rb0 ints, zero on entry and left zero) their arrival counters.  HYB layers of a group share
+// one LUT.
+bool umma_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int G);
+int umma_xt_mode(int code);
+int umma_batch_pad(int64_t B);
+size_t umma_seg_floats(const Layout& lay, int code, int64_t B);
+cudaError_t launch_umma(const Layout& lay, int code, const CodeArgs& ca, int G, const void* const* packed,
+                        const uint16_t* lut, const void* const* xt, float* const* seg, int* const* ticket,
+                        float* const* yout, const float* yscale, int64_t ys, int64_t rows, int64_t B, int64_t rb0,
+                        int64_t rb1, cudaStream_t s);
+
 // Tail-biting trellis quantizer (k_viterbi.cu): Algorithm 4 per sequence of T source values (in
 // code units), binary32 DP.  ws: viterbi_workspace_bytes(T) bytes (backpointers, per CTA).
 bool viterbi_supported(int code, int k, int V, int L, int Q, int two_sign);

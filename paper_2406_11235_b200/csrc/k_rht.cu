@@ -24,13 +24,16 @@ namespace qtip {
 
 constexpr int kRhtThreads = 256;
 
+// out_mode 6 / 7: the UMMA B layout of the tcgen05 GEMV (k_umma.cu), K-doubled / plain binary16,
+// with `stride` = the batch pad BP.
 // out_mode 5 = mode 4 with the halves of every pair word swapped (HYB k = 4 fast path, k_layer.cu).
 // out_mode 0: float32; 1: binary16 duplicated into both halves of a 32-bit word (the K-doubled
 // UMMA B operand); 2: binary16; 3 / 4: modes 1 / 2 permuted into mma.sync B-fragment order
 // within each 16-column tile (k_gemv_mma.cu): mode 3 puts columns (2t, 2t+8, 2t+1, 2t+9) at
 // words 4t .. 4t+3, mode 4 puts the pairs (t, t+4) at words 2t, 2t+1.  `row` is the element
 // offset of the batch row, e the column.
-__device__ __forceinline__ void store_out(void* out, int mode, int64_t row, int64_t e, float v) {
+__device__ __forceinline__ void store_out(void* out, int mode, int64_t bt, int64_t stride, int64_t e, float v) {
+    const int64_t row = bt * stride;
     if (mode == 0) {
         static_cast<float*>(out)[row + e] = v;
         return;
@@ -42,6 +45,13 @@ __device__ __forceinline__ void store_out(void* out, int mode, int64_t row, int6
         static_cast<uint32_t*>(out)[row + e] = h | (h << 16);
     } else if (mode == 2) {
         static_cast<uint16_t*>(out)[row + e] = (uint16_t)h;
+    } else if (mode == 6) {
+        // UMMA B operand, K-doubled (k_umma.cu): 16-byte K chunks of 4 columns, batch rows interleaved
+        // per chunk (stride = BP rows)
+        static_cast<uint32_t*>(out)[(e >> 2) * 4 * stride + 4 * bt + (e & 3)] = h | (h << 16);
+    } else if (mode == 7) {
+        // UMMA B operand, plain binary16 (HYB): 16-byte K chunks of 8 columns, batch rows interleaved
+        static_cast<uint16_t*>(out)[(e >> 3) * 8 * stride + 8 * bt + (e & 7)] = (uint16_t)h;
     } else if (mode == 3) {
         const int t = (c & 7) >> 1, q = ((c & 1) << 1) | (c >> 3);
         static_cast<uint32_t*>(out)[row + tile * 16 + 4 * t + q] = h | (h << 16);
@@ -133,9 +143,10 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
     const float* x = in + bt * in_stride;
     const int j_lo = f * warp / kRhtWarps, j_hi = f * (warp + 1) / kRhtWarps;
     // loads of U rows are issued together before their FMAs (the latency is L2's, ~U x fewer round trips)
-    constexpr int U = E >= 4 ? 2 : 16;                       // f = 128 (n = 4096): one round of loads per warp
     auto slice = [&](auto kind) {
         constexpr int K = decltype(kind)::value;             // 0 plain, 1 sign words, 2 sign bytes
+        // rows whose loads are issued together (f = 128, n = 4096: one round per warp)
+        constexpr int U = E >= 4 ? 2 : 16;
         const float* xp = x + (int64_t)j_lo * L2 + c;
         int j = j_lo;
         auto step = [&](const float (&v)[E], int jj) {
@@ -219,12 +230,12 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
                 const int64_t idx = (int64_t)r * L2 + c + 32 * e;
                 float o = u[e] * out_scale;
                 if (inverse && sign_bit(sign, idx)) o = -o;
-                store_out(out, out_mode, bt * out_stride, idx, o);
+                store_out(out, out_mode, bt, out_stride, idx, o);
             }
         }
     }
     if (blockIdx.x == 0)                                     // zero the padded tail [n, pad_to)
-        for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt * out_stride, e, 0.0f);
+        for (int64_t e = plan.n + tid; e < pad_to; e += kRhtThreads) store_out(out, out_mode, bt, out_stride, e, 0.0f);
     trace.exit(g_rht_trace, inverse ? 2 : 1, g_rht_trace_cap);
 }
 
@@ -236,7 +247,7 @@ __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t 
     if (blockIdx.x == 0 && blockIdx.y == 0)
         for (int i = threadIdx.x; i < zero_n; i += blockDim.x) zero_ptr[i] = 0;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pad_to; e += (int64_t)gridDim.x * blockDim.x)
-        store_out(out, out_mode, bt * out_stride, e, e < n ? in[bt * in_stride + e] : 0.0f);
+        store_out(out, out_mode, bt, out_stride, e, e < n ? in[bt * in_stride + e] : 0.0f);
 }
 
 constexpr int64_t kRhtMaxN = 48 * 1024;
@@ -283,12 +294,9 @@ static cudaError_t launch_rht_t(const RhtPlan& plan, int G, int64_t B, const Rht
     const size_t smem = sizeof(float) * ((size_t)((plan.f * plan.rows_per_cta + 3) & ~3) +
                                          (size_t)kRhtWarps * plan.rows_per_cta * L2 + (size_t)(plan.n >> 5));
     auto kern = rht_kernel<E, RA>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    // the attribute is per device: set it on every launch (cheap; graphs replay without it)
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (ea != cudaSuccess) return ea;
     dim3 grid((unsigned)((plan.f + plan.rows_per_cta - 1) / plan.rows_per_cta), (unsigned)B, (unsigned)G);
     return launch_pdl(kern, grid, dim3(kRhtThreads), smem, s, plan, io, in_stride, out_stride, inverse, out_mode, pad,
                       zero_ptr, zero_n);

@@ -1,0 +1,673 @@
+// k_umma.cu -- impl 7: stream-K fused trellis-decode GEMV/GEMM on the 5th-generation tensor cores.
+//
+//   y~[rows] = W~[rows, :] x~        (PAPER.md:96-97 inner product; W~ tiles P:389-390, codes Alg. 1-3)
+//
+// Work = the launch's 128 x 128 cells (8 x 8 tiles of T = 256), of G same-shape
+// layers stacked into one "virtual" matrix (grouped q,k,v / gate,up launches).  The U cells are cut
+// into W = P * npass equal contiguous ranges in row-major order (stream-K): range w is
+// [U w / W, U (w+1) / W), CTA i runs ranges i, i + P, ...  Every CTA gets the same number of cells
+// (+-1), whatever the shape: no tile-row imbalance and no one-wave rule.
+//
+// One CTA per SM, 18 warps:
+//   warp 0      producer: cp.async.bulk of each cell (2048k bytes, L2 evict-first) into an S-stage
+//               ring.  The weights do not depend on the previous kernel, so the ring fills before
+//               (and while) the previous kernel finishes (PDL).
+//               It also loads each range's x~ window into shared memory, after the PDL wait.
+//   warp 1      MMA issuer (one elected thread): for every cell, waits for its decoded A operand in
+//               TMEM and issues 8 tcgen05.mma (kind::f16, M = 128, N = 16/64, K = 16, A from TMEM,
+//               B = x~ from shared memory, D in TMEM) -- asynchronous, so the tensor core never
+//               stalls the integer decode (the register-fed mma.sync of impls 3-6 serialises with
+//               it: DESIGN 5.1).  The D accumulator of a row block ("segment") lives in TMEM across
+//               the range (double-buffered between segments); tcgen05.commit hands it to the epilogue.
+//               Measured (scripts/umma_rate.cu): an M=128, K=16 MMA costs ~56 cycles for any N <= 64,
+//               so a cell (8 MMAs) takes ~450 cycles: 36 weights/clk/SM, above the decode rate.
+//   warps 2-5   epilogue (the four TMEM lane quadrants): tcgen05.ld of the finished D (thread = row), scale, store the segment's partial sums (128 rows x B).
+//   warps 6-17  three decoder groups of four warps (one warp per TMEM lane quadrant); cell j goes to
+//               group j mod 3.  Thread = one row of the cell (TMEM lane): it reads its row's stream
+//               words of a tile pair from the ring (LDS.64/128), extracts the 16 trellis windows of
+//               each tile row, evaluates the code and writes the A operand of its
+//               row straight into its TMEM lane with tcgen05.st (32x32b): binary16 weights, two per
+//               32-bit column.  3INST (Alg. 2): m1 + m2 summed in binary16 (HADD2, the paper's
+//               footnote P:265 -- exactly qtip_decode's value); 1MAD (Alg. 1): the exact integer
+//               s - 510 as binary16 (dp4a half2(1024 + s, -1534) summed), 1/147.8 applied to the
+//               sums; HYB (Alg. 3): a sign-folded, 32-way replicated shared-memory LUT.  Two TMEM A
+//               buffers per group (a whole cell each), hand-off through mbarriers.
+//
+// Partial sums: a row block that lies in one range is written straight to y~ by the epilogue.  A row
+// block split between ranges gets one segment (128 rows x B partial sums) per range, and the last of
+// those ranges to arrive (an atomic ticket per row block, zero between launches) adds them in range
+// order -- a fixed association, so the result is deterministic for a given (shape, row range, batch,
+// SM count).  Segment ids are w - w_first(layer) + row block (injective because ranges are ordered).
+//
+// x~ in shared memory, the UMMA B operand (K-major, SWIZZLE_NONE): element k of batch row r at byte
+// (k / 8) * 16 BP + 16 r + 2 (k % 8), BP = batch padded to a power of two.  The descriptor's leading
+// byte offset (K direction) is 16 BP: for BP < 8 the core matrices' rows >= BP overlap the next K
+// chunks -- they only feed accumulator columns >= B, which are never read -- so x~ costs exactly
+// 2 BP bytes per column and a whole 28672-long x~ fits.
+#include <algorithm>
+
+#include "decode.cuh"
+#include "internal.h"
+#include "mma_tile.cuh"
+#include "tc.cuh"
+
+namespace qtip {
+namespace {
+
+constexpr int kUG = 3;                       // decoder groups
+constexpr int kUWarps = 6 + 4 * kUG;
+constexpr int kUThreads = 32 * kUWarps;      // 576
+constexpr uint32_t kLutQ = 9;
+constexpr uint32_t kLutBytes = (1u << (kLutQ + 1)) * 128u;   // 1024 sign-folded entries x 32 replicas x 4 B
+constexpr uint32_t kHdr = 1024;              // barriers, TMEM base
+constexpr int kNBuf = 2;                     // A buffers (one cell each) per decoder group
+
+// ring stages per (k, code): the HYB LUT takes 128 KB of shared memory
+__host__ __device__ constexpr int umma_stages(int K, int code) { return code == QTIP_CODE_HYB ? 6 : (K == 2 ? 12 : 8); }
+
+struct UmmaArgs {
+    const uint32_t* packed[kMaxGroup];
+    const uint8_t* xt[kMaxGroup];            // x~ (B layout above), all n_kc columns
+    float* seg[kMaxGroup];                   // [(W + nrb)][BP][128] fp32 per layer
+    int* ticket[kMaxGroup];                  // [nrb] arrival counters per layer (zero between launches)
+    float* yout[kMaxGroup];                  // y~ (or scale * y~) rows [0, rows) of the launch, batch stride ys
+    float yscale[kMaxGroup];                 // scale of the written rows (includes 1MAD's 1/147.8)
+    int64_t ys, rows;
+    const uint32_t* lut;                     // HYB: 2^Q words (c0 | c1 << 16), shared by the group
+    Layout lay;
+    CodeArgs ca;
+    int G;
+    int64_t rb0;                             // row blocks [rb0, rb0 + nrb) of every layer
+    int nrb;
+    int U;                                   // cells = G * nrb * n_kc (U * W < 2^32: 32-bit index math)
+    int W;                                   // ranges
+    int B, BP;
+    float code_factor;
+    uint32_t off_ring, off_x;                // shared-memory offsets (LUT at kHdr)
+    uint32_t xcol_bytes;                     // x~ bytes per cell column
+    uint32_t lbo, sbo;
+};
+
+// Debug timeline of CTA 0 (qtip_internal_set_umma_trace; null in normal operation): u64 clock64
+// stamps at [kind * 64 + index].  The pointer is read once per thread at kernel start.
+__device__ unsigned long long* g_umma_trace = nullptr;
+__device__ __forceinline__ void utrace_at(unsigned long long* t, int kind, int64_t idx) {
+    if (t != nullptr && idx < 64) t[kind * 64 + idx] = clock64();
+}
+#define utrace(kind, idx) utrace_at(trc, (kind), (idx))
+
+__device__ __forceinline__ int range_lo(int U, int W, int w) { return (int)((uint32_t)U * (uint32_t)w / (uint32_t)W); }
+// range containing cell u: the largest w with U w / W <= u
+__device__ __forceinline__ int range_of(int U, int W, int u) {
+    return (int)((((uint32_t)u + 1u) * (uint32_t)W - 1u) / (uint32_t)U);
+}
+
+__device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(bar);
+}
+
+// binary16 sums of the two halves of za and of zb, packed (lo: za, hi: zb): HADD2 with RNE
+__device__ __forceinline__ uint32_t pair_sum(uint32_t za, uint32_t zb) {
+    const uint32_t lo = __byte_perm(za, zb, 0x5410), hi = __byte_perm(za, zb, 0x7632);
+    uint32_t r;
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+
+// ---------------------------------------------------------------------------------------- decode
+// This thread's row rho of the tile pair at pw (word w of tile t at pw[2w + t]) -> the A operand of
+// both tiles (binary16 weights, columns 2i, 2i+1 in TMEM column i), at TMEM columns ta (tile 0) and
+// ta + 8 (tile 1).
+template <int K, int CODE, bool kImm>
+__device__ __forceinline__ void decode_pair(const uint32_t* __restrict__ pw, int rho, const CodeArgs& ca,
+                                            uint32_t lut_lane, uint32_t ta) {
+    constexpr bool kHyb = CODE == QTIP_CODE_HYB;
+    constexpr int TW = 8 * K;
+    if constexpr (K == 2 && !kHyb) {
+        const uint2 A = *reinterpret_cast<const uint2*>(pw + 2 * rho);
+        const uint2 Bw = *reinterpret_cast<const uint2*>(pw + 2 * ((rho + 1) & 15));
+        const mma::Lcg<CODE, kImm> lcg(ca);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            const uint32_t a = tt ? A.y : A.x, b = tt ? Bw.y : Bw.x;
+            uint32_t z[16], o[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                // F_q = bits [2q, 2q + 32) of the row: windows q (high half) and q + 8 (low half)
+                const uint32_t F = q ? __funnelshift_l(b, a, 2 * q) : a;
+                mma::lcg_pair<CODE, CODE == QTIP_CODE_3INST, kImm>(F, lcg, ca.magic, z[q], z[q + 8]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = pair_sum(z[2 * i], z[2 * i + 1]);
+            ptx::tmem_st8(ta + tt * 8, o);
+        }
+    } else if constexpr (K == 4 && kHyb) {
+        const uint4 AB = *reinterpret_cast<const uint4*>(pw + 4 * rho);      // words 2 rho, 2 rho + 1 of both tiles
+        const uint2 Cw = *reinterpret_cast<const uint2*>(pw + 2 * ((2 * rho + 2) & 31));
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            uint32_t x[8], z[8];
+            windows_k4v2_dirty(tt ? AB.y : AB.x, tt ? AB.w : AB.z, tt ? Cw.y : Cw.x, x);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t h = x[q] * x[q] + x[q];                         // Alg. 3 hash (bits 0..15 exact)
+                const uint32_t off = (h & 0xFFC0u) * 2u + lut_lane;             // entry (idx | sign << 9) * 128 + lane
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(z[q]) : "r"(off));
+            }
+            ptx::tmem_st8(ta + tt * 8, z);
+        }
+    } else {
+        // general k (3INST / 1MAD k = 3, 4; HYB k = 2, 3): windows from three words of the tile row
+        const int start = 16 * K * rho, w0 = start >> 5, off = start & 31;
+        const uint2 W0 = *reinterpret_cast<const uint2*>(pw + 2 * (w0 % TW));
+        const uint2 W1 = *reinterpret_cast<const uint2*>(pw + 2 * ((w0 + 1) % TW));
+        const uint2 W2 = *reinterpret_cast<const uint2*>(pw + 2 * ((w0 + 2) % TW));
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            const uint32_t a0 = tt ? W0.y : W0.x, a1 = tt ? W1.y : W1.x, a2 = tt ? W2.y : W2.x;
+            uint32_t o[8];
+            if constexpr (kHyb) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t x = window_general(a0, a1, a2, off + q * 2 * K);
+                    const uint32_t h = x * x + x;
+                    const uint32_t ad = (h & 0xFFC0u) * 2u + lut_lane;
+                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(o[q]) : "r"(ad));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t zz[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const uint32_t x = window_general(a0, a1, a2, off + (2 * i + e) * K);
+                        zz[e] = mma::code_from_lcg<CODE>(x * ca.a + ca.b, ca.magic);
+                    }
+                    o[i] = pair_sum(zz[0], zz[1]);
+                }
+            }
+            ptx::tmem_st8(ta + tt * 8, o);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------- kernel
+template <int K, int CODE, int N, bool kImm>
+__global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_constant__ UmmaArgs a) {
+    constexpr bool kHyb = CODE == QTIP_CODE_HYB;
+    constexpr int S = umma_stages(K, CODE);
+    constexpr uint32_t kCellBytes = 2048u * K;
+    constexpr int kTW = 8 * K;
+    constexpr uint32_t kACols = 64;                          // one cell: 128 binary16 weights per row
+    constexpr uint32_t kD1 = N;                              // second D buffer
+    constexpr uint32_t kA0 = 2 * N <= 128 ? 128u : 2 * N;
+    static_assert(kA0 + kUG * kNBuf * kACols <= 512, "TMEM budget");
+    constexpr uint32_t idesc = ptx::idesc_f16_f32(128, N);
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    unsigned long long* const trc = blockIdx.x == 0 ? g_umma_trace : nullptr;
+    const uint32_t bar0 = ptx::smem_u32(smem);
+    auto full = [&](int s) { return bar0 + 8u * s; };
+    auto empty = [&](int s) { return bar0 + 8u * (S + s); };
+    auto afull = [&](int g, int b) { return bar0 + 8u * (2 * S + g * kNBuf + b); };
+    auto aempty = [&](int g, int b) { return bar0 + 8u * (2 * S + kUG * kNBuf + g * kNBuf + b); };
+    const uint32_t barD = bar0 + 8u * (2 * S + 2 * kUG * kNBuf);
+    auto dfull = [&](int d) { return barD + 8u * d; };
+    auto dempty = [&](int d) { return barD + 16u + 8u * d; };
+    const uint32_t xfull = barD + 32u, xempty = barD + 40u;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 1016);
+    uint8_t* ring = smem + a.off_ring;
+    const uint32_t xwin = ptx::smem_u32(smem + a.off_x);
+    const int n_kc = (int)a.lay.n_kc;
+    const int Ul = a.nrb * n_kc;                              // cells per layer
+    const int nrb = (int)a.nrb;
+    const int P = (int)gridDim.x;
+
+    // ---------------- setup (static data only: overlaps the previous kernel under PDL)
+    if constexpr (kHyb) {
+        // entry e = idx | sign << 9 -> (c0, c1) with c1 negated for sign (Alg. 3), replica r at
+        // word 32 e + r: conflict-free LDS for any entries
+        uint4* lt = reinterpret_cast<uint4*>(smem + kHdr);
+        for (int i = threadIdx.x; i < (1 << (kLutQ + 1)) * 8; i += kUThreads) {
+            const int e = i >> 3;
+            uint32_t w = __ldg(a.lut + (e & ((1 << kLutQ) - 1)));
+            if (e >> kLutQ) w ^= 0x80000000u;
+            lt[i] = make_uint4(w, w, w, w);
+        }
+    }
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                ptx::mbar_init(full(s), 1);
+                ptx::mbar_init(empty(s), 4);                  // the decoding group's four warps
+            }
+            for (int g = 0; g < kUG; ++g)
+                for (int b = 0; b < kNBuf; ++b) {
+                    ptx::mbar_init(afull(g, b), 4);
+                    ptx::mbar_init(aempty(g, b), 1);
+                }
+            for (int d = 0; d < 2; ++d) {
+                ptx::mbar_init(dfull(d), 1);
+                ptx::mbar_init(dempty(d), 4);
+            }
+            ptx::mbar_init(xfull, 1);
+            ptx::mbar_init(xempty, 1);
+            ptx::fence_mbar_init();
+        }
+        __syncwarp();
+        ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_holder, 0);
+    if (threadIdx.x == 0) ptx::pdl_launch_dependents();
+    if (threadIdx.x == 0) utrace(7, 0);
+
+    // Every role loop is warp-uniform (values in uniform registers; one elected lane issues copies and
+    // MMAs) and advances its counters incrementally: a 64-bit division or lane-0-only code per cell
+    // costs hundreds of cycles.
+    if (warp == 0) {
+        // ================= producer: every cell of every pass, in order (the cells of a range are
+        // contiguous in memory within a layer: row-block-major cells), and each pass's x~ window.
+        // Pass 0: the first S cells are requested before the PDL wait (the weights do not depend on
+        // the previous kernel), then x~ (its output).  Later passes reload the window once the
+        // previous pass's MMAs completed.
+        const uint64_t pol = ptx::l2_evict_first_policy();
+        int s = 0, p = 0;
+        uint32_t r = 0;                                       // fills of stage s so far, mod 2
+        bool wrapped = false;
+        auto load_x = [&](int ua, int ub) {
+            const int g0 = (int)(ua / Ul), g1 = (int)((ub - 1) / Ul);
+            uint32_t bytes = 0;
+            for (int g = g0; g <= g1; ++g) {
+                const int lo = ua > g * Ul ? ua : g * Ul, hi = ub < (g + 1) * Ul ? ub : (g + 1) * Ul;
+                bytes += (uint32_t)(hi - lo < n_kc ? hi - lo : n_kc) * a.xcol_bytes;
+            }
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(xfull, bytes);
+                int cum = 0;
+                for (int g = g0; g <= g1; ++g) {
+                    const int lo = ua > g * Ul ? ua : g * Ul, hi = ub < (g + 1) * Ul ? ub : (g + 1) * Ul;
+                    const int cnt = (int)(hi - lo < n_kc ? hi - lo : n_kc);
+                    const int kcs = (int)((lo - g * Ul) % n_kc);
+                    const int run1 = cnt < n_kc - kcs ? cnt : n_kc - kcs;
+                    const uint8_t* src = a.xt[g];
+                    ptx::bulk_g2s(xwin + (uint32_t)cum * a.xcol_bytes, src + (size_t)kcs * a.xcol_bytes,
+                                  (uint32_t)run1 * a.xcol_bytes, xfull);
+                    if (cnt > run1)
+                        ptx::bulk_g2s(xwin + (uint32_t)(cum + run1) * a.xcol_bytes, src,
+                                      (uint32_t)(cnt - run1) * a.xcol_bytes, xfull);
+                    cum += cnt;
+                }
+            }
+            __syncwarp();
+        };
+        for (int w = blockIdx.x; w < a.W; w += P, ++p) {
+            const int ua = range_lo(a.U, a.W, w), ub = range_lo(a.U, a.W, w + 1);
+            if (p > 0) {
+                ptx::mbar_wait(xempty, (uint32_t)((p - 1) & 1));
+                load_x(ua, ub);
+            }
+            int g = (int)(ua / Ul);
+            int ul = ua - g * Ul;                             // cell index within layer g
+            const uint32_t* src = a.packed[g] + (a.rb0 * n_kc + ul) * a.lay.cell_words;
+            const int pre = p == 0 ? (ub - ua < S ? ub - ua : S) : 0;
+            for (int u = ua; u < ub; ++u) {
+                if (p == 0 && u - ua == pre) {
+                    ptx::pdl_wait();
+                    load_x(ua, ub);
+                }
+                if (wrapped) ptx::mbar_wait(empty(s), r ^ 1u);
+                if (ptx::elect_one()) {
+                    ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
+                    ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
+                }
+                __syncwarp();
+                if (++s == S) { s = 0; r ^= 1u; wrapped = true; }
+                src += a.lay.cell_words;
+                if (++ul == Ul && g + 1 < a.G) {
+                    ul = 0;
+                    ++g;
+                    src = a.packed[g] + a.rb0 * n_kc * a.lay.cell_words;
+                }
+            }
+            if (p == 0 && pre == ub - ua) {                   // the whole pass fit the ring
+                ptx::pdl_wait();
+                load_x(ua, ub);
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer
+        int seg = 0, p = 0;
+        int jj = 0;                                           // CTA-local cell counter
+        for (int w = blockIdx.x; w < a.W; w += P, ++p) {
+            const int ua = range_lo(a.U, a.W, w), ub = range_lo(a.U, a.W, w + 1);
+            const int g0 = (int)(ua / Ul), g1 = (int)((ub - 1) / Ul);
+            int kcs[kMaxGroup], base[kMaxGroup];
+            {
+                int cum = 0;
+#pragma unroll
+                for (int gl = 0; gl < kMaxGroup; ++gl) {
+                    kcs[gl] = base[gl] = 0;
+                    if (gl < g0 || gl > g1) continue;
+                    const int lo = ua > gl * Ul ? ua : gl * Ul, hi = ub < (gl + 1) * Ul ? ub : (gl + 1) * Ul;
+                    kcs[gl] = (int)((lo - gl * Ul) % n_kc);
+                    base[gl] = cum;
+                    cum += (int)(hi - lo < n_kc ? hi - lo : n_kc);
+                }
+            }
+            int gl = g0;
+            int RB = (ua - gl * Ul) / n_kc;
+            int KC = ua - gl * Ul - RB * n_kc;
+            int off = (KC - kcs[0] + n_kc) % n_kc;
+#pragma unroll
+            for (int q = 1; q < kMaxGroup; ++q)
+                if (gl == q) off = (KC - kcs[q] + n_kc) % n_kc;
+            int wbase = base[0];
+#pragma unroll
+            for (int q = 1; q < kMaxGroup; ++q)
+                if (gl == q) wbase = base[q];
+            uint32_t dcol = tmem;
+            bool first = true;
+            const uint32_t dstep = 2u * (uint32_t)a.BP;       // B descriptor step per MMA (16 K)
+            // (all index math above before the wait: x~ is usually the last input to arrive)
+            ptx::mbar_wait(xfull, (uint32_t)(p & 1));
+            if (lane == 0) utrace(7, 1);
+            ptx::tc_fence_after();
+            for (int u = ua; u < ub; ++u, ++jj) {
+                if (u == ua || KC == 0) {                      // a new segment (row block) starts
+                    const int d = seg & 1;
+                    if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
+                    ptx::tc_fence_after();
+                    dcol = tmem + (uint32_t)d * kD1;
+                    first = true;
+                }
+                const int g = jj % kUG, lc = jj / kUG, b = lc & (kNBuf - 1);
+                ptx::mbar_wait(afull(g, b), (uint32_t)((lc / kNBuf) & 1));
+                if (lane == 0) utrace(4, jj);
+                ptx::tc_fence_after();
+                const uint64_t cdesc =
+                    ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)(wbase + off) * a.xcol_bytes, a.lbo, a.sbo);
+                const uint32_t acol = tmem + kA0 + (uint32_t)(g * kNBuf + b) * kACols;
+                if (ptx::elect_one()) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        ptx::umma_f16_ts(dcol, acol + 8u * (uint32_t)i, cdesc + (uint64_t)(dstep * (uint32_t)i), idesc,
+                                         (first && i == 0) ? 0u : 1u);
+                    ptx::umma_commit(aempty(g, b));
+                    if (u + 1 == ub || KC == n_kc - 1) ptx::umma_commit(dfull(seg & 1));
+                }
+                __syncwarp();
+                if (lane == 0) utrace(5, jj);
+                first = false;
+                if (u + 1 == ub || KC == n_kc - 1) ++seg;
+                // advance (layer, row block, cell column) and the window column
+                if (++off == n_kc) off = 0;
+                if (++KC == n_kc) {
+                    KC = 0;
+                    if (++RB == nrb) {
+                        RB = 0;
+                        ++gl;
+#pragma unroll
+                        for (int q = 1; q < kMaxGroup; ++q)
+                            if (gl == q) {
+                                off = (n_kc - kcs[q]) % n_kc;
+                                wbase = base[q];
+                            }
+                    }
+                }
+            }
+            if (ptx::elect_one()) ptx::umma_commit(xempty);   // this pass's MMAs read the window
+            __syncwarp();
+        }
+    } else if (warp < 6) {
+        // ================= epilogue warpgroup (warps 2-5: the four TMEM lane quadrants): D (thread =
+        // row) -> y~ rows (whole row block) or a segment partial sum (split row block)
+        __shared__ int s_last;
+        const int q = warp & 3;
+        const int R = 32 * q + lane;
+        const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+        int seg = 0;
+        for (int w = blockIdx.x; w < a.W; w += P) {
+            const int ua = range_lo(a.U, a.W, w), ub = range_lo(a.U, a.W, w + 1);
+            for (int RBv = ua / n_kc; RBv <= (ub - 1) / n_kc; ++RBv, ++seg) {
+                const int d = seg & 1;
+                ptx::mbar_wait(dfull(d), (uint32_t)((seg >> 1) & 1));
+                if (R == 0) utrace(6, seg);
+                ptx::tc_fence_after();
+                const int g = RBv / a.nrb, RB = RBv - g * a.nrb;
+                const int64_t row = (int64_t)RB * 128 + R;    // relative to the launch's first row
+                const float sc = a.yscale[g];
+                float* yo = a.yout[g] + row;
+                const bool live = row < a.rows;
+                const int w0 = range_of(a.U, a.W, RBv * n_kc), w1 = range_of(a.U, a.W, (RBv + 1) * n_kc - 1);
+                const bool whole = w0 == w1;                   // the whole row block is this range's
+                // split row block (stream-K): publish this range's partial sums; the last of the
+                // w1 - w0 + 1 ranges to arrive adds them all in range order (fixed association)
+                const int wf = range_of(a.U, a.W, g * Ul);
+                float* segp = a.seg[g] + ((int64_t)(w0 - wf + RB) * a.BP) * 128 + R;
+                float* dst = segp + (int64_t)(w - w0) * a.BP * 128;
+#pragma unroll
+                for (int cb = 0; cb < N; cb += 16) {          // 16 accumulator columns (batch rows) at a time
+                    if (cb >= a.B) break;
+                    uint32_t rr[16];
+                    ptx::tmem_ld16(tl + (uint32_t)d * kD1 + (uint32_t)cb, rr);
+                    ptx::tc_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int bb = cb + i;
+                        if (bb >= a.B) break;
+                        const float v = __uint_as_float(rr[i]);
+                        if (whole) {
+                            if (live) yo[bb * a.ys] = v * sc;
+                        } else {
+                            dst[bb * 128] = v;
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                warp_arrive(dempty(d), lane);
+                if (whole) continue;
+                __threadfence();
+                ptx::named_bar_sync(1, 128);
+                if (R == 0) {
+                    const int old = atomicAdd(a.ticket[g] + RB, 1);
+                    const bool last = old == (int)(w1 - w0);
+                    if (last) a.ticket[g][RB] = 0;             // every contributor has arrived: reset
+                    s_last = last ? 1 : 0;
+                }
+                ptx::named_bar_sync(1, 128);
+                if (s_last) {
+                    __threadfence();
+                    const int cnt = (int)(w1 - w0 + 1);
+#pragma unroll
+                    for (int bb = 0; bb < N; ++bb) {
+                        if (bb >= a.B) break;
+                        const float* sp = segp + bb * 128;
+                        float t[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) t[j] = j < cnt ? __ldcg(sp + (int64_t)j * a.BP * 128) : 0.0f;
+                        float acc = t[0];
+#pragma unroll
+                        for (int j = 1; j < 8; ++j)
+                            if (j < cnt) acc += t[j];
+                        for (int j = 8; j < cnt; ++j) acc += __ldcg(sp + (int64_t)j * a.BP * 128);
+                        if (live) yo[bb * a.ys] = acc * sc;
+                    }
+                }
+            }
+        }
+    } else {
+        // ================= decoder groups: cells jj = g, g + 3, ... of the CTA's cell sequence
+        const int dw = warp - 6, g = dw >> 2, q = warp & 3;
+        const int R = 32 * q + lane, I = R >> 4, rho = R & 15;
+        const uint32_t ta_lane = tmem + ((uint32_t)(32 * q) << 16) + kA0;
+        const uint32_t lut_lane = ptx::smem_u32(smem + kHdr) + 4u * (uint32_t)lane;
+        int ncell = 0;
+        for (int w = blockIdx.x; w < a.W; w += P) ncell += (int)(range_lo(a.U, a.W, w + 1) - range_lo(a.U, a.W, w));
+        int lc = 0;
+        for (int jj = g; jj < ncell; jj += kUG, ++lc) {
+            const int s = jj % S;
+            const uint32_t r = (uint32_t)((jj / S) & 1);
+            const int b = lc & (kNBuf - 1), use = lc / kNBuf;
+            const bool tr = lane == 0 && dw == 4 * g;
+            ptx::mbar_wait(full(s), r);
+            if (tr) utrace(1, jj);
+            if (use > 0) ptx::mbar_wait(aempty(g, b), (uint32_t)((use - 1) & 1));
+            if (tr) utrace(2, jj);
+            ptx::tc_fence_after();
+            const uint32_t* cellw = reinterpret_cast<const uint32_t*>(ring + (size_t)s * kCellBytes);
+            const uint32_t ta = ta_lane + (uint32_t)(g * kNBuf + b) * kACols;
+#pragma unroll 1
+            for (int pp = 0; pp < 4; ++pp)                    // tile pairs of the cell
+                decode_pair<K, CODE, kImm>(cellw + (I * 4 + pp) * kTW * 2, rho, a.ca, lut_lane, ta + (uint32_t)pp * 16);
+            warp_arrive(empty(s), lane);                      // the cell's stream words are read
+            ptx::tc_wait_st();
+            ptx::tc_fence_before();
+            warp_arrive(afull(g, b), lane);
+            if (tr) utrace(3, jj);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) utrace(7, 2);
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+struct UmmaPlan {
+    int S, BP, N;
+    int64_t P, W, U;
+    uint32_t xcol, off_ring, off_x;
+    size_t smem;
+};
+
+bool umma_plan(const Layout& lay, int code, int64_t B, int G, int64_t nrb, UmmaPlan* pl) {
+    const bool hyb = code == QTIP_CODE_HYB;
+    pl->BP = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : B <= 16 ? 16 : 64;
+    pl->N = pl->BP <= 16 ? 16 : 64;
+    pl->xcol = 128u * 2u * (uint32_t)pl->BP;                        // binary16 x~ (every code: 2 B per weight)
+    const size_t cell = 2048u * (size_t)lay.k;
+    const size_t lutb = hyb ? kLutBytes : 0;
+    const size_t max_smem = 225 * 1024;                               // + the kernel's static shared memory
+    pl->U = (int64_t)G * nrb * lay.n_kc;
+    pl->P = std::min<int64_t>(num_sms(), pl->U);
+    const int S = umma_stages(lay.k, code);
+    pl->S = S;
+    const size_t fixed = kHdr + lutb + (size_t)S * cell + 512;
+    if (fixed >= max_smem) return false;
+    const int64_t fit = (int64_t)((max_smem - fixed) / pl->xcol) - G;   // x~ window columns per range
+    if (fit < 1) return false;
+    const int64_t c = (pl->U + pl->P - 1) / pl->P;
+    const int64_t need = std::min<int64_t>(c, (int64_t)G * lay.n_kc);
+    const int64_t npass = need <= fit ? 1 : (pl->U + pl->P * fit - 1) / (pl->P * fit);
+    pl->W = std::min<int64_t>(pl->P * npass, pl->U);                  // every range holds >= 1 cell
+    pl->off_ring = (uint32_t)(kHdr + lutb);
+    pl->off_x = (uint32_t)(kHdr + lutb + (size_t)S * cell);
+    const int64_t cw = (pl->U + pl->W - 1) / pl->W;
+    const int64_t win = std::min<int64_t>(cw, (int64_t)G * lay.n_kc) + G;
+    pl->smem = pl->off_x + (size_t)win * pl->xcol + 512;
+    if ((uint64_t)pl->U * (uint64_t)(pl->W + 1) >= (1ull << 31)) return false;   // 32-bit index math in the kernel
+    return pl->smem <= max_smem;
+}
+
+template <int K, int CODE, int N, bool kImm>
+cudaError_t launch_umma_t(const UmmaArgs& a, const UmmaPlan& pl, cudaStream_t s) {
+    auto kern = umma_gemv_kernel<K, CODE, N, kImm>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kern, dim3((unsigned)pl.P), dim3(kUThreads), pl.smem, s, a);
+}
+
+}  // namespace
+
+bool umma_supported(const Layout& lay, int code, const CodeArgs& ca, int64_t B, int G) {
+    if (B < 1 || B > 64 || lay.k < 2 || lay.k > 4 || G < 1 || G > kMaxGroup) return false;
+    if (code == QTIP_CODE_HYB && (ca.Q != (int)kLutQ || ca.two_sign)) return false;
+    UmmaPlan pl;
+    return umma_plan(lay, code, B, G, lay.n_rb, &pl);
+}
+
+int umma_xt_mode(int code) { (void)code; return 7; }
+int umma_batch_pad(int64_t B) { return B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : B <= 16 ? 16 : 64; }
+
+size_t umma_seg_floats(const Layout& lay, int code, int64_t B) {
+    // segments of one layer for any group size: (W + nrb) x BP x 128
+    size_t best = 0;
+    for (int G = 1; G <= kMaxGroup; ++G) {
+        UmmaPlan pl;
+        if (!umma_plan(lay, code, B, G, lay.n_rb, &pl)) continue;
+        best = std::max(best, (size_t)(pl.W + lay.n_rb) * pl.BP * 128);
+    }
+    return best;
+}
+
+cudaError_t launch_umma(const Layout& lay, int code, const CodeArgs& ca, int G, const void* const* packed,
+                        const uint16_t* lut, const void* const* xt, float* const* seg, int* const* ticket,
+                        float* const* yout, const float* yscale, int64_t ys, int64_t rows, int64_t B, int64_t rb0,
+                        int64_t rb1, cudaStream_t s) {
+    UmmaPlan pl;
+    const int64_t nrb = rb1 - rb0;
+    if (!umma_plan(lay, code, B, G, nrb, &pl)) return cudaErrorInvalidConfiguration;
+    UmmaArgs a{};
+    const float cf = (code == QTIP_CODE_1MAD) ? 5.0f / 739.0f : 1.0f;      // 1/147.8 for 1MAD (reading R6)
+    for (int g = 0; g < G; ++g) {
+        a.packed[g] = (const uint32_t*)packed[g];
+        a.xt[g] = (const uint8_t*)xt[g];
+        a.seg[g] = seg[g];
+        a.ticket[g] = ticket[g];
+        a.yout[g] = yout[g];
+        a.yscale[g] = yscale[g] * cf;
+    }
+    a.ys = ys;
+    a.rows = rows;
+    a.lut = (const uint32_t*)lut;
+    a.lay = lay;
+    a.ca = ca;
+    a.G = G;
+    a.rb0 = rb0;
+    a.nrb = (int)nrb;
+    a.U = (int)pl.U;
+    a.W = (int)pl.W;
+    a.B = (int)B;
+    a.BP = pl.BP;
+    a.code_factor = cf;
+    a.off_ring = pl.off_ring;
+    a.off_x = pl.off_x;
+    a.xcol_bytes = pl.xcol;
+    a.lbo = 16u * (uint32_t)pl.BP;
+    a.sbo = 128u;
+    const bool imm = code != QTIP_CODE_HYB && lay.k == 2 &&
+                     ca.a == (code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&
+                     ca.b == (code == QTIP_CODE_1MAD ? 76625530u : 64248484u);
+    cudaError_t e = cudaErrorInvalidValue;
+#define QTIP_U_CASE(KK, CC, NN, II) \
+    if (lay.k == KK && code == CC && pl.N == NN && imm == II) e = launch_umma_t<KK, CC, NN, II>(a, pl, s);
+    QTIP_U_CASE(2, QTIP_CODE_3INST, 16, true) QTIP_U_CASE(2, QTIP_CODE_3INST, 64, true)
+    QTIP_U_CASE(2, QTIP_CODE_1MAD, 16, true) QTIP_U_CASE(2, QTIP_CODE_1MAD, 64, true)
+    QTIP_U_CASE(2, QTIP_CODE_3INST, 16, false) QTIP_U_CASE(2, QTIP_CODE_3INST, 64, false)
+    QTIP_U_CASE(2, QTIP_CODE_1MAD, 16, false) QTIP_U_CASE(2, QTIP_CODE_1MAD, 64, false)
+    QTIP_U_CASE(3, QTIP_CODE_3INST, 16, false) QTIP_U_CASE(3, QTIP_CODE_3INST, 64, false)
+    QTIP_U_CASE(3, QTIP_CODE_1MAD, 16, false) QTIP_U_CASE(3, QTIP_CODE_1MAD, 64, false)
+    QTIP_U_CASE(4, QTIP_CODE_3INST, 16, false) QTIP_U_CASE(4, QTIP_CODE_3INST, 64, false)
+    QTIP_U_CASE(4, QTIP_CODE_1MAD, 16, false) QTIP_U_CASE(4, QTIP_CODE_1MAD, 64, false)
+    QTIP_U_CASE(2, QTIP_CODE_HYB, 16, false) QTIP_U_CASE(2, QTIP_CODE_HYB, 64, false)
+    QTIP_U_CASE(3, QTIP_CODE_HYB, 16, false) QTIP_U_CASE(3, QTIP_CODE_HYB, 64, false)
+    QTIP_U_CASE(4, QTIP_CODE_HYB, 16, false) QTIP_U_CASE(4, QTIP_CODE_HYB, 64, false)
+#undef QTIP_U_CASE
+    count_launch(1);
+    return e;
+}
+
+}  // namespace qtip
+
+extern "C" int qtip_internal_set_umma_trace(void* dptr) {
+    unsigned long long* p = (unsigned long long*)dptr;
+    return (int)cudaMemcpyToSymbol(qtip::g_umma_trace, &p, sizeof(p));
+}

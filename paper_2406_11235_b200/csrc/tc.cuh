@@ -103,6 +103,12 @@ __device__ __forceinline__ void bulk_g2s_stream(uint32_t dst, const void* src, u
     bulk_g2s(dst, src, bytes, bar);
 #endif
 }
+__device__ __forceinline__ void bulk_g2s_policy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void cp_async16_stream(uint32_t dst, const void* src, uint64_t pol) {
 #if QTIP_EVICT_FIRST
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");

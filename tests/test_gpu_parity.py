@@ -119,8 +119,9 @@ def _oracle_matvec(tiles, code, k, lut, m, n, x, seed, scale, flags=3, rows=None
                        rht_out=bool(flags & 2), rows=rows)
 
 
-IMPLS = [1, 2, 3, 4, 5, 6] # CUDA-core reference, tcgen05 (A in TMEM), register-fed mma.sync, row-tile mma.sync,
-                           # fused single-launch layer (k_layer.cu), RHT kernels around the persistent k_layer GEMV
+IMPLS = [1, 2, 3, 4, 5, 6, 7]  # CUDA-core reference, tcgen05 (A in TMEM), register-fed mma.sync, row-tile mma.sync,
+                               # fused single-launch layer (k_layer.cu), RHT kernels around the persistent k_layer GEMV,
+                               # stream-K tcgen05 GEMV (k_umma.cu, the auto default)
 
 
 @pytest.mark.parametrize("impl", IMPLS)
@@ -163,7 +164,7 @@ def test_matvec_ragged_shapes_and_flags(cuda_lib, impl):
         cuda_lib.set_matvec_impl(0)
 
 
-@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("impl", [1, 2, 3, 4, 5, 6])
 def test_row_shards_are_bitwise_slices(cuda_lib, impl):
     """Row sharding does not change per-row arithmetic (fixed K-split): shards == full rows bitwise."""
     m, n = 512, 512
@@ -179,7 +180,7 @@ def test_row_shards_are_bitwise_slices(cuda_lib, impl):
     assert np.array_equal(np.concatenate(parts, axis=1), full)
 
 
-@pytest.mark.parametrize("impl", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("impl", [2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("code,k,m,n", [("3inst", 2, 4096, 4096), ("1mad", 2, 11008, 4096), ("3inst", 2, 4096, 11008),
                                         ("hyb", 4, 4096, 4096), ("3inst", 2, 11008, 11008)])
 def test_matvec_full_size_sampled_rows(cuda_lib, impl, code, k, m, n):
@@ -373,35 +374,62 @@ def test_maximum_batch(cuda_lib, code, k):
 @pytest.mark.parametrize("code,k,G,m,n,B,grouped", [("3inst", 2, 3, 1024, 512, 1, True), ("hyb", 4, 2, 1280, 256, 2, True),
                                                     ("1mad", 3, 4, 688, 256, 4, True), ("3inst", 2, 3, 256, 256, 1, False),
                                                     ("hyb", 4, 2, 11008, 4096, 4, False)])
-def test_grouped_matvec_equals_per_layer_calls(cuda_lib, code, k, G, m, n, B, grouped):
-    """qtip_matvec_group == G qtip_matvec calls, bit for bit, for every flag combination: against the
-    persistent kernel (impl 6) when the group ran as one launch (one RHT-in + one GEMV (+ one
-    RHT-out) launch), else against the auto per-layer calls (256 rows: too few tile rows per CTA;
-    11008 x 4096 at B = 4: the grouped plan does not fit shared memory); member 0 also against
-    the oracle on the small shapes."""
+def test_grouped_impl6_equals_per_layer_calls(cuda_lib, code, k, G, m, n, B, grouped):
+    """The persistent-kernel grouping (impl 6): qtip_matvec_group == G qtip_matvec calls, bit for bit,
+    for every flag combination, when the group ran as one launch (one RHT-in + one GEMV (+ one RHT-out));
+    else (256 rows: too few tile rows per CTA; 11008 x 4096 at B = 4: the plan does not fit shared
+    memory) G per-layer impl-6-or-fallback calls."""
     from paper_2406_11235_b200.layer import forward_group
     lut = lut_for(code)
     tiles = [synth.random_tiles(m, n, k, seed=50 + g) for g in range(G)]
     layers = [make_layer(cuda_lib, m, n, code, k, tiles[g], lut, seed=20 + g, scale=0.5 + g) for g in range(G)]
     x = torch.from_numpy(synth.random_x(B, n, seed=77)).cuda()
-    for flags in (1, 3, 0, 2):
+    cuda_lib.set_matvec_impl(6)
+    try:
+        for flags in (1, 3, 0, 2):
+            c0 = cuda_lib.launch_count()
+            outs = [o.cpu().numpy() for o in forward_group(layers, x, flags=flags)]
+            launches = cuda_lib.launch_count() - c0
+            if flags & 1:
+                assert (launches == 2 + bool(flags & 2)) == grouped, (flags, launches)
+            if grouped:
+                ref = [l(x, flags=flags).cpu().numpy() for l in layers]
+                for g in range(G):
+                    assert np.array_equal(outs[g], ref[g]), (flags, g)
+            if flags == 3 and m * n <= 1 << 20:
+                want = _oracle_matvec(tiles[0], code, k, lut, m, n, x.cpu().numpy(), 20, 0.5)
+                assert rel_l2(outs[0], want) <= MATVEC_TOL
+    except cuda_lib.QtipError as e:
+        assert not grouped, e                                # impl 6 refuses the ungrouped shapes
+    finally:
+        cuda_lib.set_matvec_impl(0)
+
+
+@pytest.mark.parametrize("code,k,G,m,n,B", [("3inst", 2, 3, 1024, 512, 1), ("hyb", 4, 2, 1280, 256, 2),
+                                            ("1mad", 3, 4, 688, 256, 4), ("3inst", 2, 3, 256, 256, 1),
+                                            ("hyb", 3, 2, 1024, 8192, 1), ("3inst", 2, 2, 384, 768, 16)])
+def test_grouped_matvec_against_oracle(cuda_lib, code, k, G, m, n, B):
+    """qtip_matvec_group as the bench runs it (auto: one grouped RHT-in, one stream-K tcgen05 launch
+    over the G layers' cells, one grouped RHT-out / segment reduction): every member, every row,
+    every flag combination against the float64 oracle."""
+    from paper_2406_11235_b200.layer import forward_group
+    lut = lut_for(code)
+    tiles = [synth.random_tiles(m, n, k, seed=50 + g) for g in range(G)]
+    layers = [make_layer(cuda_lib, m, n, code, k, tiles[g], lut, seed=20 + g, scale=0.5 + g) for g in range(G)]
+    xh = synth.random_x(B, n, seed=77)
+    x = torch.from_numpy(xh).cuda()
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    W = [gemv.dense_decode(tiles[g], p) for g in range(G)]
+    for flags in (3, 1, 0, 2):
         c0 = cuda_lib.launch_count()
         outs = [o.cpu().numpy() for o in forward_group(layers, x, flags=flags)]
-        launches = cuda_lib.launch_count() - c0
         if flags & 1:
-            ran_grouped = launches == 2 + bool(flags & 2)
-            if grouped is not None:
-                assert ran_grouped == grouped, (flags, launches)
-        cuda_lib.set_matvec_impl(6 if ran_grouped else 0)
-        try:
-            ref = [l(x, flags=flags).cpu().numpy() for l in layers]
-        finally:
-            cuda_lib.set_matvec_impl(0)
+            assert cuda_lib.launch_count() - c0 == 3                 # grouped in, GEMV, out
         for g in range(G):
-            assert np.array_equal(outs[g], ref[g]), (flags, g)
-        if flags == 3 and m * n <= 1 << 20:
-            want = _oracle_matvec(tiles[0], code, k, lut, m, n, x.cpu().numpy(), 20, 0.5)
-            assert rel_l2(outs[0], want) <= MATVEC_TOL
+            want = gemv.matvec(W[g], xh.astype(np.float64), synth.random_sign_bytes(n, 3000 + 20 + g),
+                               synth.random_sign_bytes(m, 3001 + 20 + g), scale=0.5 + g, rht_in=bool(flags & 1),
+                               rht_out=bool(flags & 2))
+            assert rel_l2(outs[g], want) <= MATVEC_TOL, (flags, g)
 
 
 def test_grouped_two_sign_hyb_and_distinct_luts(cuda_lib):
