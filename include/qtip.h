@@ -111,9 +111,19 @@ qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* 
  *     scale * W~ x~.
  *     A partial row range (row_begin > 0 or row_end < m) requires RHT_OUT off; row_begin
  *     and row_end must be multiples of 128 (or row_end == m).
- *   d_workspace: DEVICE scratch of >= qtip_matvec_workspace_bytes(...) bytes, 256-B aligned.
- *   Deterministic: the K-split and reduction order depend only on (m, n), not on timing,
- *   so a row shard reproduces the full call's rows bit for bit. */
+ *   d_workspace: DEVICE scratch of >= qtip_matvec_workspace_bytes(...) bytes, 256-B aligned,
+ *     zero-filled before its first use.  It holds x~, partial sums and the kernels' arrival
+ *     counters / grid-barrier words: every call leaves those counters zero (or, for the grid
+ *     barriers, in a consistent state), and every call that transforms x (no QTIP_XT_READY)
+ *     clears them before the GEMV starts, so only a QTIP_XT_READY call on never-used scratch
+ *     needs the zero fill.  Not shared between concurrent calls.
+ *   Deterministic: the reduction order depends on (p, m, n, B, row range, SM count), never on
+ *     timing -- repeated calls are bitwise identical.  Kernels 1-6 split K by (m, n) only, so a
+ *     row shard reproduces the full call's rows bit for bit; the stream-K kernel (7) cuts the
+ *     launch's own cells into equal ranges, so a shard's rows agree with the full call only to
+ *     fp32 rounding (both within the 1e-3 parity bar).
+ *   The kernel choice (auto) depends on (p, m, n, B) only, not on the row range, so QTIP_XT_READY
+ *     reuses an x~ written by a call with any row range. */
 qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B,
                         const void* d_packed, const uint16_t* d_lut,
                         const uint8_t* d_sign_n, const uint8_t* d_sign_m, float scale,
@@ -179,10 +189,12 @@ qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T,
                                   size_t workspace_bytes, void* stream);
 
 /* Selects the matvec kernel: 0 = auto (the measured-fastest supported kernel), 1 = CUDA-core
- * reference kernel, 2 = tcgen05 kernel (A in TMEM), 3 = register-fed mma.sync kernel with
- * split-K over 128-column cells, 4 = row-tile mma.sync kernel (one CTA per 16 rows, B <= 4),
- * 5 = fused single-launch layer kernel (RHT-in, GEMV, RHT-out with in-kernel grid barriers),
- * 6 = RHT kernels around the persistent row-owning GEMV of 5 (HYB k = 4 auto choice).
+ * reference kernel, 2 = tcgen05 kernel (A in TMEM, per-cell split-K), 3 = register-fed mma.sync
+ * kernel with split-K over 128-column cells, 4 = row-tile mma.sync kernel (one CTA per 16 rows,
+ * B <= 4), 5 = fused single-launch layer kernel (RHT-in, GEMV, RHT-out with in-kernel grid
+ * barriers), 6 = RHT kernels around the persistent row-owning GEMV of 5, 7 = RHT kernels around the
+ * stream-K tcgen05 GEMV (k_umma.cu: decoded binary16 weights in TMEM, asynchronous UMMA, equal
+ * cell ranges per SM; auto for HYB at B <= 8 with >= 10 cells per SM).
  * Process-wide; for ablations and tests. */
 void qtip_set_matvec_impl(int impl);
 int qtip_get_matvec_impl(void);

@@ -317,12 +317,15 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
         // (or segment reduction) reading the partial-sum segments
         const int xmode = umma_xt_mode(p->code);
         const int64_t bp = umma_batch_pad(B);
+        int* tk0[kMaxGroup];                                       // the GEMV's row-block tickets: cleared here
+        for (int g = 0; g < G; ++g) tk0[g] = (int*)((char*)d_workspace[g] + o.cnt);
         if (!xready) {
             if (rin) {
                 e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, bp, 0, std::vector<float>(G, 1.0f).data(), s, xmode,
-                                     l.n_pad);
+                                     l.n_pad, tk0, (int)l.n_rb);
             } else {
-                for (int g = 0; g < G && e == cudaSuccess; ++g) e = launch_convert(d_x, n, n, B, xt[g], bp, xmode, l.n_pad, s);
+                for (int g = 0; g < G && e == cudaSuccess; ++g)
+                    e = launch_convert(d_x, n, n, B, xt[g], bp, xmode, l.n_pad, s, tk0[g], (int)l.n_rb);
             }
             if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group rht_in");
         }
@@ -375,12 +378,13 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
         ydst[g] = rout ? yt[g] : d_y[g];
         sc[g] = rout ? 1.0f : scale[g];
     }
-    if (!xready) {
+    if (!xready) {                                                // also clears the barrier / ticket words
         if (rin) {
             e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, l.n_pad, 0, std::vector<float>(G, 1.0f).data(), s,
-                                 xmode6, l.n_pad);
+                                 xmode6, l.n_pad, (int* const*)bar, 256);
         } else {
-            for (int g = 0; g < G && e == cudaSuccess; ++g) e = launch_convert(d_x, n, n, B, xt[g], l.n_pad, xmode6, l.n_pad, s);
+            for (int g = 0; g < G && e == cudaSuccess; ++g)
+                e = launch_convert(d_x, n, n, B, xt[g], l.n_pad, xmode6, l.n_pad, s, (int*)bar[g], 256);
         }
         if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec_group rht_in");
     }
@@ -517,9 +521,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
         const int xmode6 = p->code == QTIP_CODE_HYB ? 5 : xmode;   // HYB fast path: swapped pairs
         e = cudaSuccess;
-        if (!(flags & QTIP_XT_READY)) {
-            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode6, l.n_pad);
-            else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode6, l.n_pad, s);
+        if (!(flags & QTIP_XT_READY)) {                          // also clears the barrier / ticket words
+            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode6, l.n_pad, (int*)bar, 256);
+            else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode6, l.n_pad, s, (int*)bar, 256);
         }
         if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
         const bool prof = g_prof_start && g_prof_stop;
@@ -536,7 +540,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         return QTIP_OK;
     }
     if (impl == 5) {
-        // one persistent launch: RHT-in, decode-GEMV, reduction, RHT-out (k_layer.cu)
+        // one persistent launch: RHT-in, decode-GEMV, reduction, RHT-out (k_layer.cu); its grid-barrier
+        // and ticket words start from zero whatever the caller's workspace held
+        if ((e = cudaMemsetAsync(bar, 0, 1024, s)) != cudaSuccess) return cuda_fail(e, "qtip_matvec barrier words");
         const int64_t row_words = l.n_pad * ((xmode == 1 || xmode == 3) ? 4 : 2) / 4;
         const bool prof = g_prof_start && g_prof_stop;
         if (prof) record_event(g_prof_start, s);

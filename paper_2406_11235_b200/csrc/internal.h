@@ -33,6 +33,28 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Cooperative launch (the driver guarantees every CTA of the grid is co-resident, or refuses the
+// launch) for kernels that spin on grid-wide barriers / tickets (k_layer.cu): two such grids on
+// concurrent streams, or under MPS, could otherwise split the SMs and wait on each other.  PDL is
+// kept when enabled.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    prefer_max_smem((const void*)kern);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Hadamard factor tables (hadamard.cpp): n = b * 2^a; device +-1 table of H_b (or H_b^T), one
 // bit row per matrix row padded to 32-bit words (bit j of row i set <=> entry = -1), cached per device.
 bool hadamard_factor(int64_t n, int* b, int* a);
@@ -66,10 +88,12 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas = 128);
 cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, const float* in, int64_t in_stride,
                        void* out, int64_t out_stride, int inverse, float scale, cudaStream_t s, int out_mode = 0,
                        int64_t pad_to = 0, int* zero_ptr = nullptr, int zero_n = 0);
-// G transforms of the same plan in one launch (grid.z = g): sign[g], in[g], out[g], scale[g].
+// G transforms of the same plan in one launch (grid.z = g): sign[g], in[g], out[g], scale[g];
+// zero[g][0 .. zero_n) cleared after the PDL wait (the GEMVs' counters), when zero is given.
 cudaError_t launch_rht_group(const RhtPlan& plan, int G, int64_t B, const uint8_t* const* sign, const float* const* in,
                              int64_t in_stride, void* const* out, int64_t out_stride, int inverse, const float* scale,
-                             cudaStream_t s, int out_mode = 0, int64_t pad_to = 0);
+                             cudaStream_t s, int out_mode = 0, int64_t pad_to = 0, int* const* zero = nullptr,
+                             int zero_n = 0);
 // x (float32) -> out_mode encoding, zero padded to pad_to (used when RHT-in is off).
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
                            int out_mode, int64_t pad_to, cudaStream_t s, int* zero_ptr = nullptr, int zero_n = 0);

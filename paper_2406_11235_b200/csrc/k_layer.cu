@@ -882,7 +882,7 @@ cudaError_t launch_layer_t(LayerArgs a, size_t smem, cudaStream_t s) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kLThreads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;               // grid barrier needs co-residency
-    return launch_pdl(kern, dim3((unsigned)num_sms()), dim3(kLThreads), smem, s, a);
+    return launch_coop(kern, dim3((unsigned)num_sms()), dim3(kLThreads), smem, s, a);
 }
 
 size_t align128(size_t v) { return (v + 127) & ~(size_t)127; }

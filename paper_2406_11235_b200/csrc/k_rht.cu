@@ -78,6 +78,8 @@ struct RhtIO {
     const float* in[kMaxGroup];
     void* out[kMaxGroup];
     float out_scale[kMaxGroup];
+    int* zero[kMaxGroup];                                    // cleared after the PDL wait (the GEMV's counters)
+    int zero_n;
 };
 
 template <int E, int RA>
@@ -132,6 +134,8 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
     trace.waited(g_rht_trace);
     if (blockIdx.x == 0 && blockIdx.y == 0 && z == 0)
         for (int i = tid; i < zero_n; i += kRhtThreads) zero_ptr[i] = 0;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && io.zero[z])
+        for (int i = tid; i < io.zero_n; i += kRhtThreads) io.zero[z][i] = 0;
     __syncthreads();
 
     // slice sums: acc[q][e] = sum_{j in slice} D[r0 + ro RA + q][j] V[j][c + 32 e]
@@ -329,10 +333,12 @@ cudaError_t launch_rht(const RhtPlan& plan, int64_t B, const uint8_t* sign, cons
 
 cudaError_t launch_rht_group(const RhtPlan& plan, int G, int64_t B, const uint8_t* const* sign, const float* const* in,
                              int64_t in_stride, void* const* out, int64_t out_stride, int inverse, const float* scale,
-                             cudaStream_t s, int out_mode, int64_t pad_to) {
+                             cudaStream_t s, int out_mode, int64_t pad_to, int* const* zero, int zero_n) {
     if (G < 1 || G > kMaxGroup) return cudaErrorInvalidValue;
     RhtIO io{};
+    io.zero_n = zero ? zero_n : 0;
     for (int g = 0; g < G; ++g) {
+        io.zero[g] = zero ? zero[g] : nullptr;
         io.sign[g] = sign[g];
         io.in[g] = in[g];
         io.out[g] = out[g];

@@ -48,11 +48,12 @@ class QTIPLinear:
     # ------------------------------------------------------------------ compute
     def forward(self, x, out=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_OUT, rows=None, stream=None):
         """x: float32 CUDA (B, n) -> float32 (B, m) (or the row range of scale * W~ x~)."""
-        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous()
+        _check_io(x, (x.shape[0] if x.dim() == 2 else -1, self.n), self.device, "x")
         B = x.shape[0]
         r0, r1 = rows if rows is not None else (0, self.m)
         if out is None:
             out = torch.empty((B, r1 - r0), dtype=torch.float32, device=self.device)
+        _check_io(out, (B, r1 - r0), self.device, "out")
         if B == 0:                                  # empty batch: nothing to compute, no launch
             return out
         qtip.qtip_matvec(self.p, self.m, self.n, B, self.packed, self.lut, self.sign_n, self.sign_m, self.scale,
@@ -72,6 +73,16 @@ class QTIPLinear:
         return self.m * self.n * self.k // 8
 
 
+def _check_io(t, shape, device, name):
+    """The C ABI receives raw pointers: shapes, dtype, layout and device are checked here."""
+    if not (isinstance(t, torch.Tensor) and t.dtype == torch.float32 and t.is_cuda and t.is_contiguous()):
+        raise ValueError(f"{name}: a contiguous float32 CUDA tensor is required")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.device != device and not (device.index is None and t.device.type == device.type):
+        raise ValueError(f"{name}: on {t.device}, the layer is on {device}")
+
+
 _SIDE = {}
 
 
@@ -89,10 +100,14 @@ def forward_group(layers, x, outs=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_O
     for l in layers[1:]:
         if (l.m, l.n, l.code, l.k) != (l0.m, l0.n, l0.code, l0.k) or bytes(l.p) != bytes(l0.p):
             raise ValueError("forward_group: layers must share shape and QTIP parameters")
-    assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.shape[1] == l0.n
+    _check_io(x, (x.shape[0] if x.dim() == 2 else -1, l0.n), l0.device, "x")
     B = x.shape[0]
     if outs is None:
         outs = [torch.empty((B, l.m), dtype=torch.float32, device=l.device) for l in layers]
+    if len(outs) != len(layers):
+        raise ValueError("forward_group: one output per layer")
+    for l, o in zip(layers, outs):
+        _check_io(o, (B, l.m), l.device, "outs[]")
     if B == 0:                                      # empty batch: nothing to compute, no launch
         return outs
     if len(layers) > 1 and stream is None and not qtip.group_fused(l0.p, len(layers), l0.m, l0.n, B):

@@ -4,8 +4,9 @@ Each rank owns a contiguous range of output rows (a multiple of 128 = one cell r
 computes scale * W~[rows] x~ with qtip_matvec (RHT-in on the replicated x, RHT-out off),
 the shards are exchanged with one all-gather over NCCL (NVLink 5 / NVSwitch), and every
 rank applies the inverse output RHT y = S_m H_m^T y~ / sqrt(m) (it mixes all rows, so it
-cannot be split).  Per-row arithmetic is unchanged by sharding, so the gathered y~ equals
-the single-GPU y~ bit for bit.
+cannot be split).  With kernels 1-6 per-row arithmetic is unchanged by sharding (the gathered
+y~ equals the single-GPU y~ bit for bit); the stream-K kernel (7) partitions each shard's own
+cells, so there the agreement is to fp32 rounding (include/qtip.h).
 """
 import numpy as np
 

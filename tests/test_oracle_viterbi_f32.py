@@ -46,9 +46,38 @@ def test_f32_tailbite_batch_is_tail_biting():
     tab = (tab / tab.std()).astype(np.float32)
     S = np.random.default_rng(13).normal(size=(3, 32)).astype(np.float32)
     st, cost = viterbi.tailbite_encode_f32_batch(S, L, k, V, tab)
-    for w in st:
+    for w, c, s in zip(st, cost, S):
         # closure: the last state's bottom L-kV bits are the first state's top L-kV bits
         assert (int(w[0]) >> (k * V)) == (int(w[-1]) & ((1 << (L - k * V)) - 1))
-        bits = trellis.states_to_bits(w, L, k, V, tail_biting=True) if hasattr(trellis, "states_to_bits") else None
-        assert bits is None or len(bits) == k * V * len(w)
-    assert np.all(cost > 0)
+        assert trellis.is_walk(w, L, k, V, tail_biting=True)
+        # the reported cost is the squared error of the returned walk (binary32 rounding)
+        assert abs(c - _cost64(w, s.astype(np.float64), tab.astype(np.float64))) <= 1e-4 * c
+
+
+def test_f32_tailbite_batch_pinned_to_exact_optimum_and_f64_alg4():
+    """Algorithm 4 in binary32 (the GPU quantizer's reference, reading R17) against things other
+    than itself, on tiny trellises: the exact tail-biting optimum by brute force over every cyclic
+    bit string (its cost is a lower bound Alg. 4 meets or exceeds), the float64 Alg. 4
+    (pinned to Table 3 in test_oracle_viterbi.py) -- same walk whenever no two candidate costs lie
+    within binary32 rounding of each other -- and P:348's seam rule checked on the walks: the
+    constrained pass's first and last states share the overlap the rotated pass produced."""
+    rng = np.random.default_rng(17)
+    agree = 0
+    for trial in range(30):
+        L, k, V, T = 6, 2, 1, 8
+        tab = rng.normal(size=1 << L).astype(np.float32)
+        s = rng.normal(size=T).astype(np.float32)
+        st, cost = viterbi.tailbite_encode_f32_batch(s[None, :], L, k, V, tab)
+        st, cost = st[0], float(cost[0])
+        _, best = viterbi.brute_force(s.astype(np.float64), L, k, V, tab.astype(np.float64), tail_biting=True)
+        assert cost >= best * (1 - 1e-5) - 1e-6                              # never below the optimum
+        assert trellis.is_walk(st, L, k, V, tail_biting=True)
+        st64, c64 = viterbi.tailbite_encode(s.astype(np.float64), L, k, V, tab.astype(np.float64))
+        assert abs(cost - c64) <= 1e-4 * max(1.0, c64)
+        agree += int(np.array_equal(st, st64))
+        # seam rule: the overlap O is the rotated walk's state at 1-indexed group T/2 (reading R3)
+        srot = np.roll(s, T // 2)
+        rot, _ = viterbi.viterbi_f32(srot, L, k, V, tab)
+        O = int(rot[T // 2 - 1]) & ((1 << (L - k)) - 1)
+        assert (int(st[0]) >> k) == O and (int(st[-1]) & ((1 << (L - k)) - 1)) == O
+    assert agree >= 27
