@@ -147,6 +147,69 @@ def oracle_sample(m=2048, n=4096, code="3inst", k=2, reps=1):
     return nbytes, times
 
 
+def _oracle_rows_worker(job):
+    """One process of the all-cores oracle: decode a block of tile rows and form its rows of W~ x~."""
+    from threadpoolctl import threadpool_limits
+    from oracle import gemv
+    m, n, k, code, I0, I1, xt = job
+    tiles = synth.random_tiles(m, n, k, seed=1000)[I0:I1]
+    lut = synth.gaussian_lut(9) if code == "hyb" else None
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    with threadpool_limits(1):
+        return I0, xt @ gemv.dense_decode(tiles, p).T
+
+
+def oracle_sample_all_cores(m=2048, n=4096, code="3inst", k=2, procs=None):
+    """The same oracle computation split over all host cores (a process pool over tile-row blocks;
+    the RHTs stay on the parent).  Returns (bytes, seconds, processes)."""
+    import multiprocessing as mproc
+    from oracle import rht
+    procs = procs or os.cpu_count() or 1
+    x = synth.random_x(1, n).astype(np.float64)
+    sm, sn = synth.random_sign_bytes(m, 3001), synth.random_sign_bytes(n, 3000)
+    mt = m // 16
+    blocks = [(i * mt // procs, (i + 1) * mt // procs) for i in range(procs)]
+    with mproc.get_context("spawn").Pool(procs) as pool:
+        pool.map(_oracle_rows_worker, [(256, 256, k, code, 0, 16, np.zeros((1, 256)))] * procs)   # warm
+        t0 = time.perf_counter()
+        xt = rht.rht_forward(x, sn, n)
+        yt = np.zeros((1, m))
+        for I0, part in pool.map(_oracle_rows_worker, [(m, n, k, code, a, b, xt) for a, b in blocks if b > a]):
+            yt[:, 16 * I0:16 * I0 + part.shape[1]] = part
+        rht.rht_inverse(yt, sm, m)
+        dt = time.perf_counter() - t0
+    return m * n * k / 8, dt, procs
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(code, k):
+    """The oracle timed on this host: single thread (the reference arm's setting) and all cores, on a
+    2048 x 4096 sample of the workload's code; microseconds per layer extrapolated from the
+    per-weight time (decode dominates; the RHTs are < 3 %) for the C1-C3 shapes."""
+    nbytes, times = oracle_sample(2048, 4096, code, k, reps=2)
+    t1 = min(times)
+    nb_all, t_all, procs = oracle_sample_all_cores(2048, 4096, code, k)
+    per_w1, per_wN = t1 / (2048 * 4096), t_all / (2048 * 4096)
+    shapes = {"256x256": 256 * 256, "4096x4096": 4096 * 4096, "11008x4096": 11008 * 4096, "4096x11008": 4096 * 11008}
+    return {"value": round(nbytes / t1 / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"2 x one 2048x4096 {code} k={k} layer (decode + float64 RHT-in/GEMV/RHT-out), single thread "
+                      f"(best of 2); all-cores: the same layer split over a {procs}-process pool",
+            "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+            "all_cores": {"value": round(nb_all / t_all / 1e9, 5), "unit": "GB/s", "cores": procs},
+            "us_per_layer_1_core": {s: round(per_w1 * w * 1e6, 0) for s, w in shapes.items()},
+            "us_per_layer_all_cores": {s: round(per_wN * w * 1e6, 0) for s, w in shapes.items()}}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -185,9 +248,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N ranks with torchrun, or let "
+                         "bench.py relaunch itself)")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local} but only {torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # communicator lines (nRanks, NVLS / P2P transport) in the log; the JSON line stays last on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     qtip.load()
     qtip.set_matvec_impl(args.matvec_impl)
@@ -445,12 +516,96 @@ def run_ours(args):
     h2d = sum(x.numel() * 4 for x in xh.values())
     d2h = yh.numel() * 4
 
+    # ---- C4 (BASELINE configs[3]): the 70B layers 8192x28672 and 28672x8192, 3INST k=2, batch 1, row-
+    #      sharded over the ranks (all-gather of y~, replicated RHT-out); 4 distinct copies per shape in
+    #      the graph (4 x 58.7 MB > L2).  Plus the all-gather latency of the exchange step alone.
+    scaling_70b = None
+    if not args.no_70b:
+        scaling_70b = {"code": "3inst", "k": 2, "batch": 1, "ranks": world, "layers": {}}
+        for si, (m, n) in enumerate([(8192, 28672), (28672, 8192)]):
+            tiles = synth.random_tiles(m, n, 2, seed=1500 + si)
+            smb, snb = synth.random_sign_bytes(m, 3501 + si), synth.random_sign_bytes(n, 3500 + si)
+            copies = []
+            for c in range(4):
+                if world == 1:
+                    lay = QTIPLinear(m, n, code="3inst", k=2, device=dev)
+                    if c == 0:
+                        lay.load_tiles(tiles, smb, snb)
+                    else:
+                        lay.packed.copy_(copies[0].packed)
+                        lay.sign_m.copy_(copies[0].sign_m)
+                        lay.sign_n.copy_(copies[0].sign_n)
+                else:
+                    lay = ShardedQTIPLinear(m, n, rank, world, code="3inst", k=2, device=dev)
+                    if c == 0:
+                        lay.load_tiles(tiles, smb, snb)
+                    else:
+                        lay.local.packed.copy_(copies[0].local.packed)
+                        lay.local.sign_n.copy_(copies[0].local.sign_n)
+                        lay.sign_m.copy_(copies[0].sign_m)
+                copies.append(lay)
+            del tiles
+            xc = torch.from_numpy(synth.random_x(1, n, seed=2500 + si)).to(dev)
+            yc = [torch.empty((1, m), dtype=torch.float32, device=dev) for _ in copies]
+            loc = [(c if world == 1 else c.local) for c in copies]
+            yl = [torch.empty((1, t.m), dtype=torch.float32, device=dev) for t in loc]
+
+            def run_c4(gemv_only=False):
+                for c, lay in enumerate(copies):
+                    if gemv_only:
+                        loc[c].forward(xc, out=yl[c], flags=qtip.QTIP_RHT_IN | qtip.QTIP_XT_READY)
+                    elif world == 1:
+                        lay.forward(xc, out=yc[c])
+                    else:
+                        yc[c].copy_(lay.forward(xc))
+
+            times = {}
+            for mode in (False, True):
+                run_c4()
+                gc = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
+                    run_c4(mode)
+                    with torch.cuda.graph(gc, stream=s):
+                        run_c4(mode)
+                torch.cuda.current_stream().wait_stream(s)
+                for _ in range(3):
+                    gc.replay()
+                barrier()
+                c0_, c1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                c0_.record()
+                for _ in range(5):
+                    gc.replay()
+                c1_.record()
+                torch.cuda.synchronize()
+                times[mode] = max_over_ranks(1e3 * c0_.elapsed_time(c1_) / (5 * len(copies)))
+                del gc
+            scaling_70b["layers"][f"{m}x{n}"] = {
+                "us_per_layer": round(times[False], 3), "GBps": round(m * n / 4 / (times[False] * 1e-6) / 1e9, 1),
+                "gemv_only_us_max_over_ranks": round(times[True], 3),
+                "rank_rows": (copies[0].rows[1] - copies[0].rows[0]) if world > 1 else m}
+            del copies, loc
+        if world > 1:
+            lam = {}
+            for nbytes_ag in (32768, 114688):
+                per = nbytes_ag // 4 // world
+                send_t = torch.zeros(per, dtype=torch.float32, device=dev)
+                recv_t = torch.empty(per * world, dtype=torch.float32, device=dev)
+                for _ in range(10):
+                    dist.all_gather_into_tensor(recv_t, send_t)
+                barrier()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record()
+                for _ in range(100):
+                    dist.all_gather_into_tensor(recv_t, send_t)
+                a1.record()
+                torch.cuda.synchronize()
+                lam[str(nbytes_ag)] = round(max_over_ranks(1e3 * a0.elapsed_time(a1) / 100), 3)
+            scaling_70b["allgather_us"] = lam
+        torch.cuda.empty_cache()
+
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        nbytes, times = oracle_sample(2048, 4096, code, k, reps=3)
-        cpu = {"value": nbytes * len(times) / sum(times) / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"3 x one 2048x4096 {code} k={k} layer (decode + float64 RHT-in/GEMV/RHT-out), "
-                         f"single thread, host nproc={os.cpu_count()}"}
+        cpu = cpu_baseline(code, k)
 
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_sum = clk.summary()
@@ -475,24 +630,23 @@ def run_ours(args):
                        if args.workload == "llama2-7b" else "distinct weights per layer",
                        "matvec_impl": qtip.get_matvec_impl(),
                        "arith": "decoded weights and RHT'd x in binary16, fp32 accumulation"},
-            # 3INST k=2 is bound by integer decode arithmetic, not HBM: its peak is the
-            # ALU-pipe bound derived from the unit counts and the SM clock, the HBM fraction is kept
-            "roofline": {"bound": "alu" if alu_bound else "hbm", "achieved": round(gemv_gbs, 1),
-                         "peak": round(alu_peak, 1) if alu_bound else peak, "unit": "GB/s",
-                         "frac": round(gemv_gbs / (alu_peak if alu_bound else peak), 4),
+            # against the MEASURED HBM copy bandwidth (MEASURED_PEAKS.json): the metric is compressed
+            # bytes per second.  The integer-decode bounds of 3INST k=2 are context only.
+            "roofline": {"bound": "hbm", "achieved": round(gemv_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gemv_gbs / peak, 4),
                          "traffic": traffic(args.workload, code, k, qtip.get_matvec_impl()),
                          "kernel": "fused decode-GEMV launches of the step (grouped where the step groups), back-to-back graph",
-                         "peak_kind": ("derived: 32 weights/clk/SM on the ALU pipe (per weight 1/2 funnel shift + "
-                                       "1/2 shift + 1 LOP3 at 64 lanes/clk/SM) x SMs x SM clock x k/8 B of stream"
-                                       if alu_bound else peak_kind),
-                         "hbm_peak": peak, "hbm_frac": round(gemv_gbs / peak, 4),
+                         "peak_kind": peak_kind,
                          "us_per_layer": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3),
-                         # context: the measured decode-MMA loop ceiling of 3INST k=2
-                         # (scripts/decode_microbench.cu, 19.2 weights/clk/SM), the practical bound
-                         # below HBM for this code
+                         # context: the ALU-pipe bound of the 3INST k=2 decode (32 weights/clk/SM: per weight
+                         # 1/2 funnel shift + 1/2 shift + 1 LOP3 at 64 lanes/clk/SM) and the measured
+                         # decode + mma.sync loop ceiling (scripts/decode_microbench.cu, 19.2 weights/clk/SM)
+                         "alu_bound": (None if not alu_bound else {
+                             "GBps": round(alu_peak, 1), "frac": round(gemv_gbs / alu_peak, 4)}),
                          "decode_loop_ceiling": (None if (code, k) != ("3inst", 2) else {
                              "weights_per_clk_per_sm": 19.2, "GBps": round(19.2 * sm_count * clk_mhz * 1e6 * k / 8 / 1e9, 1),
                              "frac": round(gemv_gbs / (19.2 * sm_count * clk_mhz * 1e6 * k / 8 / 1e9), 4)})},
+            "scaling_70b": scaling_70b,
             "cpu_baseline": cpu,
             "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 5)},
@@ -502,6 +656,22 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def relaunch_multi_rank(args):
+    """`bench.py --gpus N` without torchrun: start N ranks on this node (torch.distributed.run, one
+    process per GPU, rendezvous on 127.0.0.1) -- or fail clearly when fewer GPUs are visible."""
+    import socket
+    import torch
+    ngpu = torch.cuda.device_count()
+    if ngpu < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {ngpu} CUDA device(s) visible")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -517,9 +687,12 @@ def main():
     ap.add_argument("--blocks", type=int, default=None)
     ap.add_argument("--matvec-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-70b", action="store_true", help="skip the C4 70B-layer block (scaling_70b)")
     ap.add_argument("--grouping", default="launch", choices=["streams", "launch", "serial"],
                     help="layers of a block that share an input: concurrent streams, one grouped launch, or serial")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_multi_rank(args)
     if args.impl == "reference":
         run_reference(args)
     else:

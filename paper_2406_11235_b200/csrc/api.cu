@@ -243,10 +243,12 @@ static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
     if (g_impl == 7) return true;
     // auto (measured, profiles/r2_*): the tcgen05 stream-K kernel wins for HYB at batch
     // 1-8 once every SM has >= 10 cells of the launch (q,k,v / gate,up groups and the 11008-wide
-    // layers); short single launches keep the row-tile kernel (fixed start-up + stream-K fix-up cost),
-    // and 3INST / 1MAD stay on the register-fed kernels (their decode, not the MMA, is the bound)
+    // layers); short single launches keep the row-tile kernel (fixed start-up + stream-K fix-up cost).
+    // For 3INST / 1MAD the decode (5 instructions per weight), not the MMA, bounds it: only the 70B
+    // layers (>= 40 cells per SM) gain (C4 8192 x 28672: 69.6 -> 66.7 us)
     const int64_t cells = (int64_t)G * l.n_rb * l.n_kc;
-    return p->code == QTIP_CODE_HYB && B <= 8 && cells >= 10 * (int64_t)num_sms();
+    const int64_t min_cells = (p->code == QTIP_CODE_HYB ? 10 : 40) * (int64_t)num_sms();
+    return B <= 8 && cells >= min_cells;
 }
 
 int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B) {
