@@ -154,6 +154,48 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
                               const uint8_t* const* d_sign_m, const float* scale, const float* d_x, float* const* d_y,
                               int flags, void* const* d_workspace, size_t workspace_bytes, void* stream);
 
+/* A CHAIN of dependent layers in one persistent launch (impl 8, k_chain.cu): a decode step of a
+ * model applies its linear layers in stages, each stage's layers reading one input that is the
+ * output of a layer of the previous stage (q, k, v -> o -> gate, up -> down -> next q, k, v):
+ *     stage 0:  d_y[l] = scale_l S_m H_m^T W~_l H_n S_n x
+ *     stage s:  the same with x := d_y[src_l], src_l a layer of stage s-1
+ * i.e. exactly the qtip_matvec calls (RHT in and out) made one after another, but with the weight
+ * stream and trellis decode of later layers overlapping the transforms and hand-offs of earlier
+ * ones (no kernel boundary between layers).
+ *   layers: HOST array in stage order; stage numbers 0, 1, 2, ... (consecutive, non-decreasing);
+ *     the layers of one stage share n and src; stage 0 has src = -1 (the external x); a stage
+ *     holds 1..4 layers; src's m must equal the reader's n.  d_packed (16-B aligned, qtip_pack
+ *     layout), d_sign_n / d_sign_m (as qtip_matvec) and d_y (DEVICE float32 [B][m], written by
+ *     every run) are the caller's and must stay valid while the plan is used.
+ *   p: as qtip_matvec with 2 <= k <= 4; HYB needs Q = 9, one-sign and d_lut (one table for every
+ *     layer of the chain).  B: 1..16.  m, n: multiples of 16 with a supported Hadamard order.
+ *   qtip_chain_plan_create validates, builds the device tables and allocates the plan's own device
+ *     memory (x~ / y~ / partial-sum buffers and counters, ~(n + 4m + 512 (P + m/128)) B bytes per
+ *     layer, P = SM count) on the current device; it synchronises the device once.  Errors:
+ *     QTIP_ERR_INVALID_PARAMS (structure), QTIP_ERR_SHAPE, QTIP_ERR_ALIGNMENT, QTIP_ERR_UNSUPPORTED
+ *     (batch, code, stage too large, shared memory), QTIP_ERR_CUDA.
+ *   qtip_chain_run: d_x DEVICE float32 [B][n of stage 0]; stream-ordered, graph-capturable (a
+ *     memset of the plan's counters, then one cooperative kernel).  One run at a time per plan.
+ *   Results: every layer's y within the qtip_matvec parity bar of the float64 definition applied
+ *     to that layer's actual input; deterministic for a given plan and SM count.
+ *   qtip_chain_plan_destroy frees the plan (NULL is a no-op). */
+typedef struct {
+    const void* d_packed;
+    const uint8_t* d_sign_n;
+    const uint8_t* d_sign_m;
+    float scale;
+    int64_t m, n;
+    float* d_y;
+    int32_t stage;
+    int32_t src;
+} qtip_chain_layer;
+typedef struct qtip_chain_plan qtip_chain_plan;
+qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const qtip_chain_layer* layers, int64_t B,
+                                   const uint16_t* d_lut, qtip_chain_plan** plan);
+qtip_status qtip_chain_run(qtip_chain_plan* plan, const float* d_x, void* stream);
+void qtip_chain_plan_destroy(qtip_chain_plan* plan);
+int32_t qtip_chain_plan_stages(const qtip_chain_plan* plan);
+
 /* Random Hadamard transform of B vectors of length n:
  *   inverse = 0:  out = H_n (S . in) / sqrt(n)
  *   inverse = 1:  out = S . (H_n^T in) / sqrt(n)

@@ -47,6 +47,11 @@ qtip_status check_shape(int64_t m, int64_t n) {
 }
 }  // namespace
 
+// Error / code-argument helpers for the other translation units' extern "C" entry points (k_chain.cu).
+qtip_status api_fail(qtip_status s, const char* msg) { return fail(s, msg); }
+qtip_status api_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+CodeArgs api_code_args(const qtip_params* p) { return code_args(p); }
+
 void count_launch(int n) { g_launches += (uint64_t)n; }
 
 bool g_pdl = true;

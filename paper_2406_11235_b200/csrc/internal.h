@@ -9,6 +9,11 @@ namespace qtip {
 
 void count_launch(int n);
 int num_sms();
+// api.cu's status / message helpers and code arguments, for entry points defined in other files.
+qtip_status api_fail(qtip_status s, const char* msg);
+qtip_status api_cuda_fail(cudaError_t e, const char* where);
+struct CodeArgs;
+CodeArgs api_code_args(const qtip_params* p);
 
 // Launch with programmatic dependent launch enabled (the kernel may start while its predecessor
 // on the stream drains; it must griddepcontrol.wait before reading the predecessor's output).

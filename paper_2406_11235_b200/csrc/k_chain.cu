@@ -1,0 +1,904 @@
+// k_chain.cu -- impl 8: a chain of dependent QTIP layers in ONE persistent tcgen05 launch.
+//
+//   stage 0:  y_l = scale_l S_m H_m^T W~_l H_n S_n x                (every layer l)
+//   stage s:  the same with x := y_src(s), src(s) a layer of stage s-1
+//
+// A decode step of a model is such a chain (q,k,v -> o -> gate,up -> down -> next block's q,k,v).
+// Per layer the GEMV itself only needs x~ at MMA time: the packed weights (the
+// only large traffic) and their trellis decode (Alg. 1-3) do not depend on the activations.  So a
+// single grid, one CTA per SM, streams and decodes the weights of ALL layers back to back -- the
+// producer and the decoders run ahead of the data into the next layers -- and only the MMAs wait
+// for each stage's x~.  The per-layer kernel boundaries of the separate RHT-in -> GEMV -> RHT-out
+// kernels (a PDL release after a full grid costs ~1.3 us) disappear; what is left
+// per stage transition is a flag hand-off and the transforms, overlapped with the next stage's
+// decode.
+//
+// Roles (18 warps, 576 threads):
+//   warp 0      producer: cp.async.bulk of every cell of the CTA's ranges of all stages into an
+//               S-stage ring (L2 evict-first).  Never waits on data.
+//   warp 1      MMA issuer: per stage waits for the x~ of the layers its range touches (xready
+//               counters in global memory), bulk-loads that x~ window into shared memory (double
+//               buffered by stage parity), then issues 8 tcgen05.mma (M = 128, N = 16, K = 16, A =
+//               decoded weights in TMEM, B = x~ in shared memory) per cell, as in k_umma.cu.
+//   warps 2-5   epilogue + transforms: D (TMEM) -> y~ rows or stream-K segments of split row
+//               blocks (last arriver adds them in range order), a done counter per layer; then
+//               this CTA's share of the stage transition's transforms:
+//                 Tout(l): y_l = scale S_m (H_m^T y~_l)/sqrt(m)   (user output, fp32)
+//                 Tin(l'): x~_l' = H_n (S_n y_src)/sqrt(n)         (binary16, UMMA B layout)
+//               each task waits on a counter (done / yready) and bumps one (yready / xready).
+//   warps 6-17  three decoder groups (thread = TMEM lane = row of a cell), udec::decode_pair.
+//
+// Transforms (reading R7: H_n = H_b (x) H_{2^a}).  With L2 = 2^a2 (a2 = a for a <= 5, 5 if 5 < a < 7,
+// else min(a, 12)) and the dense factor D = H_b (x) H_{2^(a-a2)} of order f = n / L2,
+//     (H v)[i L2 + c] = FWHT_L2( sum_j D[i][j] V[j][.] )[c],     V[j][c] = v[j L2 + c],
+// so a task owns R rows i of D and needs every V[j] once (read from L2) and no other task's
+// result.  L2 <= 32: lane c of an L2-lane group accumulates its rows and the FWHT runs in
+// shuffles; L2 >= 128: thread = column (mod 128), the lowest 5 FWHT levels in shuffles, the rest in
+// radix-8 passes over shared memory.  The inverse uses D^T (H_b^T: Paley-I is skew, reading R8).
+//
+// Deadlock freedom (every CTA resident: cooperative launch): each role walks the stages in order;
+// weights and decode never wait on data; a CTA's epilogue warps do E(s-1) then the transition-s
+// tasks (all Tout before all Tin on every CTA), Tout waits only on E(s-1) of all CTAs, Tin only on
+// Tout.  Shared-memory reuse: the x~ buffer of stage s-2 is the transition-s scratch... see the
+// barrier notes in the kernel.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+#include "umma_decode.cuh"
+
+namespace qtip {
+namespace {
+
+constexpr int kCG = 3;                        // decoder groups
+constexpr int kCWarps = 6 + 4 * kCG;
+constexpr int kCThreads = 32 * kCWarps;       // 576
+constexpr int kCNBuf = 2;                     // TMEM A buffers per decoder group
+constexpr uint32_t kCHdr = 1024;
+constexpr uint32_t kCLutQ = 9;
+constexpr uint32_t kCLutBytes = (1u << (kCLutQ + 1)) * 128u;
+constexpr int kMaxStageLayers = 4;
+constexpr int kXfThreads = 128;               // the epilogue warps
+
+struct Xform {
+    int n;          // transform length (m for the inverse, n for the forward)
+    int b, a1;      // D = H_b (x) H_{2^a1}
+    int L2;         // FWHT length done per row
+    int f;          // order of D (= b 2^a1), n = f L2
+    int R;          // rows of D per task
+    int ntask;
+};
+
+struct ChainLayerDev {
+    const uint32_t* packed;
+    const uint8_t* sign_n;
+    const uint8_t* sign_m;
+    const uint32_t* hb_n;      // H_b bit rows for the forward over n (nullptr if b = 1)
+    const uint32_t* hbt_m;     // H_b^T bit rows for the inverse over m (nullptr if b = 1)
+    float* y;                  // user output [B][m]
+    uint16_t* xt;              // x~ [n_pad / 8][BP][8] binary16 (RHT out_mode 7)
+    float* yt;                 // y~ [B][m_pad]
+    float* seg;                // stream-K segments [(P + n_rb)][BP][128]
+    int* ticket;               // [n_rb] arrivals (zero between launches)
+    float scale;
+    int m, n, n_rb, n_kc;
+    int src;                   // -1: the external x
+    int cum;                   // first cell in the stage's numbering
+    int wfirst;                // range (CTA) holding that cell
+    Xform out, in;
+};
+
+struct ChainStageDev {
+    int l0, nl, U, n_kc;
+    int rb_cum[kMaxStageLayers + 1];   // row-block prefix of the stage's layers
+};
+
+struct ChainArgs {
+    const ChainLayerDev* L;
+    const ChainStageDev* S;
+    int nstages, nlayers;
+    int* ctr;                  // done[nl] | yready[nl] | xready[nl]
+    const float* x;            // external input [B][n of stage 0]
+    const uint32_t* lut;       // HYB: 2^Q words (c0 | c1 << 16), shared by the chain
+    CodeArgs ca;
+    int B, BP;
+    uint32_t xcol_bytes, lbo, sbo;
+    uint32_t off_ring, off_x, xbuf_bytes;
+};
+
+__host__ __device__ constexpr int chain_stages(int K, int code) { return code == QTIP_CODE_HYB ? 6 : (K == 2 ? 12 : 8); }
+
+__device__ __forceinline__ int range_lo(int U, int W, int w) { return (int)((uint32_t)U * (uint32_t)w / (uint32_t)W); }
+__device__ __forceinline__ int range_of(int U, int W, int u) {
+    return (int)((((uint32_t)u + 1u) * (uint32_t)W - 1u) / (uint32_t)U);
+}
+__device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(bar);
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+    while (ld_acquire(p) < target) __nanosleep(32);
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// D[i][j] of a transform (sign as +-1.0f): H_b[i_b][j_b] (-1)^popcount(i_1 & j_1), i = i_b 2^a1 + i_1
+__device__ __forceinline__ float dsign(const uint32_t* __restrict__ hb, int b, int a1, int i, int j) {
+    const int ib = i >> a1, jb = j >> a1, m1 = (1 << a1) - 1;
+    uint32_t s = __popc((uint32_t)(i & j & m1)) & 1u;
+    if (b > 1) s ^= (__ldg(hb + (size_t)ib * ((b + 31) >> 5) + (jb >> 5)) >> (jb & 31)) & 1u;
+    return s ? -1.0f : 1.0f;
+}
+
+// One transform task on the 128 epilogue threads (tid 0..127, named barrier 1).  dir 0: x~ of
+// layer Ld from its input; dir 1: y of layer Ld from its y~.  sm: scratch (the idle x~ buffer).
+__device__ void run_xform(const ChainArgs& a, const ChainLayerDev& Ld, int dir, int part, float* sm, int tid) {
+    const Xform X = dir ? Ld.out : Ld.in;
+    const int L2 = X.L2, f = X.f;
+    const int r0 = part * X.R, R = min(X.R, f - r0);
+    const float* in;
+    int64_t in_stride;
+    const uint8_t* sg_in = nullptr;
+    if (dir == 0) {
+        in = Ld.src < 0 ? a.x : a.L[Ld.src].y;
+        in_stride = X.n;
+        sg_in = Ld.sign_n;
+    } else {
+        in = Ld.yt;
+        in_stride = (int64_t)Ld.n_rb * 128;
+    }
+    const uint32_t* hb = dir ? Ld.hbt_m : Ld.hb_n;
+    const float fac = dir ? Ld.scale * rsqrtf((float)X.n) : rsqrtf((float)X.n);
+    float* Dsm = sm;                                    // [R][f] +-1.0f
+    float* Z = sm + ((R * f + 31) & ~31);               // [R][L2] (L2 >= 128)
+    for (int e = tid; e < R * f; e += kXfThreads) Dsm[e] = dsign(hb, X.b, X.a1, r0 + e / f, e % f);
+    ptx::named_bar_sync(1, kXfThreads);
+    const int lane = tid & 31;
+    for (int bt = 0; bt < a.B; ++bt) {
+        const float* inb = in + bt * in_stride;
+        if (L2 <= 32) {
+            // lane group of L2 lanes = one row of D at a time; slot = tid / L2
+            const int c = tid & (L2 - 1), slot = tid / L2, nslot = kXfThreads / L2;
+            for (int rl0 = 0; rl0 < R; rl0 += 2 * nslot) {
+                const int ra = rl0 + slot, rb = rl0 + nslot + slot;
+                float za = 0.0f, zb = 0.0f;
+                const float* da = Dsm + (ra < R ? ra : 0) * f;
+                const float* db = Dsm + (rb < R ? rb : 0) * f;
+#pragma unroll 4
+                for (int j = 0; j < f; ++j) {
+                    const int e = j * L2 + c;
+                    float v = __ldcg(inb + e);
+                    if (sg_in) v = ((sg_in[e >> 3] >> (e & 7)) & 1u) ? -v : v;
+                    za = fmaf(da[j], v, za);
+                    zb = fmaf(db[j], v, zb);
+                }
+#pragma unroll
+                for (int s = 1; s < 32; s <<= 1) {
+                    if (s >= L2) break;
+                    const float oa = __shfl_xor_sync(0xffffffffu, za, s), ob = __shfl_xor_sync(0xffffffffu, zb, s);
+                    za = (lane & s) ? oa - za : za + oa;
+                    zb = (lane & s) ? ob - zb : zb + ob;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rl = h ? rb : ra;
+                    if (rl >= R) continue;
+                    const int e = (r0 + rl) * L2 + c;
+                    const float v = (h ? zb : za) * fac;
+                    if (dir == 0) {
+                        Ld.xt[(e >> 3) * 8 * a.BP + 8 * bt + (e & 7)] = __half_as_ushort(__float2half_rn(v));
+                    } else {
+                        Ld.y[(int64_t)bt * Ld.m + e] = ((Ld.sign_m[e >> 3] >> (e & 7)) & 1u) ? -v : v;
+                    }
+                }
+            }
+        } else {
+            // thread = column c (mod 128) of each row: accumulate, the 5 lane levels in shuffles
+            for (int idx = tid; idx < R * L2; idx += kXfThreads) {
+                const int rl = idx / L2, c = idx - rl * L2;
+                const float* d = Dsm + rl * f;
+                float z = 0.0f;
+#pragma unroll 4
+                for (int j = 0; j < f; ++j) {
+                    const int e = j * L2 + c;
+                    float v = __ldcg(inb + e);
+                    if (sg_in) v = ((sg_in[e >> 3] >> (e & 7)) & 1u) ? -v : v;
+                    z = fmaf(d[j], v, z);
+                }
+#pragma unroll
+                for (int s = 1; s < 32; s <<= 1) {
+                    const float o = __shfl_xor_sync(0xffffffffu, z, s);
+                    z = (lane & s) ? o - z : z + o;
+                }
+                Z[idx] = z;
+            }
+            // levels h = 32 .. L2/2 in radix-8 / 4 / 2 passes (conflict-free: consecutive g)
+            for (int h = 32; h < L2;) {
+                const int lv = (L2 / h >= 8) ? 3 : (L2 / h >= 4 ? 2 : 1);
+                const int r = 1 << lv;
+                ptx::named_bar_sync(1, kXfThreads);
+                const int ng = R * (L2 >> lv);
+                for (int g = tid; g < ng; g += kXfThreads) {
+                    const int rl = g / (L2 >> lv), q = g - rl * (L2 >> lv);
+                    float* zr = Z + rl * L2 + (q / h) * (h * r) + (q % h);
+                    float v[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k < r) v[k] = zr[k * h];
+#pragma unroll
+                    for (int hh = 1; hh < 8; hh <<= 1) {
+                        if (hh >= r) break;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if (k < r && !(k & hh)) {
+                                const float p0 = v[k], p1 = v[k + hh];
+                                v[k] = p0 + p1;
+                                v[k + hh] = p0 - p1;
+                            }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k < r) zr[k * h] = v[k];
+                }
+                h <<= lv;
+            }
+            ptx::named_bar_sync(1, kXfThreads);
+            for (int idx = tid; idx < R * L2; idx += kXfThreads) {
+                const int rl = idx / L2, c = idx - rl * L2;
+                const int e = (r0 + rl) * L2 + c;
+                const float v = Z[idx] * fac;
+                if (dir == 0) {
+                    Ld.xt[(e >> 3) * 8 * a.BP + 8 * bt + (e & 7)] = __half_as_ushort(__float2half_rn(v));
+                } else {
+                    Ld.y[(int64_t)bt * Ld.m + e] = ((Ld.sign_m[e >> 3] >> (e & 7)) & 1u) ? -v : v;
+                }
+            }
+            ptx::named_bar_sync(1, kXfThreads);       // Z is reused by the next batch row
+        }
+    }
+}
+
+template <int K, int CODE, bool kImm>
+__global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_constant__ ChainArgs a) {
+    constexpr bool kHyb = CODE == QTIP_CODE_HYB;
+    constexpr int S = chain_stages(K, CODE);
+    constexpr int N = 16;
+    constexpr uint32_t kCellBytes = 2048u * K;
+    constexpr int kTW = 8 * K;
+    constexpr uint32_t kACols = 64;
+    constexpr uint32_t kD1 = N;
+    constexpr uint32_t kA0 = 128;
+    static_assert(kA0 + kCG * kCNBuf * kACols <= 512, "TMEM budget");
+    constexpr uint32_t idesc = ptx::idesc_f16_f32(128, N);
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const uint32_t bar0 = ptx::smem_u32(smem);
+    auto full = [&](int s) { return bar0 + 8u * s; };
+    auto empty = [&](int s) { return bar0 + 8u * (S + s); };
+    auto afull = [&](int g, int b) { return bar0 + 8u * (2 * S + g * kCNBuf + b); };
+    auto aempty = [&](int g, int b) { return bar0 + 8u * (2 * S + kCG * kCNBuf + g * kCNBuf + b); };
+    const uint32_t barD = bar0 + 8u * (2 * S + 2 * kCG * kCNBuf);
+    auto dfull = [&](int d) { return barD + 8u * d; };
+    auto dempty = [&](int d) { return barD + 16u + 8u * d; };
+    auto xfull = [&](int b) { return barD + 32u + 8u * b; };      // x~ window b landed
+    auto xfree = [&](int b) { return barD + 48u + 8u * b; };      // MMAs reading window b done
+    // transitions done on this CTA (monotonic; an mbarrier's parity could alias when a CTA with
+    // empty ranges runs two transitions ahead of its MMA warp)
+    volatile int* s_tdone = reinterpret_cast<volatile int*>(smem + 1008);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 1016);
+    uint8_t* ring = smem + a.off_ring;
+    const int P = (int)gridDim.x;
+    const int cta = (int)blockIdx.x;
+    const int ns = a.nstages;
+    const ChainStageDev* __restrict__ Sd = a.S;
+    const ChainLayerDev* __restrict__ Lg = a.L;
+
+    if constexpr (kHyb) {
+        uint4* lt = reinterpret_cast<uint4*>(smem + kCHdr);
+        for (int i = threadIdx.x; i < (1 << (kCLutQ + 1)) * 8; i += kCThreads) {
+            const int e = i >> 3;
+            uint32_t w = __ldg(a.lut + (e & ((1 << kCLutQ) - 1)));
+            if (e >> kCLutQ) w ^= 0x80000000u;
+            lt[i] = make_uint4(w, w, w, w);
+        }
+    }
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                ptx::mbar_init(full(s), 1);
+                ptx::mbar_init(empty(s), 4);
+            }
+            for (int g = 0; g < kCG; ++g)
+                for (int b = 0; b < kCNBuf; ++b) {
+                    ptx::mbar_init(afull(g, b), 4);
+                    ptx::mbar_init(aempty(g, b), 1);
+                }
+            for (int d = 0; d < 2; ++d) {
+                ptx::mbar_init(dfull(d), 1);
+                ptx::mbar_init(dempty(d), 4);
+                ptx::mbar_init(xfull(d), 1);
+                ptx::mbar_init(xfree(d), 1);
+            }
+            ptx::fence_mbar_init();
+            *s_tdone = 0;
+        }
+        __syncwarp();
+        ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_holder, 0);
+
+    if (warp == 0) {
+        // ================= producer: all cells of this CTA's range of every stage, in order
+        const uint64_t pol = ptx::l2_evict_first_policy();
+        int s = 0;
+        uint32_t r = 0;
+        bool wrapped = false;
+        for (int t = 0; t < ns; ++t) {
+            const ChainStageDev st = Sd[t];
+            const int ua = range_lo(st.U, P, cta), ub = range_lo(st.U, P, cta + 1);
+            if (ua >= ub) continue;
+            int li = 0;
+            while (li + 1 < st.nl && Lg[st.l0 + li + 1].cum <= ua) ++li;
+            int ul = ua - Lg[st.l0 + li].cum;
+            int lcells = Lg[st.l0 + li].n_rb * st.n_kc;
+            const int64_t cw = (int64_t)128 * kTW;
+            const uint32_t* src = Lg[st.l0 + li].packed + (int64_t)ul * cw;
+            for (int u = ua; u < ub; ++u) {
+                if (wrapped) ptx::mbar_wait(empty(s), r ^ 1u);
+                if (ptx::elect_one()) {
+                    ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
+                    ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
+                }
+                __syncwarp();
+                if (++s == S) { s = 0; r ^= 1u; wrapped = true; }
+                src += cw;
+                if (++ul == lcells && li + 1 < st.nl) {
+                    ++li;
+                    ul = 0;
+                    lcells = Lg[st.l0 + li].n_rb * st.n_kc;
+                    src = Lg[st.l0 + li].packed;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= x~ loader + MMA issuer
+        int seg = 0, jj = 0;
+        const uint32_t dstep = 2u * (uint32_t)a.BP;
+        for (int t = 0; t < ns; ++t) {
+            const ChainStageDev st = Sd[t];
+            const int ua = range_lo(st.U, P, cta), ub = range_lo(st.U, P, cta + 1);
+            const int xb = t & 1;
+            const uint32_t xwin = ptx::smem_u32(smem + a.off_x + (uint32_t)xb * a.xbuf_bytes);
+            // the window buffer was the scratch of transition t-1 and the B operand of stage t-2
+            if (t >= 1) {
+                if (lane == 0)
+                    while (*s_tdone < t) __nanosleep(32);
+                __syncwarp();
+            }
+            if (t >= 2) ptx::mbar_wait(xfree(xb), (uint32_t)(((t - 2) >> 1) & 1));
+            int kcs[kMaxStageLayers], base[kMaxStageLayers];
+            int g0 = 0, g1 = -1;
+            if (ua < ub) {
+                while (g0 + 1 < st.nl && Lg[st.l0 + g0 + 1].cum <= ua) ++g0;
+                g1 = g0;
+                while (g1 + 1 < st.nl && Lg[st.l0 + g1 + 1].cum < ub) ++g1;
+                uint32_t bytes = 0;
+                int cum = 0;
+#pragma unroll
+                for (int gl = 0; gl < kMaxStageLayers; ++gl) {
+                    kcs[gl] = base[gl] = 0;
+                    if (gl < g0 || gl > g1) continue;
+                    const int c0 = Lg[st.l0 + gl].cum, c1 = c0 + Lg[st.l0 + gl].n_rb * st.n_kc;
+                    const int lo = ua > c0 ? ua : c0, hi = ub < c1 ? ub : c1;
+                    kcs[gl] = (lo - c0) % st.n_kc;
+                    base[gl] = cum;
+                    cum += hi - lo < st.n_kc ? hi - lo : st.n_kc;
+                }
+                bytes = (uint32_t)cum * a.xcol_bytes;
+                if (lane == 0) {
+                    for (int gl = g0; gl <= g1; ++gl) spin_until(a.ctr + 2 * a.nlayers + st.l0 + gl, Lg[st.l0 + gl].in.ntask);
+                    fence_proxy_async_global();
+                    ptx::fence_proxy_async_smem();
+                    ptx::mbar_arrive_expect_tx(xfull(xb), bytes);
+                    for (int gl = g0; gl <= g1; ++gl) {
+                        const int c0 = Lg[st.l0 + gl].cum, c1 = c0 + Lg[st.l0 + gl].n_rb * st.n_kc;
+                        const int lo = ua > c0 ? ua : c0, hi = ub < c1 ? ub : c1;
+                        const int cnt = hi - lo < st.n_kc ? hi - lo : st.n_kc;
+                        const int run1 = cnt < st.n_kc - kcs[gl] ? cnt : st.n_kc - kcs[gl];
+                        const uint8_t* xs = reinterpret_cast<const uint8_t*>(Lg[st.l0 + gl].xt);
+                        ptx::bulk_g2s(xwin + (uint32_t)base[gl] * a.xcol_bytes, xs + (size_t)kcs[gl] * a.xcol_bytes,
+                                      (uint32_t)run1 * a.xcol_bytes, xfull(xb));
+                        if (cnt > run1)
+                            ptx::bulk_g2s(xwin + (uint32_t)(base[gl] + run1) * a.xcol_bytes, xs,
+                                          (uint32_t)(cnt - run1) * a.xcol_bytes, xfull(xb));
+                    }
+                }
+                __syncwarp();
+                ptx::mbar_wait(xfull(xb), (uint32_t)((t >> 1) & 1));
+            } else {
+                // keep the window barrier's phases aligned with the stage count
+                if (lane == 0) ptx::mbar_arrive(xfull(xb));
+                __syncwarp();
+                ptx::mbar_wait(xfull(xb), (uint32_t)((t >> 1) & 1));
+            }
+            ptx::tc_fence_after();
+            if (ua < ub) {
+                int gl = g0;
+                const int cl = ua - Lg[st.l0 + gl].cum;
+                int RB = cl / st.n_kc, KC = cl - RB * st.n_kc;
+                int nrb = Lg[st.l0 + gl].n_rb;
+                int off = (KC - kcs[gl] + st.n_kc) % st.n_kc;
+                int wbase = base[gl];
+                uint32_t dcol = tmem;
+                bool first = true;
+                for (int u = ua; u < ub; ++u, ++jj) {
+                    if (u == ua || KC == 0) {
+                        const int d = seg & 1;
+                        if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
+                        ptx::tc_fence_after();
+                        dcol = tmem + (uint32_t)d * kD1;
+                        first = true;
+                    }
+                    const int g = jj % kCG, lc = jj / kCG, b = lc & (kCNBuf - 1);
+                    ptx::mbar_wait(afull(g, b), (uint32_t)((lc / kCNBuf) & 1));
+                    ptx::tc_fence_after();
+                    const uint64_t cdesc = ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)(wbase + off) * a.xcol_bytes, a.lbo, a.sbo);
+                    const uint32_t acol = tmem + kA0 + (uint32_t)(g * kCNBuf + b) * kACols;
+                    const bool seg_end = (u + 1 == ub) || (KC == st.n_kc - 1);
+                    if (ptx::elect_one()) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            ptx::umma_f16_ts(dcol, acol + 8u * (uint32_t)i, cdesc + (uint64_t)(dstep * (uint32_t)i), idesc,
+                                             (first && i == 0) ? 0u : 1u);
+                        ptx::umma_commit(aempty(g, b));
+                        if (seg_end) ptx::umma_commit(dfull(seg & 1));
+                    }
+                    __syncwarp();
+                    first = false;
+                    if (seg_end) ++seg;
+                    if (++off == st.n_kc) off = 0;
+                    if (++KC == st.n_kc) {
+                        KC = 0;
+                        if (++RB == nrb && gl + 1 <= g1) {
+                            RB = 0;
+                            ++gl;
+                            nrb = Lg[st.l0 + gl].n_rb;
+                            off = (st.n_kc - kcs[gl]) % st.n_kc;
+                            wbase = base[gl];
+                        }
+                    }
+                }
+            }
+            if (ptx::elect_one()) ptx::umma_commit(xfree(xb));   // this stage's MMAs read window xb
+            __syncwarp();
+        }
+    } else if (warp < 6) {
+        // ================= epilogue (E(s)) and transition tasks (T(s))
+        __shared__ int s_last;
+        const int q = warp & 3;
+        const int R = 32 * q + lane;                  // TMEM lane = row of the row block
+        const int tid = (int)threadIdx.x - 64;        // 0..127 over warps 2-5
+        const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+        int seg = 0;
+        for (int t = 0; t <= ns; ++t) {
+            if (t >= 1) {
+                // ---- E(t-1): this CTA's segments of stage t-1
+                const ChainStageDev st = Sd[t - 1];
+                const int ua = range_lo(st.U, P, cta), ub = range_lo(st.U, P, cta + 1);
+                if (ua < ub) {
+                    for (int RBv = ua / st.n_kc; RBv <= (ub - 1) / st.n_kc; ++RBv, ++seg) {
+                        const int d = seg & 1;
+                        int gl = 0;
+                        while (gl + 1 < st.nl && st.rb_cum[gl + 1] <= RBv) ++gl;
+                        const int li = st.l0 + gl;
+                        const int RB = RBv - st.rb_cum[gl];
+                        float* const yt = Lg[li].yt;
+                        const int mp = Lg[li].n_rb * 128;
+                        const int w0 = range_of(st.U, P, RBv * st.n_kc), w1 = range_of(st.U, P, (RBv + 1) * st.n_kc - 1);
+                        const bool whole = w0 == w1;
+                        float* segp = Lg[li].seg + ((int64_t)(w0 - Lg[li].wfirst + RB) * a.BP) * 128 + R;
+                        float* dst = segp + (int64_t)(cta - w0) * a.BP * 128;
+                        ptx::mbar_wait(dfull(d), (uint32_t)((seg >> 1) & 1));
+                        ptx::tc_fence_after();
+                        uint32_t rr[16];
+                        ptx::tmem_ld16(tl + (uint32_t)d * kD1, rr);
+                        ptx::tc_wait_ld();
+                        ptx::tc_fence_before();
+                        warp_arrive(dempty(d), lane);
+#pragma unroll
+                        for (int bb = 0; bb < 16; ++bb) {
+                            if (bb >= a.B) break;
+                            const float v = __uint_as_float(rr[bb]);
+                            if (whole) yt[(int64_t)bb * mp + RB * 128 + R] = v;
+                            else dst[bb * 128] = v;
+                        }
+                        bool fin = whole;
+                        if (!whole) {
+                            __threadfence();
+                            ptx::named_bar_sync(1, kXfThreads);
+                            if (tid == 0) {
+                                const int old = atomicAdd(Lg[li].ticket + RB, 1);
+                                const bool last = old == w1 - w0;
+                                if (last) Lg[li].ticket[RB] = 0;
+                                s_last = last ? 1 : 0;
+                            }
+                            ptx::named_bar_sync(1, kXfThreads);
+                            fin = s_last != 0;
+                            if (fin) {
+                                __threadfence();
+                                const int cnt = w1 - w0 + 1;
+                                for (int bb = 0; bb < a.B; ++bb) {
+                                    const float* sp = segp + bb * 128;
+                                    float acc = __ldcg(sp);
+                                    for (int j = 1; j < cnt; ++j) acc += __ldcg(sp + (int64_t)j * a.BP * 128);
+                                    yt[(int64_t)bb * mp + RB * 128 + R] = acc;
+                                }
+                            }
+                        }
+                        if (fin) {
+                            // the row block of y~ is final: count it (release)
+                            __threadfence();
+                            ptx::named_bar_sync(1, kXfThreads);
+                            if (tid == 0) atomicAdd(a.ctr + li, 1);
+                        }
+                    }
+                }
+            }
+            // ---- T(t): Tout of stage t-1, then Tin of stage t; task j on CTA (j + 7 t) mod P
+            {
+                int nto = 0, nti = 0;
+                if (t >= 1)
+                    for (int gl = 0; gl < Sd[t - 1].nl; ++gl) nto += Lg[Sd[t - 1].l0 + gl].out.ntask;
+                if (t < ns)
+                    for (int gl = 0; gl < Sd[t].nl; ++gl) nti += Lg[Sd[t].l0 + gl].in.ntask;
+                const int rot = (int)((7ll * t) % P);
+                int j = cta - rot;
+                if (j < 0) j += P;
+                float* scratch = reinterpret_cast<float*>(smem + a.off_x + (uint32_t)((t + 1) & 1) * a.xbuf_bytes);
+                for (; j < nto + nti; j += P) {
+                    const int dir = j < nto ? 1 : 0;
+                    int jr = dir ? j : j - nto;
+                    const ChainStageDev& st = Sd[dir ? t - 1 : t];
+                    int li = st.l0;
+                    while (true) {
+                        const int nt = dir ? Lg[li].out.ntask : Lg[li].in.ntask;
+                        if (jr < nt) break;
+                        jr -= nt;
+                        ++li;
+                    }
+                    const ChainLayerDev Ld = Lg[li];
+                    if (tid == 0) {
+                        if (dir) spin_until(a.ctr + li, Ld.n_rb);
+                        else if (Ld.src >= 0) spin_until(a.ctr + a.nlayers + Ld.src, Lg[Ld.src].out.ntask);
+                    }
+                    ptx::named_bar_sync(1, kXfThreads);
+                    run_xform(a, Ld, dir, jr, scratch, tid);
+                    if (!dir) fence_proxy_async_global();
+                    __threadfence();
+                    ptx::named_bar_sync(1, kXfThreads);
+                    if (tid == 0) atomicAdd(a.ctr + (dir ? a.nlayers : 2 * a.nlayers) + li, 1);
+                }
+                ptx::named_bar_sync(1, kXfThreads);
+                if (tid == 0) {
+                    __threadfence_block();
+                    *s_tdone = t + 1;
+                }
+            }
+        }
+    } else {
+        // ================= decoders: cells jj = g, g + 3, ... of the CTA's cell sequence
+        const int dw = warp - 6, g = dw >> 2, q = warp & 3;
+        const int R = 32 * q + lane, I = R >> 4, rho = R & 15;
+        const uint32_t ta_lane = tmem + ((uint32_t)(32 * q) << 16) + kA0;
+        const uint32_t lut_lane = ptx::smem_u32(smem + kCHdr) + 4u * (uint32_t)lane;
+        int ncell = 0;
+        for (int t = 0; t < ns; ++t) ncell += range_lo(Sd[t].U, P, cta + 1) - range_lo(Sd[t].U, P, cta);
+        int lc = 0;
+        for (int jj = g; jj < ncell; jj += kCG, ++lc) {
+            const int s = jj % S;
+            const uint32_t r = (uint32_t)((jj / S) & 1);
+            const int b = lc & (kCNBuf - 1), use = lc / kCNBuf;
+            ptx::mbar_wait(full(s), r);
+            if (use > 0) ptx::mbar_wait(aempty(g, b), (uint32_t)((use - 1) & 1));
+            ptx::tc_fence_after();
+            const uint32_t* cellw = reinterpret_cast<const uint32_t*>(ring + (size_t)s * kCellBytes);
+            const uint32_t ta = ta_lane + (uint32_t)(g * kCNBuf + b) * kACols;
+#pragma unroll 1
+            for (int pp = 0; pp < 4; ++pp)
+                udec::decode_pair<K, CODE, kImm>(cellw + (I * 4 + pp) * kTW * 2, rho, a.ca, lut_lane, ta + (uint32_t)pp * 16);
+            warp_arrive(empty(s), lane);
+            ptx::tc_wait_st();
+            ptx::tc_fence_before();
+            warp_arrive(afull(g, b), lane);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int K, int CODE, bool kImm>
+cudaError_t launch_chain_t(const ChainArgs& a, int P, size_t smem, cudaStream_t s) {
+    auto kern = chain_kernel<K, CODE, kImm>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    prefer_max_smem((const void*)kern);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)P);
+    cfg.blockDim = dim3(kCThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+// Transform geometry over length n (reading R7): see the file comment.
+bool make_xform(int64_t n, int P, Xform* X) {
+    int b = 0, a = 0;
+    if (!hadamard_factor(n, &b, &a)) return false;
+    int a2 = a <= 5 ? a : (a < 7 ? 5 : std::min(a, 12));
+    X->n = (int)n;
+    X->b = b;
+    X->a1 = a - a2;
+    X->L2 = 1 << a2;
+    X->f = (int)(n >> a2);
+    // rows per task: about 64 tasks per transform at most (the transition's tasks spread over the
+    // CTAs), and for L2 >= 128 the task's rows of Z must fit the scratch (<= 4096 floats)
+    const int target = std::max(1, std::min(64, P / 2));
+    int R = (X->f + target - 1) / target;
+    if (X->L2 >= 128) R = std::min(R, std::max(1, 4096 / X->L2));
+    X->R = std::max(1, R);
+    X->ntask = (X->f + X->R - 1) / X->R;
+    return true;
+}
+
+size_t xform_scratch_bytes(const Xform& X) {
+    const size_t d = ((size_t)X.R * X.f + 31) & ~size_t(31);
+    return 4 * (d + (X.L2 >= 128 ? (size_t)X.R * X.L2 : 0));
+}
+
+}  // namespace
+}  // namespace qtip
+
+// ------------------------------------------------------------------------------------ C ABI
+using namespace qtip;
+
+struct qtip_chain_plan {
+    int device = 0;
+    int code = 0, k = 0;
+    bool imm = false;
+    int P = 0;
+    int nstages = 0, nlayers = 0;
+    int64_t B = 0;
+    size_t smem = 0;
+    ChainArgs args{};
+    void* dmem = nullptr;          // one allocation: tables, counters, per-layer buffers
+    size_t ctr_bytes = 0;
+    int* ctr = nullptr;
+};
+
+extern "C" {
+
+qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const qtip_chain_layer* layers, int64_t B,
+                                   const uint16_t* d_lut, qtip_chain_plan** out) {
+    if (!out) return api_fail(QTIP_ERR_INVALID_PARAMS, "plan pointer is NULL");
+    *out = nullptr;
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if (nlayers < 1 || !layers) return api_fail(QTIP_ERR_INVALID_PARAMS, "need at least one layer");
+    if (B < 1 || B > 16) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: batch must be in 1..16");
+    if (p->k < 2 || p->k > 4) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: needs 2 <= k <= 4");
+    if (p->code == QTIP_CODE_HYB && (p->Q != (int)kCLutQ || p->hyb_two_sign || !d_lut))
+        return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: HYB needs Q = 9, one-sign, and a LUT");
+    const int P = num_sms();
+    const int BP = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
+    // ---- validate the layer list and build the stages
+    std::vector<ChainStageDev> stages;
+    std::vector<ChainLayerDev> L(nlayers);
+    for (int i = 0; i < nlayers; ++i) {
+        const qtip_chain_layer& c = layers[i];
+        if (!c.d_packed || !c.d_sign_n || !c.d_sign_m || !c.d_y) return api_fail(QTIP_ERR_INVALID_PARAMS, "NULL layer buffer");
+        if ((reinterpret_cast<uintptr_t>(c.d_packed) & 15u)) return api_fail(QTIP_ERR_ALIGNMENT, "d_packed must be 16-B aligned");
+        if (c.m <= 0 || c.n <= 0 || c.m % kTile || c.n % kTile) return api_fail(QTIP_ERR_SHAPE, "m and n must be positive multiples of 16");
+        const int want_stage = i == 0 ? 0 : (c.stage == layers[i - 1].stage ? layers[i - 1].stage : layers[i - 1].stage + 1);
+        if (c.stage != want_stage) return api_fail(QTIP_ERR_INVALID_PARAMS, "stages must be numbered 0, 1, ... in layer order");
+        if (c.stage == 0 && c.src != -1) return api_fail(QTIP_ERR_INVALID_PARAMS, "stage 0 layers read the external x (src = -1)");
+        if (c.stage > 0) {
+            if (c.src < 0 || c.src >= i || layers[c.src].stage != c.stage - 1)
+                return api_fail(QTIP_ERR_INVALID_PARAMS, "src must be a layer of the previous stage");
+            if (layers[c.src].m != c.n) return api_fail(QTIP_ERR_SHAPE, "src layer's m must equal this layer's n");
+        }
+        if (i > 0 && c.stage == layers[i - 1].stage && (c.n != layers[i - 1].n || c.src != layers[i - 1].src))
+            return api_fail(QTIP_ERR_INVALID_PARAMS, "layers of a stage share n and src (one input)");
+        const Layout l = make_layout(c.m, c.n, p->k);
+        ChainLayerDev& d = L[i];
+        d = ChainLayerDev{};
+        d.packed = (const uint32_t*)c.d_packed;
+        d.sign_n = c.d_sign_n;
+        d.sign_m = c.d_sign_m;
+        d.y = c.d_y;
+        d.scale = c.scale;
+        d.m = (int)c.m;
+        d.n = (int)c.n;
+        d.n_rb = (int)l.n_rb;
+        d.n_kc = (int)l.n_kc;
+        d.src = c.src;
+        if (!make_xform(c.m, P, &d.out) || !make_xform(c.n, P, &d.in))
+            return api_fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m or n");
+        if (c.stage >= (int)stages.size()) {
+            ChainStageDev s{};
+            s.l0 = i;
+            s.n_kc = d.n_kc;
+            stages.push_back(s);
+        }
+        ChainStageDev& s = stages.back();
+        if (s.nl == kMaxStageLayers) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: at most 4 layers per stage");
+        d.cum = s.U;
+        s.rb_cum[s.nl] = s.U / s.n_kc;
+        s.U += d.n_rb * d.n_kc;
+        s.nl += 1;
+        s.rb_cum[s.nl] = s.U / s.n_kc;
+        if ((int64_t)s.U * (P + 1) >= (1ll << 31)) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: stage too large");
+    }
+    for (auto& s : stages)
+        for (int gl = 0; gl < s.nl; ++gl) {
+            ChainLayerDev& d = L[s.l0 + gl];
+            d.wfirst = (int)((((uint64_t)d.cum + 1) * P - 1) / s.U);
+        }
+    // ---- shared memory: ring + LUT + two x~ windows / transform scratch
+    const bool hyb = p->code == QTIP_CODE_HYB;
+    const uint32_t xcol = 128u * 2u * (uint32_t)BP;
+    size_t xbuf = 0;
+    for (auto& s : stages) {
+        for (int w = 0; w < P; ++w) {
+            const int64_t ua = (int64_t)s.U * w / P, ub = (int64_t)s.U * (w + 1) / P;
+            int64_t cols = 0;
+            for (int gl = 0; gl < s.nl; ++gl) {
+                const ChainLayerDev& d = L[s.l0 + gl];
+                const int64_t c0 = d.cum, c1 = c0 + (int64_t)d.n_rb * d.n_kc;
+                const int64_t lo = std::max(ua, c0), hi = std::min(ub, c1);
+                if (lo < hi) cols += std::min<int64_t>(hi - lo, d.n_kc);
+            }
+            xbuf = std::max(xbuf, (size_t)cols * xcol);
+        }
+    }
+    for (auto& d : L) xbuf = std::max({xbuf, xform_scratch_bytes(d.out), xform_scratch_bytes(d.in)});
+    xbuf = (xbuf + 1023) & ~size_t(1023);
+    const size_t cell = 2048u * (size_t)p->k;
+    const size_t lutb = hyb ? kCLutBytes : 0;
+    int S = chain_stages(p->k, p->code);
+    const size_t smem = kCHdr + lutb + (size_t)S * cell + 2 * xbuf;
+    if (smem > 227 * 1024) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: x~ windows / transform scratch do not fit shared memory");
+    // ---- device memory: [layer table][stage table][counters + tickets][x~][y~][segments]
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return api_cuda_fail(e, "qtip_chain_plan_create");
+    auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+    size_t off = 0;
+    const size_t o_L = off; off += al(sizeof(ChainLayerDev) * nlayers);
+    const size_t o_S = off; off += al(sizeof(ChainStageDev) * stages.size());
+    const size_t o_ctr = off;
+    size_t nctr = 3 * (size_t)nlayers;
+    for (auto& d : L) nctr += d.n_rb;
+    const size_t ctr_bytes = al(nctr * sizeof(int));
+    off += ctr_bytes;
+    std::vector<size_t> o_xt(nlayers), o_yt(nlayers), o_seg(nlayers);
+    for (int i = 0; i < nlayers; ++i) {
+        const ChainLayerDev& d = L[i];
+        o_xt[i] = off; off += al((size_t)d.n_kc * 128 * BP * 2);
+        o_yt[i] = off; off += al((size_t)B * d.n_rb * 128 * 4);
+        o_seg[i] = off; off += al((size_t)(P + d.n_rb) * BP * 128 * 4);
+    }
+    void* dmem = nullptr;
+    if ((e = cudaMalloc(&dmem, off)) != cudaSuccess) return api_cuda_fail(e, "qtip_chain_plan_create: cudaMalloc");
+    if ((e = cudaMemset(dmem, 0, off)) != cudaSuccess) {
+        cudaFree(dmem);
+        return api_cuda_fail(e, "qtip_chain_plan_create: cudaMemset");
+    }
+    char* base = (char*)dmem;
+    int* tk = (int*)(base + o_ctr) + 3 * nlayers;
+    for (int i = 0; i < nlayers; ++i) {
+        ChainLayerDev& d = L[i];
+        d.xt = (uint16_t*)(base + o_xt[i]);
+        d.yt = (float*)(base + o_yt[i]);
+        d.seg = (float*)(base + o_seg[i]);
+        d.ticket = tk;
+        tk += d.n_rb;
+        d.hb_n = d.in.b > 1 ? hadamard_table_device(d.in.b, false, &e) : nullptr;
+        if (e == cudaSuccess) d.hbt_m = d.out.b > 1 ? hadamard_table_device(d.out.b, true, &e) : nullptr;
+        if (e != cudaSuccess) {
+            cudaFree(dmem);
+            return api_cuda_fail(e, "qtip_chain_plan_create: Hadamard tables");
+        }
+    }
+    if ((e = cudaMemcpy(base + o_L, L.data(), sizeof(ChainLayerDev) * nlayers, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(base + o_S, stages.data(), sizeof(ChainStageDev) * stages.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cudaFree(dmem);
+        return api_cuda_fail(e, "qtip_chain_plan_create: tables");
+    }
+    qtip_chain_plan* pl = new qtip_chain_plan();
+    pl->device = dev;
+    pl->code = p->code;
+    pl->k = p->k;
+    const CodeArgs ca = api_code_args(p);
+    pl->imm = !hyb && p->k == 2 && ca.a == (p->code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&
+              ca.b == (p->code == QTIP_CODE_1MAD ? 76625530u : 64248484u);
+    pl->P = P;
+    pl->nstages = (int)stages.size();
+    pl->nlayers = nlayers;
+    pl->B = B;
+    pl->smem = smem;
+    pl->dmem = dmem;
+    pl->ctr = (int*)(base + o_ctr);
+    pl->ctr_bytes = ctr_bytes;
+    ChainArgs& a = pl->args;
+    a.L = (const ChainLayerDev*)(base + o_L);
+    a.S = (const ChainStageDev*)(base + o_S);
+    a.nstages = pl->nstages;
+    a.nlayers = nlayers;
+    a.ctr = pl->ctr;
+    a.lut = (const uint32_t*)d_lut;
+    a.ca = ca;
+    a.B = (int)B;
+    a.BP = BP;
+    a.xcol_bytes = xcol;
+    a.lbo = 16u * (uint32_t)BP;
+    a.sbo = 128u;
+    a.off_ring = (uint32_t)(kCHdr + lutb);
+    a.off_x = (uint32_t)(kCHdr + lutb + (size_t)S * cell);
+    a.xbuf_bytes = (uint32_t)xbuf;
+    *out = pl;
+    return QTIP_OK;
+}
+
+qtip_status qtip_chain_run(qtip_chain_plan* pl, const float* d_x, void* stream) {
+    if (!pl || !d_x) return api_fail(QTIP_ERR_INVALID_PARAMS, "NULL plan or x");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(pl->ctr, 0, pl->ctr_bytes, s);
+    if (e != cudaSuccess) return api_cuda_fail(e, "qtip_chain_run: counters");
+    ChainArgs a = pl->args;
+    a.x = d_x;
+    e = cudaErrorInvalidValue;
+#define QTIP_C_CASE(KK, CC, II) \
+    if (pl->k == KK && pl->code == CC && pl->imm == II) e = launch_chain_t<KK, CC, II>(a, pl->P, pl->smem, s);
+    QTIP_C_CASE(2, QTIP_CODE_3INST, true) QTIP_C_CASE(2, QTIP_CODE_1MAD, true)
+    QTIP_C_CASE(2, QTIP_CODE_3INST, false) QTIP_C_CASE(2, QTIP_CODE_1MAD, false)
+    QTIP_C_CASE(3, QTIP_CODE_3INST, false) QTIP_C_CASE(3, QTIP_CODE_1MAD, false)
+    QTIP_C_CASE(4, QTIP_CODE_3INST, false) QTIP_C_CASE(4, QTIP_CODE_1MAD, false)
+    QTIP_C_CASE(2, QTIP_CODE_HYB, false) QTIP_C_CASE(3, QTIP_CODE_HYB, false) QTIP_C_CASE(4, QTIP_CODE_HYB, false)
+#undef QTIP_C_CASE
+    count_launch(1);
+    if (e != cudaSuccess) return api_cuda_fail(e, "qtip_chain_run: launch");
+    return QTIP_OK;
+}
+
+void qtip_chain_plan_destroy(qtip_chain_plan* pl) {
+    if (!pl) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(pl->device);
+    cudaFree(pl->dmem);
+    cudaSetDevice(cur);
+    delete pl;
+}
+
+int32_t qtip_chain_plan_stages(const qtip_chain_plan* pl) { return pl ? pl->nstages : 0; }
+
+}  // extern "C"

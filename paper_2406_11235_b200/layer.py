@@ -129,3 +129,53 @@ def forward_group(layers, x, outs=None, flags=qtip.QTIP_RHT_IN | qtip.QTIP_RHT_O
                            flags, [l.workspace(B) for l in layers], stream)
     return outs
 
+
+
+class QTIPChain:
+    """A chain of QTIPLinear layers run as ONE persistent launch per call (qtip_chain_run): stage 0
+    reads the external x, every later stage reads the output of one layer of the previous stage
+    (e.g. a decode step: q, k, v -> o -> gate, up -> down -> ...).
+
+    stages: list of (layers, src) with layers a list of QTIPLinear sharing n, and src the index
+    (within the previous stage) of the layer whose output is this stage's input (ignored for
+    stage 0).  Outputs: self.outs[stage][i], float32 (B, m), rewritten by every call."""
+
+    def __init__(self, stages, B=1):
+        if not stages:
+            raise ValueError("QTIPChain: no stages")
+        l0 = stages[0][0][0]
+        self.B, self.device, self.p = B, l0.device, l0.p
+        self.outs, descs, first = [], [], []
+        for si, (layers, src) in enumerate(stages):
+            outs = []
+            first.append(len(descs))
+            for lay in layers:
+                if bytes(lay.p) != bytes(l0.p):
+                    raise ValueError("QTIPChain: all layers share the QTIP parameters")
+                y = torch.empty((B, lay.m), dtype=torch.float32, device=self.device)
+                outs.append(y)
+                descs.append(dict(packed=lay.packed, sign_n=lay.sign_n, sign_m=lay.sign_m, scale=lay.scale, m=lay.m,
+                                  n=lay.n, y=y, stage=si, src=-1 if si == 0 else first[si - 1] + int(src)))
+            self.outs.append(outs)
+        self.n_in = stages[0][0][0].n
+        self.layers = [lay for layers, _ in stages for lay in layers]
+        lut = l0.lut if l0.code == "hyb" else None
+        self._plan = qtip.qtip_chain_plan_create(self.p, descs, B, lut)
+
+    def forward(self, x, stream=None):
+        _check_io(x, (self.B, self.n_in), self.device, "x")
+        qtip.qtip_chain_run(self._plan, x, stream)
+        return self.outs
+
+    __call__ = forward
+
+    def close(self):
+        if getattr(self, "_plan", None):
+            qtip.qtip_chain_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:       # noqa: BLE001  (interpreter shutdown)
+            pass

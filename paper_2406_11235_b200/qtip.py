@@ -27,7 +27,8 @@ EXPORTS = ["qtip_params_default", "qtip_params_check", "qtip_packed_bytes", "qti
            "qtip_decode", "qtip_matvec", "qtip_matvec_group", "qtip_matvec_group_fused", "qtip_matvec_workspace_bytes", "qtip_rht", "qtip_hadamard_order",
            "qtip_set_matvec_impl", "qtip_get_matvec_impl", "qtip_status_string", "qtip_last_error",
            "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl", "qtip_viterbi_workspace_bytes",
-           "qtip_viterbi_tailbite"]
+           "qtip_viterbi_tailbite", "qtip_chain_plan_create", "qtip_chain_run", "qtip_chain_plan_destroy",
+           "qtip_chain_plan_stages"]
 
 
 class QtipParams(ctypes.Structure):
@@ -35,6 +36,12 @@ class QtipParams(ctypes.Structure):
                 ("Q", ctypes.c_int32), ("tail_biting", ctypes.c_int32), ("Tx", ctypes.c_int32), ("Ty", ctypes.c_int32),
                 ("lcg_a", ctypes.c_uint32), ("lcg_b", ctypes.c_uint32), ("m_fp16", ctypes.c_uint32),
                 ("hyb_two_sign", ctypes.c_int32)]
+
+
+class ChainLayer(ctypes.Structure):
+    _fields_ = [("d_packed", ctypes.c_void_p), ("d_sign_n", ctypes.c_void_p), ("d_sign_m", ctypes.c_void_p),
+                ("scale", ctypes.c_float), ("m", ctypes.c_int64), ("n", ctypes.c_int64), ("d_y", ctypes.c_void_p),
+                ("stage", ctypes.c_int32), ("src", ctypes.c_int32)]
 
 
 class QtipError(RuntimeError):
@@ -102,6 +109,14 @@ def load(path=LIB_PATH):
     lib.qtip_profile_events.restype = None
     lib.qtip_set_pdl.argtypes = [ctypes.c_int]
     lib.qtip_set_pdl.restype = None
+    lib.qtip_chain_plan_create.argtypes = [P, i32, ctypes.POINTER(ChainLayer), i64, vp, ctypes.POINTER(vp)]
+    lib.qtip_chain_plan_create.restype = ctypes.c_int
+    lib.qtip_chain_run.argtypes = [vp, vp, vp]
+    lib.qtip_chain_run.restype = ctypes.c_int
+    lib.qtip_chain_plan_destroy.argtypes = [vp]
+    lib.qtip_chain_plan_destroy.restype = None
+    lib.qtip_chain_plan_stages.argtypes = [vp]
+    lib.qtip_chain_plan_stages.restype = i32
     _lib = lib
     return lib
 
@@ -208,6 +223,28 @@ def qtip_viterbi_tailbite(p, nseq, T, d_source, d_states, d_cost, d_workspace, d
     _check("qtip_viterbi_tailbite", load().qtip_viterbi_tailbite(
         ctypes.byref(p), nseq, T, _ptr(d_source), _ptr(d_lut), _ptr(d_states), _ptr(d_cost), _ptr(d_workspace),
         d_workspace.numel() * d_workspace.element_size(), _stream(stream)))
+
+
+def qtip_chain_plan_create(p, layers, B, d_lut=None):
+    """layers: list of dicts (packed, sign_n, sign_m: device tensors; scale; m; n; y: device
+    float32 (B, m); stage; src) in stage order -> opaque plan handle (c_void_p)."""
+    arr = (ChainLayer * len(layers))()
+    for i, d in enumerate(layers):
+        arr[i] = ChainLayer(d["packed"].data_ptr(), d["sign_n"].data_ptr(), d["sign_m"].data_ptr(), float(d["scale"]),
+                            int(d["m"]), int(d["n"]), d["y"].data_ptr(), int(d["stage"]), int(d["src"]))
+    plan = ctypes.c_void_p()
+    _check("qtip_chain_plan_create", load().qtip_chain_plan_create(ctypes.byref(p), len(layers), arr, int(B),
+                                                                   _ptr(d_lut), ctypes.byref(plan)))
+    return plan
+
+
+def qtip_chain_run(plan, d_x, stream=None):
+    _check("qtip_chain_run", load().qtip_chain_run(plan, _ptr(d_x), _stream(stream)))
+
+
+def qtip_chain_plan_destroy(plan):
+    if plan:
+        load().qtip_chain_plan_destroy(plan)
 
 
 def qtip_rht(n, B, d_sign, d_in, d_out, inverse=False, stream=None):

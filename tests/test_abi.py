@@ -169,3 +169,38 @@ def test_group_call_validation(lib):
     assert call(wsb=16) == -7                                      # workspace too small
     assert lib.qtip_matvec_group(ctypes.byref(p), 3, 256, 256, 1, None, None, arr(256), arr(256), sc, vp(256), arr(512),
                                  3, arr(256), ws, None) == -1
+
+
+def _chain_status(lib, p, layers, B=1, lut=None):
+    arr = (qtip.ChainLayer * len(layers))()
+    for i, d in enumerate(layers):
+        arr[i] = qtip.ChainLayer(0x1000, 0x2000, 0x3000, 1.0, d[0], d[1], 0x4000, d[2], d[3])
+    plan = ctypes.c_void_p()
+    return lib.qtip_chain_plan_create(ctypes.byref(p), len(layers), arr, B, lut, ctypes.byref(plan))
+
+
+def test_chain_plan_validation(lib):
+    """qtip_chain_plan_create rejects malformed chains on the host, before any device call."""
+    p = qtip.params_default("3inst", 2)
+    ok_a = (512, 256, 0, -1)
+    # stage numbers must start at 0 and grow by one
+    assert _chain_status(lib, p, [(512, 256, 1, -1)]) == -1
+    assert _chain_status(lib, p, [ok_a, (256, 512, 2, 0)]) == -1
+    # stage 0 reads x; later stages read a layer of the previous stage with m == n
+    assert _chain_status(lib, p, [(512, 256, 0, 0)]) == -1
+    assert _chain_status(lib, p, [ok_a, (256, 256, 1, 0)]) == -2
+    assert _chain_status(lib, p, [ok_a, (256, 512, 1, -1)]) == -1
+    # a stage shares n and src; at most 4 layers per stage
+    assert _chain_status(lib, p, [ok_a, (512, 128, 0, -1)]) == -1
+    assert _chain_status(lib, p, [ok_a] * 5) == -5
+    # batch 1..16, k 2..4, HYB needs its LUT
+    assert _chain_status(lib, p, [ok_a], B=17) == -5
+    assert _chain_status(lib, p, [ok_a], B=0) == -5
+    assert _chain_status(lib, qtip.params_default("3inst", 1), [ok_a]) == -5
+    assert _chain_status(lib, qtip.params_default("hyb", 4), [ok_a]) == -5
+    # shapes: positive multiples of 16
+    assert _chain_status(lib, p, [(520, 256, 0, -1)]) == -2
+    assert _chain_status(lib, p, [(512, 40, 0, -1)]) == -2
+    assert lib.qtip_chain_run(None, None, None) == -1
+    lib.qtip_chain_plan_destroy(None)
+    assert lib.qtip_chain_plan_stages(None) == 0
