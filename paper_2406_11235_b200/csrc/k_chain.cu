@@ -113,6 +113,21 @@ __device__ __forceinline__ int range_lo(int U, int W, int w) { return (int)((uin
 __device__ __forceinline__ int range_of(int U, int W, int u) {
     return (int)((((uint32_t)u + 1u) * (uint32_t)W - 1u) / (uint32_t)U);
 }
+// Debug progress words (qtip_internal_set_chain_debug; null in normal operation): 8 ints per CTA,
+// written as each role advances (host-mapped memory, read by scripts/chain_debug.py while it runs).
+__device__ int* g_chain_dbg = nullptr;
+#define CDBG(slot, val)                                           \
+    do {                                                          \
+        if (dbg) *(volatile int*)(dbg + (slot)) = (int)(val);     \
+    } while (0)
+
+// A stage of U cells is cut into W = min(P, U) non-empty ranges; CTA w < W runs range w.
+__device__ __forceinline__ int stage_ranges(int U, int P) { return U < P ? U : P; }
+__device__ __forceinline__ void cta_range(int U, int P, int cta, int& ua, int& ub) {
+    const int W = stage_ranges(U, P);
+    ua = cta < W ? range_lo(U, W, cta) : 0;
+    ub = cta < W ? range_lo(U, W, cta + 1) : 0;
+}
 __device__ __forceinline__ void warp_arrive(uint32_t bar, int lane) {
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(bar);
@@ -299,6 +314,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
     const int ns = a.nstages;
     const ChainStageDev* __restrict__ Sd = a.S;
     const ChainLayerDev* __restrict__ Lg = a.L;
+    int* const dbg = g_chain_dbg ? g_chain_dbg + 8 * cta : nullptr;
 
     if constexpr (kHyb) {
         uint4* lt = reinterpret_cast<uint4*>(smem + kCHdr);
@@ -345,13 +361,14 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
         bool wrapped = false;
         for (int t = 0; t < ns; ++t) {
             const ChainStageDev st = Sd[t];
-            const int ua = range_lo(st.U, P, cta), ub = range_lo(st.U, P, cta + 1);
+            int ua, ub;
+            cta_range(st.U, P, cta, ua, ub);
             if (ua >= ub) continue;
             int li = 0;
             while (li + 1 < st.nl && Lg[st.l0 + li + 1].cum <= ua) ++li;
             int ul = ua - Lg[st.l0 + li].cum;
             int lcells = Lg[st.l0 + li].n_rb * st.n_kc;
-            const int64_t cw = (int64_t)128 * kTW;
+            const int64_t cw = kCellBytes / 4;            // words per cell
             const uint32_t* src = Lg[st.l0 + li].packed + (int64_t)ul * cw;
             for (int u = ua; u < ub; ++u) {
                 if (wrapped) ptx::mbar_wait(empty(s), r ^ 1u);
@@ -360,6 +377,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                     ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
                 }
                 __syncwarp();
+                if (lane == 0) CDBG(0, u + 1000000 * t);
                 if (++s == S) { s = 0; r ^= 1u; wrapped = true; }
                 src += cw;
                 if (++ul == lcells && li + 1 < st.nl) {
@@ -376,16 +394,20 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
         const uint32_t dstep = 2u * (uint32_t)a.BP;
         for (int t = 0; t < ns; ++t) {
             const ChainStageDev st = Sd[t];
-            const int ua = range_lo(st.U, P, cta), ub = range_lo(st.U, P, cta + 1);
+            int ua, ub;
+            cta_range(st.U, P, cta, ua, ub);
             const int xb = t & 1;
             const uint32_t xwin = ptx::smem_u32(smem + a.off_x + (uint32_t)xb * a.xbuf_bytes);
             // the window buffer was the scratch of transition t-1 and the B operand of stage t-2
+            if (lane == 0) CDBG(1, 10 * t + 1);
             if (t >= 1) {
                 if (lane == 0)
                     while (*s_tdone < t) __nanosleep(32);
                 __syncwarp();
             }
+            if (lane == 0) CDBG(1, 10 * t + 2);
             if (t >= 2) ptx::mbar_wait(xfree(xb), (uint32_t)(((t - 2) >> 1) & 1));
+            if (lane == 0) CDBG(1, 10 * t + 3);
             int kcs[kMaxStageLayers], base[kMaxStageLayers];
             int g0 = 0, g1 = -1;
             if (ua < ub) {
@@ -424,7 +446,9 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                     }
                 }
                 __syncwarp();
+                if (lane == 0) CDBG(1, 10 * t + 4);
                 ptx::mbar_wait(xfull(xb), (uint32_t)((t >> 1) & 1));
+                if (lane == 0) CDBG(1, 10 * t + 5);
             } else {
                 // keep the window barrier's phases aligned with the stage count
                 if (lane == 0) ptx::mbar_arrive(xfull(xb));
@@ -451,6 +475,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                     }
                     const int g = jj % kCG, lc = jj / kCG, b = lc & (kCNBuf - 1);
                     ptx::mbar_wait(afull(g, b), (uint32_t)((lc / kCNBuf) & 1));
+                    if (lane == 0) CDBG(2, jj);
                     ptx::tc_fence_after();
                     const uint64_t cdesc = ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)(wbase + off) * a.xcol_bytes, a.lbo, a.sbo);
                     const uint32_t acol = tmem + kA0 + (uint32_t)(g * kCNBuf + b) * kACols;
@@ -494,17 +519,21 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
             if (t >= 1) {
                 // ---- E(t-1): this CTA's segments of stage t-1
                 const ChainStageDev st = Sd[t - 1];
-                const int ua = range_lo(st.U, P, cta), ub = range_lo(st.U, P, cta + 1);
+                int ua, ub;
+                cta_range(st.U, P, cta, ua, ub);
+                const int W = stage_ranges(st.U, P);
                 if (ua < ub) {
                     for (int RBv = ua / st.n_kc; RBv <= (ub - 1) / st.n_kc; ++RBv, ++seg) {
                         const int d = seg & 1;
+                        if (tid == 0) CDBG(3, 100 * t + 1);
+                        if (tid == 0) CDBG(4, seg);
                         int gl = 0;
                         while (gl + 1 < st.nl && st.rb_cum[gl + 1] <= RBv) ++gl;
                         const int li = st.l0 + gl;
                         const int RB = RBv - st.rb_cum[gl];
                         float* const yt = Lg[li].yt;
                         const int mp = Lg[li].n_rb * 128;
-                        const int w0 = range_of(st.U, P, RBv * st.n_kc), w1 = range_of(st.U, P, (RBv + 1) * st.n_kc - 1);
+                        const int w0 = range_of(st.U, W, RBv * st.n_kc), w1 = range_of(st.U, W, (RBv + 1) * st.n_kc - 1);
                         const bool whole = w0 == w1;
                         float* segp = Lg[li].seg + ((int64_t)(w0 - Lg[li].wfirst + RB) * a.BP) * 128 + R;
                         float* dst = segp + (int64_t)(cta - w0) * a.BP * 128;
@@ -577,11 +606,13 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                         ++li;
                     }
                     const ChainLayerDev Ld = Lg[li];
+                    if (tid == 0) CDBG(3, 100 * t + 10 + dir);
                     if (tid == 0) {
                         if (dir) spin_until(a.ctr + li, Ld.n_rb);
                         else if (Ld.src >= 0) spin_until(a.ctr + a.nlayers + Ld.src, Lg[Ld.src].out.ntask);
                     }
                     ptx::named_bar_sync(1, kXfThreads);
+                    if (tid == 0) CDBG(3, 100 * t + 20 + dir);
                     run_xform(a, Ld, dir, jr, scratch, tid);
                     if (!dir) fence_proxy_async_global();
                     __threadfence();
@@ -592,6 +623,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 if (tid == 0) {
                     __threadfence_block();
                     *s_tdone = t + 1;
+                    CDBG(3, 100 * t + 99);
                 }
             }
         }
@@ -602,7 +634,11 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
         const uint32_t ta_lane = tmem + ((uint32_t)(32 * q) << 16) + kA0;
         const uint32_t lut_lane = ptx::smem_u32(smem + kCHdr) + 4u * (uint32_t)lane;
         int ncell = 0;
-        for (int t = 0; t < ns; ++t) ncell += range_lo(Sd[t].U, P, cta + 1) - range_lo(Sd[t].U, P, cta);
+        for (int t = 0; t < ns; ++t) {
+            int ua, ub;
+            cta_range(Sd[t].U, P, cta, ua, ub);
+            ncell += ub - ua;
+        }
         int lc = 0;
         for (int jj = g; jj < ncell; jj += kCG, ++lc) {
             const int s = jj % S;
@@ -620,6 +656,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
             ptx::tc_wait_st();
             ptx::tc_fence_before();
             warp_arrive(afull(g, b), lane);
+            if (lane == 0 && q == 0) CDBG(5 + g, jj);
         }
     }
     ptx::tc_fence_before();
@@ -681,6 +718,7 @@ size_t xform_scratch_bytes(const Xform& X) {
 using namespace qtip;
 
 struct qtip_chain_plan {
+    std::vector<void*> xt, yt;     // per-layer internal buffers (debug readout)
     int device = 0;
     int code = 0, k = 0;
     bool imm = false;
@@ -734,7 +772,7 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
         d.sign_n = c.d_sign_n;
         d.sign_m = c.d_sign_m;
         d.y = c.d_y;
-        d.scale = c.scale;
+        d.scale = c.scale * (p->code == QTIP_CODE_1MAD ? 5.0f / 739.0f : 1.0f);   // 1MAD: 1/147.8 (reading R6)
         d.m = (int)c.m;
         d.n = (int)c.n;
         d.n_rb = (int)l.n_rb;
@@ -760,15 +798,17 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
     for (auto& s : stages)
         for (int gl = 0; gl < s.nl; ++gl) {
             ChainLayerDev& d = L[s.l0 + gl];
-            d.wfirst = (int)((((uint64_t)d.cum + 1) * P - 1) / s.U);
+            const int W = std::min(P, s.U);
+            d.wfirst = (int)((((uint64_t)d.cum + 1) * W - 1) / s.U);
         }
     // ---- shared memory: ring + LUT + two x~ windows / transform scratch
     const bool hyb = p->code == QTIP_CODE_HYB;
     const uint32_t xcol = 128u * 2u * (uint32_t)BP;
     size_t xbuf = 0;
     for (auto& s : stages) {
-        for (int w = 0; w < P; ++w) {
-            const int64_t ua = (int64_t)s.U * w / P, ub = (int64_t)s.U * (w + 1) / P;
+        const int W = std::min(P, s.U);
+        for (int w = 0; w < W; ++w) {
+            const int64_t ua = (int64_t)s.U * w / W, ub = (int64_t)s.U * (w + 1) / W;
             int64_t cols = 0;
             for (int gl = 0; gl < s.nl; ++gl) {
                 const ChainLayerDev& d = L[s.l0 + gl];
@@ -834,6 +874,10 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
         return api_cuda_fail(e, "qtip_chain_plan_create: tables");
     }
     qtip_chain_plan* pl = new qtip_chain_plan();
+    for (int i = 0; i < nlayers; ++i) {
+        pl->xt.push_back(L[i].xt);
+        pl->yt.push_back(L[i].yt);
+    }
     pl->device = dev;
     pl->code = p->code;
     pl->k = p->k;
@@ -902,3 +946,19 @@ void qtip_chain_plan_destroy(qtip_chain_plan* pl) {
 int32_t qtip_chain_plan_stages(const qtip_chain_plan* pl) { return pl ? pl->nstages : 0; }
 
 }  // extern "C"
+
+extern "C" int qtip_internal_chain_buffers(qtip_chain_plan* pl, int i, void** xt, void** yt) {
+    if (!pl || i < 0 || i >= pl->nlayers) return -1;
+    *xt = pl->xt[i];
+    *yt = pl->yt[i];
+    return 0;
+}
+
+extern "C" int qtip_internal_set_chain_debug(void* p) {
+    int* q = (int*)p;
+    return (int)cudaMemcpyToSymbol(qtip::g_chain_dbg, &q, sizeof(q));
+}
+
+extern "C" int qtip_internal_copy(void* dst, const void* src, size_t bytes) {
+    return (int)cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+}

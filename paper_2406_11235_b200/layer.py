@@ -148,6 +148,8 @@ class QTIPChain:
         self.outs, descs, first = [], [], []
         for si, (layers, src) in enumerate(stages):
             outs = []
+            if si > 0 and not 0 <= int(src) < len(stages[si - 1][0]):
+                raise ValueError(f"QTIPChain: stage {si} src {src} is not a layer of stage {si - 1}")
             first.append(len(descs))
             for lay in layers:
                 if bytes(lay.p) != bytes(l0.p):

@@ -1,0 +1,4 @@
+set -x
+O=gpurun_out/${1:-chain1}
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_chain.py -q > $O/t2.txt 2>&1

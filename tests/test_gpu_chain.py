@@ -57,7 +57,7 @@ def check(chain, info, lut, code, k, stages, x):
     return worst
 
 
-SMALL = [([(512, 256), (512, 256)], 0), ([(256, 512)], 1), ([(448, 256), (448, 256), (448, 256)], 2),
+SMALL = [([(512, 256), (512, 256)], 0), ([(256, 512)], 1), ([(448, 256), (448, 256), (448, 256)], 0),
          ([(256, 448)], 0), ([(11008, 256)], 0), ([(256, 11008)], 0)]
 
 
