@@ -51,6 +51,19 @@ GROUPS = {
 }
 
 
+# The step is a chain (the model's data flow): the first group of block 0 reads the external x; every
+# later group reads the output of one layer of the previous group -- o reads q's output (a stand-in
+# for attention), gate and up read o's, down reads gate's (a stand-in for silu(gate) * up), the next
+# block's q, k, v read down's.  CHAIN_SRC[workload][g] = index within group g-1 of that layer.
+CHAIN_SRC = {
+    "llama2-7b": [0, 0, 0, 0],
+    "llama2-70b": [0, 0, 0, 0],
+    "c4-70b": [0, 0],
+}
+# code variance over the 2^16 states (R9): scale = 1 / sqrt(n var) keeps |y| ~ |x| along the chain
+CODE_VAR = {"3inst": 1.547, "1mad": 1.0, "hyb": 1.0}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -277,7 +290,8 @@ def run_ours(args):
         tiles = synth.random_tiles(m, n, k, seed=1000 + si)
         sm, sn = synth.random_sign_bytes(m, 3001 + si), synth.random_sign_bytes(n, 3000 + si)
         if world == 1:
-            lay = QTIPLinear(m, n, code=code, k=k, device=dev).load_tiles(tiles, sm, sn, scale=1.0, lut=lut)
+            lay = QTIPLinear(m, n, code=code, k=k, device=dev).load_tiles(tiles, sm, sn, scale=1.0 / np.sqrt(n * CODE_VAR[code]),
+                                                                          lut=lut)
         else:
             lay = ShardedQTIPLinear(m, n, rank, world, code=code, k=k, device=dev).load_tiles(tiles, sm, sn, lut=lut)
         protos[(m, n)] = lay
@@ -307,13 +321,29 @@ def run_ours(args):
     outs = [torch.empty((B, lay.m), dtype=torch.float32, device=dev) for lay in layers]
     step_bytes = sum(m * n * k // 8 for (m, n) in shapes) * nblocks
 
+
+    nl_blk = len(shapes)
     groups = GROUPS[args.workload]
     side = [torch.cuda.Stream(device=dev) for _ in range(max(len(g) for g in groups) - 1)]
+    chained = args.workload in CHAIN_SRC and world == 1
+    src_of = {}                                       # layer index -> layer index whose output it reads
+    if chained:
+        for blk in range(nblocks):
+            for gi, grp in enumerate(groups):
+                if blk == 0 and gi == 0:
+                    continue
+                pg = groups[gi - 1] if gi > 0 else groups[-1]
+                pb = blk if gi > 0 else blk - 1
+                for i in grp:
+                    src_of[blk * nl_blk + i] = pb * nl_blk + pg[CHAIN_SRC[args.workload][gi]]
+
+    def input_of(i):
+        return outs[src_of[i]] if i in src_of else xs[layers[i].n]
 
     def run_layer(i):
         lay, o = layers[i], outs[i]
         if world == 1:
-            lay.forward(xs[lay.n], out=o)
+            lay.forward(input_of(i), out=o)
         else:
             o.copy_(lay.forward(xs[lay.n]))
 
@@ -333,7 +363,7 @@ def run_ours(args):
                         if len(idx) == 1:
                             run_layer(idx[0])
                         else:
-                            forward_group([layers[i] for i in idx], xs[layers[idx[0]].n], outs=[outs[i] for i in idx])
+                            forward_group([layers[i] for i in idx], input_of(idx[0]), outs=[outs[i] for i in idx])
                     if len(parts) == 1:
                         run_part(parts[0])
                         continue
@@ -515,6 +545,66 @@ def run_ours(args):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     h2d = sum(x.numel() * 4 for x in xh.values())
     d2h = yh.numel() * 4
+    layers_path = {"ms_per_step": round(ms, 5), "GBps": round(value, 2), "e2e_ms_per_step": round(e2e_ms, 5),
+                   "step_serial_ms": round(ms_serial, 5), "gemv_only_GBps": round(gemv_gbs, 1),
+                   "launches_per_step": launches_per_step}
+
+    # ---- the chain kernel (impl 8, qtip_chain_run): the whole step -- every layer, its RHT-in, GEMV
+    #      and RHT-out, and the stage hand-offs -- as ONE persistent launch
+    chain_res = None
+    if args.path == "chain" and chained and B <= 16:
+        from paper_2406_11235_b200.layer import QTIPChain
+        cstages = []
+        for blk in range(nblocks):
+            for gi, grp in enumerate(groups):
+                cstages.append(([layers[blk * nl_blk + i] for i in grp], CHAIN_SRC[args.workload][gi]))
+        chain = QTIPChain(cstages, B=B)
+        x0 = xs[layers[0].n]
+        chain(x0)
+        torch.cuda.synchronize()
+        c0 = qtip.launch_count()
+        gch = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(gch, stream=s):
+                chain(x0)
+        torch.cuda.current_stream().wait_stream(s)
+        launches_chain = qtip.launch_count() - c0
+        for _ in range(max(3, args.warmup)):
+            gch.replay()
+        barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            h0.record()
+            for _ in range(args.steps):
+                gch.replay()
+            h1.record()
+            torch.cuda.synchronize()
+        ms_chain = max_over_ranks(h0.elapsed_time(h1) / args.steps)
+        # end to end: pinned H2D of x, the chain, D2H of the last layer's output, all in the timed graph
+        xh0 = torch.from_numpy(synth.random_x(B, layers[0].n, seed=2000 + layers[0].n)).pin_memory()
+        yl = chain.outs[-1][-1]
+        yh0 = torch.empty(tuple(yl.shape), dtype=torch.float32).pin_memory()
+        gce = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(gce, stream=s):
+                x0.copy_(xh0, non_blocking=True)
+                chain(x0)
+                yh0.copy_(yl, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(3):
+            gce.replay()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            gce.replay()
+        f1.record()
+        torch.cuda.synchronize()
+        e2e_chain = max_over_ranks(f0.elapsed_time(f1) / args.steps)
+        chain_res = {"ms": ms_chain, "e2e_ms": e2e_chain, "h2d": xh0.numel() * 4, "d2h": yh0.numel() * 4,
+                     "launches": launches_chain, "stages": len(cstages)}
+        del gch, gce
+        chain.close()
 
     # ---- C4 (BASELINE configs[3]): the 70B layers 8192x28672 and 28672x8192, 3INST k=2, batch 1, row-
     #      sharded over the ranks (all-gather of y~, replicated RHT-out); 4 distinct copies per shape in
@@ -607,6 +697,11 @@ def run_ours(args):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(code, k)
 
+    path = "layers"
+    if chain_res is not None:
+        path = "chain"
+        ms = chain_res["ms"]
+        value = step_bytes / (ms * 1e-3) / 1e9
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     clk_sum = clk.summary()
     clk_mhz = clk_sum.get("sm_mhz") or 1965.0
@@ -622,7 +717,12 @@ def run_ours(args):
                        "code": code, "k": k, "L": 16, "V": 2 if code == "hyb" else 1, "T": 256, "batch": B,
                        "stream_bytes_per_step": step_bytes, "tokens_per_s_equiv": round(B * 1e3 / ms, 2),
                        "per_layer": per_layer, "parallelism": f"rows{world}" if world > 1 else "single",
-                       "dependency": "block: q,k,v and gate,up share an input (one grouped launch per shape, or concurrent streams), groups sequential",
+                       "path": path,
+                       "dependency": ("chain: group g reads the output of one layer of group g-1 (o <- q, gate/up <- o, "
+                                      "down <- gate, next q/k/v <- down); q,k,v and gate,up share an input"
+                                      if chained else "fixed input per shape; groups sequential"),
+                       "layers_path": layers_path,
+                       "chain_stages": chain_res["stages"] if chain_res else None,
                        "grouping": args.grouping,
                        "step_serial_ms": round(ms_serial, 5),
                        "serial_GBps": round(step_bytes / (ms_serial * 1e-3) / 1e9, 2),
@@ -632,12 +732,15 @@ def run_ours(args):
                        "arith": "decoded weights and RHT'd x in binary16, fp32 accumulation"},
             # against the MEASURED HBM copy bandwidth (MEASURED_PEAKS.json): the metric is compressed
             # bytes per second.  The integer-decode bounds of 3INST k=2 are context only.
-            "roofline": {"bound": "hbm", "achieved": round(gemv_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(gemv_gbs / peak, 4),
+            "roofline": {"bound": "hbm", "achieved": round(value if chain_res else gemv_gbs, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round((value if chain_res else gemv_gbs) / peak, 4),
                          "traffic": traffic(args.workload, code, k, qtip.get_matvec_impl()),
-                         "kernel": "fused decode-GEMV launches of the step (grouped where the step groups), back-to-back graph",
+                         "kernel": ("chain_kernel: the step's single persistent launch (decode-GEMV of every layer + "
+                                    "in-kernel RHTs), algorithmic stream bytes / its duration (one ~1 us counter memset "
+                                    "per step included)" if chain_res else
+                                    "fused decode-GEMV launches of the step (grouped where the step groups), back-to-back graph"),
                          "peak_kind": peak_kind,
-                         "us_per_layer": round(1e3 * gemv_ms / (prof_steps * len(layers)), 3),
+                         "us_per_layer": round(1e3 * (ms if chain_res else gemv_ms / prof_steps) / len(layers), 3),
                          # context: the ALU-pipe bound of the 3INST k=2 decode (32 weights/clk/SM: per weight
                          # 1/2 funnel shift + 1/2 shift + 1 LOP3 at 64 lanes/clk/SM) and the measured
                          # decode + mma.sync loop ceiling (scripts/decode_microbench.cu, 19.2 weights/clk/SM)
@@ -648,9 +751,12 @@ def run_ours(args):
                              "frac": round(gemv_gbs / (19.2 * sm_count * clk_mhz * 1e6 * k / 8 / 1e9), 4)})},
             "scaling_70b": scaling_70b,
             "cpu_baseline": cpu,
-            "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 5)},
-            "gpu_launches": launches_per_step * args.steps,
+            "e2e": ({"value": round(step_bytes / (chain_res["e2e_ms"] * 1e-3) / 1e9, 2), "unit": "GB/s",
+                     "h2d_bytes_per_step": chain_res["h2d"], "d2h_bytes_per_step": chain_res["d2h"],
+                     "ms_per_step": round(chain_res["e2e_ms"], 5)} if chain_res else
+                    {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 5)}),
+            "gpu_launches": (chain_res["launches"] if chain_res else launches_per_step) * args.steps,
             "clocks": clk_sum,
         }
         print(json.dumps(line), flush=True)
@@ -688,6 +794,9 @@ def main():
     ap.add_argument("--matvec-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-70b", action="store_true", help="skip the C4 70B-layer block (scaling_70b)")
+    ap.add_argument("--path", default="chain", choices=["chain", "layers"],
+                    help="chain: the whole step as one persistent chain-kernel launch (1 GPU, batch <= 16, chained "
+                         "workloads); layers: per-layer RHT-in / GEMV / RHT-out launches")
     ap.add_argument("--grouping", default="launch", choices=["streams", "launch", "serial"],
                     help="layers of a block that share an input: concurrent streams, one grouped launch, or serial")
     args = ap.parse_args()

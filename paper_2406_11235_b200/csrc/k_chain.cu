@@ -116,9 +116,26 @@ __device__ __forceinline__ int range_of(int U, int W, int u) {
 // Debug progress words (qtip_internal_set_chain_debug; null in normal operation): 8 ints per CTA,
 // written as each role advances (host-mapped memory, read by scripts/chain_debug.py while it runs).
 __device__ int* g_chain_dbg = nullptr;
+__device__ int g_chain_yield = 1;        // decoders pause while a transform task runs (knob)
 #define CDBG(slot, val)                                           \
     do {                                                          \
         if (dbg) *(volatile int*)(dbg + (slot)) = (int)(val);     \
+    } while (0)
+
+// Debug timeline (qtip_internal_set_chain_trace; null in normal operation): %globaltimer ns at
+// [(cta * kTrStages + stage) * 8 + event], stages < kTrStages.  Events: 0 MMA starts waiting for the
+// stage's x~, 1 window landed, 2 last MMA issued, 3 epilogue E(stage) done, 4 first transition task
+// of T(stage+1) starts, 5 T(stage+1) done, 6 decoders' first cell of the stage, 7 producer's first cell.
+constexpr int kTrStages = 160;
+__device__ unsigned long long* g_chain_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define CTR(stage, ev)                                                                          \
+    do {                                                                                        \
+        if (trc && (stage) < kTrStages) trc[((size_t)cta * kTrStages + (stage)) * 8 + (ev)] = gtimer(); \
     } while (0)
 
 // A stage of U cells is cut into W = min(P, U) non-empty ranges; CTA w < W runs range w.
@@ -142,140 +159,347 @@ __device__ __forceinline__ void spin_until(const int* p, int target) {
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// D[i][j] of a transform (sign as +-1.0f): H_b[i_b][j_b] (-1)^popcount(i_1 & j_1), i = i_b 2^a1 + i_1
-__device__ __forceinline__ float dsign(const uint32_t* __restrict__ hb, int b, int a1, int i, int j) {
-    const int ib = i >> a1, jb = j >> a1, m1 = (1 << a1) - 1;
+// D[i][j] of a transform (sign as +-1.0f): H_b[i_b][j_b] (-1)^popcount(i_1 & j_1), i = i_b 2^a1 + i_1;
+// hrow = the H_b bit row of i_b (staged in shared memory).
+__device__ __forceinline__ float dsign(const uint32_t* hrow, int b, int a1, int i, int j) {
+    const int jb = j >> a1, m1 = (1 << a1) - 1;
     uint32_t s = __popc((uint32_t)(i & j & m1)) & 1u;
-    if (b > 1) s ^= (__ldg(hb + (size_t)ib * ((b + 31) >> 5) + (jb >> 5)) >> (jb & 31)) & 1u;
+    if (b > 1) s ^= (hrow[jb >> 5] >> (jb & 31)) & 1u;
     return s ? -1.0f : 1.0f;
+}
+// Stage the H_b bit rows of D rows r0 .. r0+R-1 into hbits[rl * wpr + w] (wpr = ceil(b / 32)).
+__device__ __forceinline__ void stage_hbits(const uint32_t* __restrict__ hb, const Xform& X, int r0, int R,
+                                            uint32_t* hbits, int tid) {
+    if (X.b <= 1) return;
+    const int wpr = (X.b + 31) >> 5;
+    for (int e = tid; e < R * wpr; e += kXfThreads) hbits[e] = __ldg(hb + (size_t)((r0 + e / wpr) >> X.a1) * wpr + e % wpr);
+}
+
+// Scratch layout of a transform task (floats): [ssg: sign bytes n/8][ssg2: the fused source's S_m]
+// [D: L2 <= 32: D^(T) rows as [f][8] floats; L2 >= 128: f floats (one row)][buf: reduction / exchange].
+__host__ __device__ inline int xf_sign_floats(int n) { return ((n / 8 + 15) & ~15) / 4; }
+__host__ __device__ inline int xf_d_floats(const Xform& X) {           // D (+ the staged H_b bit rows)
+    return (X.L2 <= 32 ? 8 * X.f : ((X.f + 3) & ~3)) + ((8 * ((X.b + 31) >> 5) + 3) & ~3);
+}
+__host__ __device__ inline int xf_buf_floats(const Xform& X) {
+    return X.L2 <= 32 ? 8 * 128 : X.L2 + X.L2 / 32;   // small: [slots][R <= 8][L2] partial sums; large: the row (zp)
+}
+
+// Where a task's results go (kept in registers: the layer descriptor itself is a local copy).
+struct XfOut {
+    uint16_t* xt;      // dir 0: x~ (binary16, UMMA B layout, batch pad BP)
+    float* y;          // dir 1: y [B][m]
+    int m, BP, dir;
+};
+// Output element e of batch row bt: x~ or y (S_m applied; the scale is in v).
+__device__ __forceinline__ void xf_store(const XfOut& o, int bt, int e, float v, const uint8_t* sgn) {
+    if (o.dir == 0) {
+        o.xt[(e >> 3) * 8 * o.BP + 8 * bt + (e & 7)] = __half_as_ushort(__float2half_rn(v));
+    } else {
+        o.y[(int64_t)bt * o.m + e] = ((sgn[e >> 3] >> (e & 7)) & 1u) ? -v : v;
+    }
+}
+__device__ __forceinline__ float sgnf(const uint8_t* s, int e, float v) { return ((s[e >> 3] >> (e & 7)) & 1u) ? -v : v; }
+
+// Copy nbytes (even) of sign bytes to shared memory with every load of a batch in flight at once
+// (a loop of load -> store would pay one L2 round trip per iteration).
+__device__ __forceinline__ void stage_signs(uint8_t* dst, const uint8_t* __restrict__ src, int nbytes, int tid) {
+    const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
+    uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+    const int nh = nbytes >> 1;
+    for (int b0 = 0; b0 < nh; b0 += 8 * kXfThreads) {
+        uint16_t t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = b0 + tid + kXfThreads * i;
+            t[i] = e < nh ? __ldg(s16 + e) : (uint16_t)0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = b0 + tid + kXfThreads * i;
+            if (e < nh) d16[e] = t[i];
+        }
+    }
+}
+
+// L2 >= 128 transforms work in shared memory with compact loops: the kernel's SASS is large (the
+// decode templates), and an unrolled register FWHT here runs cold out of the instruction cache at
+// every stage transition (ncu: ~80 % of the task's stalls were instruction fetch).  Element e of a
+// row lives at float zp(e) = e + 4 (e / 128) (16-byte aligned float4 runs; radix-8 passes with
+// h >= 64 are conflict-free, h = 1, 8 at most 4-way).
+__device__ __forceinline__ int zp(int e) { return e + 4 * (e >> 7); }
+
+// In-place FWHT of length L2 (pow2 >= 128) on Z, radix-8 / 4 / 2 passes over 128 threads.
+__device__ void fwht_smem(float* Z, int L2, int tid) {
+    for (int h = 1; h < L2;) {
+        const int rem = L2 / h;
+        const int lv = rem >= 8 ? 3 : rem >= 4 ? 2 : 1;
+        const int r = 1 << lv, ng = L2 >> lv;
+        ptx::named_bar_sync(1, kXfThreads);
+#pragma unroll 1
+        for (int g = tid; g < ng; g += kXfThreads) {
+            const int base = (g / h) * (h * r) + (g % h);
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < r) v[k] = Z[zp(base + k * h)];
+#pragma unroll
+            for (int hh = 1; hh < 8; hh <<= 1)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (hh < r && !(k & hh) && k + hh < r) {
+                        const float p0 = v[k], p1 = v[k + hh];
+                        v[k] = p0 + p1;
+                        v[k + hh] = p0 - p1;
+                    }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < r) Z[zp(base + k * h)] = v[k];
+        }
+        h <<= lv;
+    }
+    ptx::named_bar_sync(1, kXfThreads);
+}
+
+// L2 >= 128, one row (r0) of D per task: Z = sum_j D[r0][j] X[j][.] (input signs applied), FWHT_L2,
+// store.  Fused (Ls != nullptr, pow2 n, f = 1): X is first y_src computed here from the source's y~
+// (inverse FWHT, scale_src S_m,src / sqrt(n)), so the task needs no hand-off.
+__device__ void xf_large(const XfOut& o, const ChainLayerDev& Ld, const ChainLayerDev* Ls, int dir, int bt,
+                         const float* inb, const Xform& X, int r0, const uint32_t* hb, uint8_t* ssg, uint8_t* ssg2,
+                         float* Dsm, float* Z, float fac, int tid, unsigned long long* tt) {
+    const int f = X.f, L2 = X.L2, n = X.n;
+    const int nq = L2 / 4;                               // float4 runs per row
+    const uint8_t* sg = dir ? Ld.sign_m : Ld.sign_n;
+    // every load of the row (float4, coalesced) in flight at once, then into shared memory
+    float4 t[8];
+    if (f == 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = tid + kXfThreads * i;
+            if (q < nq) t[i] = __ldcg(reinterpret_cast<const float4*>(inb) + q);
+        }
+    }
+    stage_signs(ssg, sg, n / 8, tid);
+    if (Ls) stage_signs(ssg2, Ls->sign_m, n / 8, tid);
+    uint32_t* hbits = reinterpret_cast<uint32_t*>(Dsm + ((f + 3) & ~3));
+    stage_hbits(hb, X, r0, 1, hbits, tid);
+    if (f == 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = tid + kXfThreads * i;
+            if (q < nq) *reinterpret_cast<float4*>(Z + zp(4 * q)) = t[i];
+        }
+    }
+    ptx::named_bar_sync(1, kXfThreads);
+    for (int e = tid; e < f; e += kXfThreads) Dsm[e] = dsign(hbits, X.b, X.a1, r0, e);
+    ptx::named_bar_sync(1, kXfThreads);
+    if (tt && tid == 0) tt[1] = gtimer();
+    if (Ls) {
+        // y_src = scale_src S_m,src (H^T y~_src) / sqrt(n); the forward's input is S_n y_src
+        fwht_smem(Z, L2, tid);
+        const float fs = Ls->scale * rsqrtf((float)n);
+#pragma unroll 1
+        for (int e = tid; e < L2; e += kXfThreads) Z[zp(e)] = sgnf(ssg, e, sgnf(ssg2, e, Z[zp(e)] * fs));
+    } else if (f == 1) {
+        const float d0 = Dsm[0];
+        if (dir == 0 || d0 != 1.0f) {
+#pragma unroll 1
+            for (int e = tid; e < L2; e += kXfThreads) Z[zp(e)] = (dir == 0 ? sgnf(ssg, e, Z[zp(e)]) : Z[zp(e)]) * d0;
+        }
+    } else {
+        // Z[c] = sum_j D[j] X[j][c]; thread: float4 runs q of the row, rows j in batches of 4
+#pragma unroll 1
+        for (int q = tid; q < nq; q += kXfThreads) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+            for (int j0 = 0; j0 < f; j0 += 4) {
+                float4 x[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (j0 + i < f) x[i] = __ldcg(reinterpret_cast<const float4*>(inb + (j0 + i) * L2) + q);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (j0 + i < f) {
+                        const int e = (j0 + i) * L2 + 4 * q;
+                        const float d = Dsm[j0 + i];
+                        float4 xv = x[i];
+                        if (dir == 0) {
+                            xv.x = sgnf(ssg, e, xv.x);
+                            xv.y = sgnf(ssg, e + 1, xv.y);
+                            xv.z = sgnf(ssg, e + 2, xv.z);
+                            xv.w = sgnf(ssg, e + 3, xv.w);
+                        }
+                        acc.x = fmaf(d, xv.x, acc.x);
+                        acc.y = fmaf(d, xv.y, acc.y);
+                        acc.z = fmaf(d, xv.z, acc.z);
+                        acc.w = fmaf(d, xv.w, acc.w);
+                    }
+            }
+            *reinterpret_cast<float4*>(Z + zp(4 * q)) = acc;
+        }
+    }
+    if (tt && tid == 0) tt[2] = gtimer();
+    fwht_smem(Z, L2, tid);
+    if (tt && tid == 0) tt[3] = gtimer();
+#pragma unroll 1
+    for (int q = tid; q < nq; q += kXfThreads) {
+        const float4 w = *reinterpret_cast<const float4*>(Z + zp(4 * q));
+        const int e = r0 * L2 + 4 * q;
+        if (o.dir == 0 && o.BP == 1) {
+            const __half2 h01 = __floats2half2_rn(w.x * fac, w.y * fac), h23 = __floats2half2_rn(w.z * fac, w.w * fac);
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t*>(&h01);
+            u.y = *reinterpret_cast<const uint32_t*>(&h23);
+            *reinterpret_cast<uint2*>(o.xt + e) = u;
+        } else if (o.dir == 1) {
+            float4 y;
+            y.x = sgnf(ssg, e, w.x * fac);
+            y.y = sgnf(ssg, e + 1, w.y * fac);
+            y.z = sgnf(ssg, e + 2, w.z * fac);
+            y.w = sgnf(ssg, e + 3, w.w * fac);
+            *reinterpret_cast<float4*>(o.y + (int64_t)bt * o.m + e) = y;
+        } else {
+            xf_store(o, bt, e, w.x * fac, ssg);
+            xf_store(o, bt, e + 1, w.y * fac, ssg);
+            xf_store(o, bt, e + 2, w.z * fac, ssg);
+            xf_store(o, bt, e + 3, w.w * fac, ssg);
+        }
+    }
+    if (tt && tid == 0) tt[4] = gtimer();
+    ptx::named_bar_sync(1, kXfThreads);                  // Z / signs are reused by the next batch row
+}
+
+// L2 <= 32: R <= 8 rows of D per task.  Thread (jslot, c): c = column, the j-slot takes rows j = slot,
+// slot + nslot, ... of X (a warp reads 32 consecutive floats per j), accumulates all R rows (D^T row
+// j of 8 floats, broadcast), in register batches of 32 loads; the slots' partial sums are added in
+// slot order through shared memory, then FWHT_L2 across the lanes and the store.
+__device__ void xf_small(const XfOut& o, const ChainLayerDev& Ld, int dir, int bt, const float* inb, const Xform& X,
+                         int r0, int R, const uint32_t* hb, uint8_t* ssg, float* Dt, float* red, float fac, int tid,
+                         unsigned long long* tt) {
+    const int lane = tid & 31, f = X.f, L2 = X.L2, n = X.n;
+    const uint8_t* sg = dir ? Ld.sign_m : Ld.sign_n;
+    const int c = lane & (L2 - 1);
+    const int nslot = kXfThreads / L2, slot = tid / L2;
+    const int nj = (f - slot + nslot - 1) / nslot;       // this thread's rows of X
+    constexpr int JB = 8;
+    float xa[JB], xb[JB];
+    auto load = [&](float (&xv)[JB], int i0) {
+#pragma unroll
+        for (int i = 0; i < JB; ++i) xv[i] = i0 + i < nj ? __ldcg(inb + (slot + nslot * (i0 + i)) * L2 + c) : 0.0f;
+    };
+    load(xa, 0);
+    stage_signs(ssg, sg, n / 8, tid);
+    uint32_t* hbits = reinterpret_cast<uint32_t*>(Dt + 8 * f);
+    stage_hbits(hb, X, r0, R, hbits, tid);
+    ptx::named_bar_sync(1, kXfThreads);
+    const int wpr = (X.b + 31) >> 5;
+    for (int e = tid; e < 8 * f; e += kXfThreads) {
+        const int j = e >> 3, rl = e & 7;
+        Dt[e] = rl < R ? dsign(hbits + rl * wpr, X.b, X.a1, r0 + rl, j) : 0.0f;
+    }
+    ptx::named_bar_sync(1, kXfThreads);
+    if (tt && tid == 0) tt[1] = gtimer();
+    float acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = 0.0f;
+    auto consume = [&](const float (&xv)[JB], int i0) {
+#pragma unroll
+        for (int i = 0; i < JB; ++i) {
+            if (i0 + i >= nj) break;
+            const int j = slot + nslot * (i0 + i);
+            const float x = dir == 0 ? sgnf(ssg, j * L2 + c, xv[i]) : xv[i];
+            const float4 d0 = *reinterpret_cast<const float4*>(Dt + 8 * j);
+            const float4 d1 = *reinterpret_cast<const float4*>(Dt + 8 * j + 4);
+            acc[0] = fmaf(d0.x, x, acc[0]);
+            acc[1] = fmaf(d0.y, x, acc[1]);
+            acc[2] = fmaf(d0.z, x, acc[2]);
+            acc[3] = fmaf(d0.w, x, acc[3]);
+            acc[4] = fmaf(d1.x, x, acc[4]);
+            acc[5] = fmaf(d1.y, x, acc[5]);
+            acc[6] = fmaf(d1.z, x, acc[6]);
+            acc[7] = fmaf(d1.w, x, acc[7]);
+        }
+    };
+    // two register batches in flight: load batch i+1 while consuming batch i
+    for (int i0 = 0; i0 < nj; i0 += 2 * JB) {
+        if (i0 + JB < nj) load(xb, i0 + JB);
+        consume(xa, i0);
+        if (i0 + 2 * JB < nj) load(xa, i0 + 2 * JB);
+        if (i0 + JB < nj) consume(xb, i0 + JB);
+    }
+    if (tt && tid == 0) tt[2] = gtimer();
+    // partial sums [slot][r][c] -> Z[r][c] = sum over slots in slot order
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        if (r < R) red[(slot * 8 + r) * L2 + c] = acc[r];
+    ptx::named_bar_sync(1, kXfThreads);
+    for (int o0 = 0; o0 < 8 * L2; o0 += kXfThreads) {
+        const int r = (o0 + tid) / L2;
+        float z = 0.0f;
+        if (r < R)
+            for (int sl = 0; sl < nslot; ++sl) z += red[(sl * 8 + r) * L2 + c];
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+            if (s >= L2) break;
+            const float oz = __shfl_xor_sync(0xffffffffu, z, s);
+            z = (lane & s) ? oz - z : z + oz;
+        }
+        if (r < R) xf_store(o, bt, (r0 + r) * L2 + c, z * fac, ssg);
+    }
+    if (tt && tid == 0) tt[3] = tt[4] = gtimer();
+    ptx::named_bar_sync(1, kXfThreads);                  // red / signs are reused by the next batch row
 }
 
 // One transform task on the 128 epilogue threads (tid 0..127, named barrier 1).  dir 0: x~ of
-// layer Ld from its input; dir 1: y of layer Ld from its y~.  sm: scratch (the idle x~ buffer).
-__device__ void run_xform(const ChainArgs& a, const ChainLayerDev& Ld, int dir, int part, float* sm, int tid) {
+// layer Ld from its input (fused: from the source's y~); dir 1: y of layer Ld from its y~.
+// sm: scratch (the idle x~ buffer).  Every global read of a phase is issued before its first use
+// (the inputs live in L2: a chain of dependent L2 round trips, not bandwidth, is what a 16-44 KB
+// transform would otherwise cost).
+__device__ void run_xform(const ChainArgs& a, const ChainLayerDev& Ld, const ChainLayerDev* Ls, int dir, int part,
+                          float* sm, int tid, unsigned long long* tt = nullptr) {
+    if (tt && tid == 0) tt[0] = gtimer();
     const Xform X = dir ? Ld.out : Ld.in;
-    const int L2 = X.L2, f = X.f;
-    const int r0 = part * X.R, R = min(X.R, f - r0);
+    const int n = X.n;
+    const int r0 = part * X.R, R = min(X.R, X.f - r0);
     const float* in;
     int64_t in_stride;
-    const uint8_t* sg_in = nullptr;
-    if (dir == 0) {
+    if (Ls) {
+        in = Ls->yt;
+        in_stride = (int64_t)Ls->n_rb * 128;
+    } else if (dir == 0) {
         in = Ld.src < 0 ? a.x : a.L[Ld.src].y;
-        in_stride = X.n;
-        sg_in = Ld.sign_n;
+        in_stride = n;
     } else {
         in = Ld.yt;
         in_stride = (int64_t)Ld.n_rb * 128;
     }
     const uint32_t* hb = dir ? Ld.hbt_m : Ld.hb_n;
-    const float fac = dir ? Ld.scale * rsqrtf((float)X.n) : rsqrtf((float)X.n);
-    float* Dsm = sm;                                    // [R][f] +-1.0f
-    float* Z = sm + ((R * f + 31) & ~31);               // [R][L2] (L2 >= 128)
-    for (int e = tid; e < R * f; e += kXfThreads) Dsm[e] = dsign(hb, X.b, X.a1, r0 + e / f, e % f);
-    ptx::named_bar_sync(1, kXfThreads);
-    const int lane = tid & 31;
+    const float fac = dir ? Ld.scale * rsqrtf((float)n) : rsqrtf((float)n);
+    uint8_t* ssg = reinterpret_cast<uint8_t*>(sm);
+    uint8_t* ssg2 = reinterpret_cast<uint8_t*>(sm + xf_sign_floats(n));
+    float* Dsm = sm + 2 * xf_sign_floats(n);
+    float* buf = Dsm + xf_d_floats(X);
+    XfOut o;
+    o.xt = Ld.xt;
+    o.y = Ld.y;
+    o.m = Ld.m;
+    o.BP = a.BP;
+    o.dir = dir;
     for (int bt = 0; bt < a.B; ++bt) {
         const float* inb = in + bt * in_stride;
-        if (L2 <= 32) {
-            // lane group of L2 lanes = one row of D at a time; slot = tid / L2
-            const int c = tid & (L2 - 1), slot = tid / L2, nslot = kXfThreads / L2;
-            for (int rl0 = 0; rl0 < R; rl0 += 2 * nslot) {
-                const int ra = rl0 + slot, rb = rl0 + nslot + slot;
-                float za = 0.0f, zb = 0.0f;
-                const float* da = Dsm + (ra < R ? ra : 0) * f;
-                const float* db = Dsm + (rb < R ? rb : 0) * f;
-#pragma unroll 4
-                for (int j = 0; j < f; ++j) {
-                    const int e = j * L2 + c;
-                    float v = __ldcg(inb + e);
-                    if (sg_in) v = ((sg_in[e >> 3] >> (e & 7)) & 1u) ? -v : v;
-                    za = fmaf(da[j], v, za);
-                    zb = fmaf(db[j], v, zb);
-                }
-#pragma unroll
-                for (int s = 1; s < 32; s <<= 1) {
-                    if (s >= L2) break;
-                    const float oa = __shfl_xor_sync(0xffffffffu, za, s), ob = __shfl_xor_sync(0xffffffffu, zb, s);
-                    za = (lane & s) ? oa - za : za + oa;
-                    zb = (lane & s) ? ob - zb : zb + ob;
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int rl = h ? rb : ra;
-                    if (rl >= R) continue;
-                    const int e = (r0 + rl) * L2 + c;
-                    const float v = (h ? zb : za) * fac;
-                    if (dir == 0) {
-                        Ld.xt[(e >> 3) * 8 * a.BP + 8 * bt + (e & 7)] = __half_as_ushort(__float2half_rn(v));
-                    } else {
-                        Ld.y[(int64_t)bt * Ld.m + e] = ((Ld.sign_m[e >> 3] >> (e & 7)) & 1u) ? -v : v;
-                    }
-                }
-            }
+        if (X.L2 <= 32) {
+            xf_small(o, Ld, dir, bt, inb, X, r0, R, hb, ssg, Dsm, buf, fac, tid, tt);
         } else {
-            // thread = column c (mod 128) of each row: accumulate, the 5 lane levels in shuffles
-            for (int idx = tid; idx < R * L2; idx += kXfThreads) {
-                const int rl = idx / L2, c = idx - rl * L2;
-                const float* d = Dsm + rl * f;
-                float z = 0.0f;
-#pragma unroll 4
-                for (int j = 0; j < f; ++j) {
-                    const int e = j * L2 + c;
-                    float v = __ldcg(inb + e);
-                    if (sg_in) v = ((sg_in[e >> 3] >> (e & 7)) & 1u) ? -v : v;
-                    z = fmaf(d[j], v, z);
-                }
-#pragma unroll
-                for (int s = 1; s < 32; s <<= 1) {
-                    const float o = __shfl_xor_sync(0xffffffffu, z, s);
-                    z = (lane & s) ? o - z : z + o;
-                }
-                Z[idx] = z;
-            }
-            // levels h = 32 .. L2/2 in radix-8 / 4 / 2 passes (conflict-free: consecutive g)
-            for (int h = 32; h < L2;) {
-                const int lv = (L2 / h >= 8) ? 3 : (L2 / h >= 4 ? 2 : 1);
-                const int r = 1 << lv;
-                ptx::named_bar_sync(1, kXfThreads);
-                const int ng = R * (L2 >> lv);
-                for (int g = tid; g < ng; g += kXfThreads) {
-                    const int rl = g / (L2 >> lv), q = g - rl * (L2 >> lv);
-                    float* zr = Z + rl * L2 + (q / h) * (h * r) + (q % h);
-                    float v[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (k < r) v[k] = zr[k * h];
-#pragma unroll
-                    for (int hh = 1; hh < 8; hh <<= 1) {
-                        if (hh >= r) break;
-#pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            if (k < r && !(k & hh)) {
-                                const float p0 = v[k], p1 = v[k + hh];
-                                v[k] = p0 + p1;
-                                v[k + hh] = p0 - p1;
-                            }
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (k < r) zr[k * h] = v[k];
-                }
-                h <<= lv;
-            }
-            ptx::named_bar_sync(1, kXfThreads);
-            for (int idx = tid; idx < R * L2; idx += kXfThreads) {
-                const int rl = idx / L2, c = idx - rl * L2;
-                const int e = (r0 + rl) * L2 + c;
-                const float v = Z[idx] * fac;
-                if (dir == 0) {
-                    Ld.xt[(e >> 3) * 8 * a.BP + 8 * bt + (e & 7)] = __half_as_ushort(__float2half_rn(v));
-                } else {
-                    Ld.y[(int64_t)bt * Ld.m + e] = ((Ld.sign_m[e >> 3] >> (e & 7)) & 1u) ? -v : v;
-                }
-            }
-            ptx::named_bar_sync(1, kXfThreads);       // Z is reused by the next batch row
+            xf_large(o, Ld, Ls, dir, bt, inb, X, r0, hb, ssg, ssg2, Dsm, buf, fac, tid, tt);
         }
     }
+    if (tt && tid == 0) tt[5] = gtimer();
+}
+
+// Is layer Ld's x~ computed by one fused task straight from its source's y~ (power-of-two n, one task
+// each way)?  Then it waits for the source's done counter, not for the source's y.
+__device__ __forceinline__ bool xf_fused(const ChainLayerDev& Ld, const ChainLayerDev* L) {
+    return Ld.src >= 0 && Ld.in.f == 1 && Ld.in.L2 >= 128 && L[Ld.src].out.f == 1 && L[Ld.src].out.L2 >= 128;
 }
 
 template <int K, int CODE, bool kImm>
@@ -307,6 +531,8 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
     // transitions done on this CTA (monotonic; an mbarrier's parity could alias when a CTA with
     // empty ranges runs two transitions ahead of its MMA warp)
     volatile int* s_tdone = reinterpret_cast<volatile int*>(smem + 1008);
+    // a transform task is running on this CTA's epilogue warps: the decoders yield the issue slots
+    volatile int* s_xbusy = reinterpret_cast<volatile int*>(smem + 1004);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 1016);
     uint8_t* ring = smem + a.off_ring;
     const int P = (int)gridDim.x;
@@ -315,6 +541,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
     const ChainStageDev* __restrict__ Sd = a.S;
     const ChainLayerDev* __restrict__ Lg = a.L;
     int* const dbg = g_chain_dbg ? g_chain_dbg + 8 * cta : nullptr;
+    unsigned long long* const trc = g_chain_trace;
 
     if constexpr (kHyb) {
         uint4* lt = reinterpret_cast<uint4*>(smem + kCHdr);
@@ -344,6 +571,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
             }
             ptx::fence_mbar_init();
             *s_tdone = 0;
+            *s_xbusy = 0;
         }
         __syncwarp();
         ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
@@ -364,6 +592,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
             int ua, ub;
             cta_range(st.U, P, cta, ua, ub);
             if (ua >= ub) continue;
+            if (lane == 0) CTR(t, 7);
             int li = 0;
             while (li + 1 < st.nl && Lg[st.l0 + li + 1].cum <= ua) ++li;
             int ul = ua - Lg[st.l0 + li].cum;
@@ -371,7 +600,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
             const int64_t cw = kCellBytes / 4;            // words per cell
             const uint32_t* src = Lg[st.l0 + li].packed + (int64_t)ul * cw;
             for (int u = ua; u < ub; ++u) {
-                if (wrapped) ptx::mbar_wait(empty(s), r ^ 1u);
+                if (wrapped) ptx::mbar_wait_sleep(empty(s), r ^ 1u);
                 if (ptx::elect_one()) {
                     ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
                     ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
@@ -406,7 +635,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 __syncwarp();
             }
             if (lane == 0) CDBG(1, 10 * t + 2);
-            if (t >= 2) ptx::mbar_wait(xfree(xb), (uint32_t)(((t - 2) >> 1) & 1));
+            if (t >= 2) ptx::mbar_wait_sleep(xfree(xb), (uint32_t)(((t - 2) >> 1) & 1));
             if (lane == 0) CDBG(1, 10 * t + 3);
             int kcs[kMaxStageLayers], base[kMaxStageLayers];
             int g0 = 0, g1 = -1;
@@ -428,6 +657,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 }
                 bytes = (uint32_t)cum * a.xcol_bytes;
                 if (lane == 0) {
+                    CTR(t, 0);
                     for (int gl = g0; gl <= g1; ++gl) spin_until(a.ctr + 2 * a.nlayers + st.l0 + gl, Lg[st.l0 + gl].in.ntask);
                     fence_proxy_async_global();
                     ptx::fence_proxy_async_smem();
@@ -447,13 +677,14 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 }
                 __syncwarp();
                 if (lane == 0) CDBG(1, 10 * t + 4);
-                ptx::mbar_wait(xfull(xb), (uint32_t)((t >> 1) & 1));
+                ptx::mbar_wait_sleep(xfull(xb), (uint32_t)((t >> 1) & 1));
                 if (lane == 0) CDBG(1, 10 * t + 5);
+                if (lane == 0) CTR(t, 1);
             } else {
                 // keep the window barrier's phases aligned with the stage count
                 if (lane == 0) ptx::mbar_arrive(xfull(xb));
                 __syncwarp();
-                ptx::mbar_wait(xfull(xb), (uint32_t)((t >> 1) & 1));
+                ptx::mbar_wait_sleep(xfull(xb), (uint32_t)((t >> 1) & 1));
             }
             ptx::tc_fence_after();
             if (ua < ub) {
@@ -468,13 +699,13 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 for (int u = ua; u < ub; ++u, ++jj) {
                     if (u == ua || KC == 0) {
                         const int d = seg & 1;
-                        if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
+                        if (seg >= 2) ptx::mbar_wait_sleep(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
                         ptx::tc_fence_after();
                         dcol = tmem + (uint32_t)d * kD1;
                         first = true;
                     }
                     const int g = jj % kCG, lc = jj / kCG, b = lc & (kCNBuf - 1);
-                    ptx::mbar_wait(afull(g, b), (uint32_t)((lc / kCNBuf) & 1));
+                    ptx::mbar_wait_sleep(afull(g, b), (uint32_t)((lc / kCNBuf) & 1));
                     if (lane == 0) CDBG(2, jj);
                     ptx::tc_fence_after();
                     const uint64_t cdesc = ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)(wbase + off) * a.xcol_bytes, a.lbo, a.sbo);
@@ -504,6 +735,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                     }
                 }
             }
+            if (lane == 0) CTR(t, 2);
             if (ptx::elect_one()) ptx::umma_commit(xfree(xb));   // this stage's MMAs read window xb
             __syncwarp();
         }
@@ -537,7 +769,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                         const bool whole = w0 == w1;
                         float* segp = Lg[li].seg + ((int64_t)(w0 - Lg[li].wfirst + RB) * a.BP) * 128 + R;
                         float* dst = segp + (int64_t)(cta - w0) * a.BP * 128;
-                        ptx::mbar_wait(dfull(d), (uint32_t)((seg >> 1) & 1));
+                        ptx::mbar_wait_sleep(dfull(d), (uint32_t)((seg >> 1) & 1));
                         ptx::tc_fence_after();
                         uint32_t rr[16];
                         ptx::tmem_ld16(tl + (uint32_t)d * kD1, rr);
@@ -584,6 +816,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 }
             }
             // ---- T(t): Tout of stage t-1, then Tin of stage t; task j on CTA (j + 7 t) mod P
+            if (t >= 1 && tid == 0) CTR(t - 1, 3);
             {
                 int nto = 0, nti = 0;
                 if (t >= 1)
@@ -594,6 +827,7 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 int j = cta - rot;
                 if (j < 0) j += P;
                 float* scratch = reinterpret_cast<float*>(smem + a.off_x + (uint32_t)((t + 1) & 1) * a.xbuf_bytes);
+                if (t >= 1 && tid == 0 && j < nto + nti) CTR(t - 1, 4);
                 for (; j < nto + nti; j += P) {
                     const int dir = j < nto ? 1 : 0;
                     int jr = dir ? j : j - nto;
@@ -606,21 +840,29 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                         ++li;
                     }
                     const ChainLayerDev Ld = Lg[li];
+                    const bool fused = !dir && xf_fused(Ld, Lg);
                     if (tid == 0) CDBG(3, 100 * t + 10 + dir);
                     if (tid == 0) {
                         if (dir) spin_until(a.ctr + li, Ld.n_rb);
+                        else if (fused) spin_until(a.ctr + Ld.src, Lg[Ld.src].n_rb);
                         else if (Ld.src >= 0) spin_until(a.ctr + a.nlayers + Ld.src, Lg[Ld.src].out.ntask);
                     }
+                    if (tid == 0) *s_xbusy = g_chain_yield;
                     ptx::named_bar_sync(1, kXfThreads);
                     if (tid == 0) CDBG(3, 100 * t + 20 + dir);
-                    run_xform(a, Ld, dir, jr, scratch, tid);
+                    unsigned long long* tt = (trc && t < kTrStages)
+                        ? trc + (size_t)P * kTrStages * 8 + ((size_t)cta * kTrStages + t) * 8 : nullptr;
+                    run_xform(a, Ld, fused ? Lg + Ld.src : nullptr, dir, jr, scratch, tid, tt);
                     if (!dir) fence_proxy_async_global();
                     __threadfence();
+                    if (tt && tid == 0) tt[6] = gtimer();
+                    if (tid == 0) *s_xbusy = 0;
                     ptx::named_bar_sync(1, kXfThreads);
                     if (tid == 0) atomicAdd(a.ctr + (dir ? a.nlayers : 2 * a.nlayers) + li, 1);
                 }
                 ptx::named_bar_sync(1, kXfThreads);
                 if (tid == 0) {
+                    if (t >= 1) CTR(t - 1, 5);
                     __threadfence_block();
                     *s_tdone = t + 1;
                     CDBG(3, 100 * t + 99);
@@ -640,12 +882,30 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
             ncell += ub - ua;
         }
         int lc = 0;
+        int tr_t = 0, tr_end = 0;                      // stage of the current cell (trace only)
+        if (trc) {
+            int ua, ub;
+            cta_range(Sd[0].U, P, cta, ua, ub);
+            tr_end = ub - ua;
+        }
         for (int jj = g; jj < ncell; jj += kCG, ++lc) {
+            if (trc) {
+                bool first = false;
+                while (jj >= tr_end && tr_t + 1 < ns) {
+                    ++tr_t;
+                    int ua, ub;
+                    cta_range(Sd[tr_t].U, P, cta, ua, ub);
+                    tr_end += ub - ua;
+                    first = true;
+                }
+                if (first && g == 0 && q == 0 && lane == 0) CTR(tr_t, 6);
+            }
             const int s = jj % S;
             const uint32_t r = (uint32_t)((jj / S) & 1);
             const int b = lc & (kCNBuf - 1), use = lc / kCNBuf;
-            ptx::mbar_wait(full(s), r);
-            if (use > 0) ptx::mbar_wait(aempty(g, b), (uint32_t)((use - 1) & 1));
+            while (*s_xbusy) __nanosleep(64);
+            ptx::mbar_wait_sleep(full(s), r);
+            if (use > 0) ptx::mbar_wait_sleep(aempty(g, b), (uint32_t)((use - 1) & 1));
             ptx::tc_fence_after();
             const uint32_t* cellw = reinterpret_cast<const uint32_t*>(ring + (size_t)s * kCellBytes);
             const uint32_t ta = ta_lane + (uint32_t)(g * kCNBuf + b) * kACols;
@@ -667,6 +927,21 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
     }
 }
 
+// Debug: one transform task alone (1 CTA, the 128 transform threads), timed with clock64.
+__global__ void __launch_bounds__(kXfThreads, 1) xform_bench_kernel(const __grid_constant__ ChainArgs a, int li, int dir,
+                                                                  int part, int fused, int iters,
+                                                                  unsigned long long* out) {
+    extern __shared__ __align__(16) uint8_t smx[];
+    const int tid = threadIdx.x;
+    const ChainLayerDev Ld = a.L[li];
+    const ChainLayerDev* Ls = fused ? a.L + Ld.src : nullptr;
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) run_xform(a, Ld, Ls, dir, part, reinterpret_cast<float*>(smx), tid);
+    __syncthreads();
+    if (tid == 0) out[0] = clock64() - t0;
+}
+
 template <int K, int CODE, bool kImm>
 cudaError_t launch_chain_t(const ChainArgs& a, int P, size_t smem, cudaStream_t s) {
     auto kern = chain_kernel<K, CODE, kImm>;
@@ -686,7 +961,9 @@ cudaError_t launch_chain_t(const ChainArgs& a, int P, size_t smem, cudaStream_t 
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// Transform geometry over length n (reading R7): see the file comment.
+// Transform geometry over length n (reading R7): see the file comment.  L2 <= 32: rows of D per task
+// so that a transform has about min(64, P/2) tasks; L2 >= 128: one row of D per task (L2 <= 4096,
+// and <= 2048 when D is not trivial, so the row's columns fit 32 registers per thread).
 bool make_xform(int64_t n, int P, Xform* X) {
     int b = 0, a = 0;
     if (!hadamard_factor(n, &b, &a)) return false;
@@ -696,19 +973,14 @@ bool make_xform(int64_t n, int P, Xform* X) {
     X->a1 = a - a2;
     X->L2 = 1 << a2;
     X->f = (int)(n >> a2);
-    // rows per task: about 64 tasks per transform at most (the transition's tasks spread over the
-    // CTAs), and for L2 >= 128 the task's rows of Z must fit the scratch (<= 4096 floats)
     const int target = std::max(1, std::min(64, P / 2));
-    int R = (X->f + target - 1) / target;
-    if (X->L2 >= 128) R = std::min(R, std::max(1, 4096 / X->L2));
-    X->R = std::max(1, R);
+    X->R = X->L2 >= 128 ? 1 : std::min(8, std::max(1, (X->f + target - 1) / target));
     X->ntask = (X->f + X->R - 1) / X->R;
     return true;
 }
 
 size_t xform_scratch_bytes(const Xform& X) {
-    const size_t d = ((size_t)X.R * X.f + 31) & ~size_t(31);
-    return 4 * (d + (X.L2 >= 128 ? (size_t)X.R * X.L2 : 0));
+    return 4 * ((size_t)2 * xf_sign_floats(X.n) + xf_d_floats(X) + xf_buf_floats(X));
 }
 
 }  // namespace
@@ -914,6 +1186,7 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
 
 qtip_status qtip_chain_run(qtip_chain_plan* pl, const float* d_x, void* stream) {
     if (!pl || !d_x) return api_fail(QTIP_ERR_INVALID_PARAMS, "NULL plan or x");
+    if (reinterpret_cast<uintptr_t>(d_x) & 15u) return api_fail(QTIP_ERR_ALIGNMENT, "d_x must be 16-B aligned");
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(pl->ctr, 0, pl->ctr_bytes, s);
     if (e != cudaSuccess) return api_cuda_fail(e, "qtip_chain_run: counters");
@@ -952,6 +1225,24 @@ extern "C" int qtip_internal_chain_buffers(qtip_chain_plan* pl, int i, void** xt
     *xt = pl->xt[i];
     *yt = pl->yt[i];
     return 0;
+}
+
+extern "C" int qtip_internal_chain_xform_bench(qtip_chain_plan* pl, int li, int dir, int part, int fused, int iters,
+                                               void* d_out, void* d_x) {
+    ChainArgs a = pl->args;
+    a.x = (const float*)d_x;
+    cudaFuncSetAttribute(xform_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    xform_bench_kernel<<<1, kXfThreads, 64 * 1024>>>(a, li, dir, part, fused, iters, (unsigned long long*)d_out);
+    return (int)cudaDeviceSynchronize();
+}
+
+extern "C" int qtip_internal_set_chain_yield(int v) {
+    return (int)cudaMemcpyToSymbol(qtip::g_chain_yield, &v, sizeof(v));
+}
+
+extern "C" int qtip_internal_set_chain_trace(void* p) {
+    unsigned long long* q = (unsigned long long*)p;
+    return (int)cudaMemcpyToSymbol(qtip::g_chain_trace, &q, sizeof(q));
 }
 
 extern "C" int qtip_internal_set_chain_debug(void* p) {

@@ -63,6 +63,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// The same wait with a suspend-time hint: a warp that must wait is descheduled until the phase
+// completes (up to the hint, ns) instead of re-issuing try_wait -- blocked warps then leave the issue
+// slots to the warps that have work (the chain kernel's transforms run beside blocked decoders).
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "QTIP_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+        "@!p bra QTIP_WAITS_%=;\n\t}" ::"r"(bar), "r"(parity)
+        : "memory");
+}
+
 // Non-blocking probe: true if the phase with the given parity has completed.
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
     uint32_t ok;
