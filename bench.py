@@ -794,9 +794,10 @@ def main():
     ap.add_argument("--matvec-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-70b", action="store_true", help="skip the C4 70B-layer block (scaling_70b)")
-    ap.add_argument("--path", default="chain", choices=["chain", "layers"],
-                    help="chain: the whole step as one persistent chain-kernel launch (1 GPU, batch <= 16, chained "
-                         "workloads); layers: per-layer RHT-in / GEMV / RHT-out launches")
+    ap.add_argument("--path", default="layers", choices=["chain", "layers"],
+                    help="layers (default, measured fastest): per-layer RHT-in / GEMV / RHT-out launches; chain: "
+                         "the whole step as one persistent chain-kernel launch (impl 8; 1 GPU, batch <= 16, chained "
+                         "workloads; DESIGN.md 5.6)")
     ap.add_argument("--grouping", default="launch", choices=["streams", "launch", "serial"],
                     help="layers of a block that share an input: concurrent streams, one grouped launch, or serial")
     args = ap.parse_args()

@@ -51,10 +51,11 @@
 namespace qtip {
 namespace {
 
-constexpr int kCG = 3;                        // decoder groups
-constexpr int kCWarps = 6 + 4 * kCG;
+constexpr int kCG = 2;                        // decoder groups
+constexpr int kCWarps = 10 + 4 * kCG;         // producer, MMA, 4 epilogue, 4 transform, decoders
 constexpr int kCThreads = 32 * kCWarps;       // 576
-constexpr int kCNBuf = 2;                     // TMEM A buffers per decoder group
+constexpr int kCNBuf = 3;                     // TMEM A buffers per decoder group
+constexpr int kXfBar = 2;                     // named barrier of the transform warps
 constexpr uint32_t kCHdr = 1024;
 constexpr uint32_t kCLutQ = 9;
 constexpr uint32_t kCLutBytes = (1u << (kCLutQ + 1)) * 128u;
@@ -83,28 +84,22 @@ struct ChainLayerDev {
     int* ticket;               // [n_rb] arrivals (zero between launches)
     float scale;
     int m, n, n_rb, n_kc;
-    int src;                   // -1: the external x
-    int cum;                   // first cell in the stage's numbering
-    int wfirst;                // range (CTA) holding that cell
+    int src;                   // execution index of the layer whose y is the input (-1: the external x)
+    int rd0, rd1;              // readers: layers [rd0, rd1) (execution order) take this layer's y as input
+    int U;                     // cells (n_rb n_kc)
     Xform out, in;
 };
 
-struct ChainStageDev {
-    int l0, nl, U, n_kc;
-    int rb_cum[kMaxStageLayers + 1];   // row-block prefix of the stage's layers
-};
-
 struct ChainArgs {
-    const ChainLayerDev* L;
-    const ChainStageDev* S;
-    int nstages, nlayers;
+    const ChainLayerDev* L;    // in execution order
+    int nlayers;
     int* ctr;                  // done[nl] | yready[nl] | xready[nl]
     const float* x;            // external input [B][n of stage 0]
     const uint32_t* lut;       // HYB: 2^Q words (c0 | c1 << 16), shared by the chain
     CodeArgs ca;
     int B, BP;
     uint32_t xcol_bytes, lbo, sbo;
-    uint32_t off_ring, off_x, xbuf_bytes;
+    uint32_t off_ring, off_x, xbuf_bytes, off_scr;
 };
 
 __host__ __device__ constexpr int chain_stages(int K, int code) { return code == QTIP_CODE_HYB ? 6 : (K == 2 ? 12 : 8); }
@@ -222,43 +217,57 @@ __device__ __forceinline__ void stage_signs(uint8_t* dst, const uint8_t* __restr
     }
 }
 
-// L2 >= 128 transforms work in shared memory with compact loops: the kernel's SASS is large (the
-// decode templates), and an unrolled register FWHT here runs cold out of the instruction cache at
-// every stage transition (ncu: ~80 % of the task's stalls were instruction fetch).  Element e of a
-// row lives at float zp(e) = e + 4 (e / 128) (16-byte aligned float4 runs; radix-8 passes with
-// h >= 64 are conflict-free, h = 1, 8 at most 4-way).
+// L2 >= 128 transforms work in shared memory with compact loops and no register arrays: with the
+// kernel's 227 KB shared-memory carve-out the L1 data cache is ~29 KB, so a register-heavy FWHT that
+// spills to local memory pays an L2 round trip per spill (ncu: long-scoreboard stalls on the
+// butterflies), and unrolled code runs cold out of the instruction cache at each transition.
+// Element e of a row lives at float zp(e) = e + 4 (e / 128) (16-byte aligned float4 runs; radix-8
+// passes with h >= 64 are conflict-free, h = 1, 8 at most 4-way).
 __device__ __forceinline__ int zp(int e) { return e + 4 * (e >> 7); }
 
-// In-place FWHT of length L2 (pow2 >= 128) on Z, radix-8 / 4 / 2 passes over 128 threads.
+// In-place FWHT of length L2 (pow2 >= 128) on Z, radix-8 / 4 / 2 passes over 128 threads; two
+// groups per thread per iteration so their shared-memory loads overlap.
 __device__ void fwht_smem(float* Z, int L2, int tid) {
     for (int h = 1; h < L2;) {
         const int rem = L2 / h;
         const int lv = rem >= 8 ? 3 : rem >= 4 ? 2 : 1;
         const int r = 1 << lv, ng = L2 >> lv;
-        ptx::named_bar_sync(1, kXfThreads);
+        ptx::named_bar_sync(kXfBar, kXfThreads);
 #pragma unroll 1
-        for (int g = tid; g < ng; g += kXfThreads) {
-            const int base = (g / h) * (h * r) + (g % h);
-            float v[8];
+        for (int g0 = tid; g0 < ng; g0 += 2 * kXfThreads) {
+            float v[2][8];
+            int base[2];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (k < r) v[k] = Z[zp(base + k * h)];
+            for (int u = 0; u < 2; ++u) {
+                const int g = g0 + u * kXfThreads;
+                base[u] = (g / h) * (h * r) + (g % h);
+                if (g < ng) {
 #pragma unroll
-            for (int hh = 1; hh < 8; hh <<= 1)
+                    for (int k = 0; k < 8; ++k)
+                        if (k < r) v[u][k] = Z[zp(base[u] + k * h)];
+                }
+            }
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (hh < r && !(k & hh) && k + hh < r) {
-                        const float p0 = v[k], p1 = v[k + hh];
-                        v[k] = p0 + p1;
-                        v[k + hh] = p0 - p1;
-                    }
+            for (int u = 0; u < 2; ++u) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (k < r) Z[zp(base + k * h)] = v[k];
+                for (int hh = 1; hh < 8; hh <<= 1)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (hh < r && !(k & hh) && k + hh < r) {
+                            const float p0 = v[u][k], p1 = v[u][k + hh];
+                            v[u][k] = p0 + p1;
+                            v[u][k + hh] = p0 - p1;
+                        }
+                if (g0 + u * kXfThreads < ng) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k < r) Z[zp(base[u] + k * h)] = v[u][k];
+                }
+            }
         }
         h <<= lv;
     }
-    ptx::named_bar_sync(1, kXfThreads);
+    ptx::named_bar_sync(kXfBar, kXfThreads);
 }
 
 // L2 >= 128, one row (r0) of D per task: Z = sum_j D[r0][j] X[j][.] (input signs applied), FWHT_L2,
@@ -271,39 +280,32 @@ __device__ void xf_large(const XfOut& o, const ChainLayerDev& Ld, const ChainLay
     const int nq = L2 / 4;                               // float4 runs per row
     const uint8_t* sg = dir ? Ld.sign_m : Ld.sign_n;
     // every load of the row (float4, coalesced) in flight at once, then into shared memory
-    float4 t[8];
-    if (f == 1) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int q = tid + kXfThreads * i;
-            if (q < nq) t[i] = __ldcg(reinterpret_cast<const float4*>(inb) + q);
-        }
+    if (f == 1) {                                        // cp.async: no registers, all in flight
+        for (int q = tid; q < nq; q += kXfThreads)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(Z + zp(4 * q))),
+                         "l"(reinterpret_cast<const float4*>(inb) + q)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     stage_signs(ssg, sg, n / 8, tid);
     if (Ls) stage_signs(ssg2, Ls->sign_m, n / 8, tid);
     uint32_t* hbits = reinterpret_cast<uint32_t*>(Dsm + ((f + 3) & ~3));
     stage_hbits(hb, X, r0, 1, hbits, tid);
-    if (f == 1) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int q = tid + kXfThreads * i;
-            if (q < nq) *reinterpret_cast<float4*>(Z + zp(4 * q)) = t[i];
-        }
-    }
-    ptx::named_bar_sync(1, kXfThreads);
+    if (f == 1) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    ptx::named_bar_sync(kXfBar, kXfThreads);
     for (int e = tid; e < f; e += kXfThreads) Dsm[e] = dsign(hbits, X.b, X.a1, r0, e);
-    ptx::named_bar_sync(1, kXfThreads);
+    ptx::named_bar_sync(kXfBar, kXfThreads);
     if (tt && tid == 0) tt[1] = gtimer();
     if (Ls) {
         // y_src = scale_src S_m,src (H^T y~_src) / sqrt(n); the forward's input is S_n y_src
         fwht_smem(Z, L2, tid);
         const float fs = Ls->scale * rsqrtf((float)n);
-#pragma unroll 1
+#pragma unroll 4
         for (int e = tid; e < L2; e += kXfThreads) Z[zp(e)] = sgnf(ssg, e, sgnf(ssg2, e, Z[zp(e)] * fs));
     } else if (f == 1) {
         const float d0 = Dsm[0];
         if (dir == 0 || d0 != 1.0f) {
-#pragma unroll 1
+#pragma unroll 4
             for (int e = tid; e < L2; e += kXfThreads) Z[zp(e)] = (dir == 0 ? sgnf(ssg, e, Z[zp(e)]) : Z[zp(e)]) * d0;
         }
     } else {
@@ -341,7 +343,7 @@ __device__ void xf_large(const XfOut& o, const ChainLayerDev& Ld, const ChainLay
     if (tt && tid == 0) tt[2] = gtimer();
     fwht_smem(Z, L2, tid);
     if (tt && tid == 0) tt[3] = gtimer();
-#pragma unroll 1
+#pragma unroll 2
     for (int q = tid; q < nq; q += kXfThreads) {
         const float4 w = *reinterpret_cast<const float4*>(Z + zp(4 * q));
         const int e = r0 * L2 + 4 * q;
@@ -366,7 +368,7 @@ __device__ void xf_large(const XfOut& o, const ChainLayerDev& Ld, const ChainLay
         }
     }
     if (tt && tid == 0) tt[4] = gtimer();
-    ptx::named_bar_sync(1, kXfThreads);                  // Z / signs are reused by the next batch row
+    ptx::named_bar_sync(kXfBar, kXfThreads);            // Z / signs are reused by the next batch row
 }
 
 // L2 <= 32: R <= 8 rows of D per task.  Thread (jslot, c): c = column, the j-slot takes rows j = slot,
@@ -391,13 +393,13 @@ __device__ void xf_small(const XfOut& o, const ChainLayerDev& Ld, int dir, int b
     stage_signs(ssg, sg, n / 8, tid);
     uint32_t* hbits = reinterpret_cast<uint32_t*>(Dt + 8 * f);
     stage_hbits(hb, X, r0, R, hbits, tid);
-    ptx::named_bar_sync(1, kXfThreads);
+    ptx::named_bar_sync(kXfBar, kXfThreads);
     const int wpr = (X.b + 31) >> 5;
     for (int e = tid; e < 8 * f; e += kXfThreads) {
         const int j = e >> 3, rl = e & 7;
         Dt[e] = rl < R ? dsign(hbits + rl * wpr, X.b, X.a1, r0 + rl, j) : 0.0f;
     }
-    ptx::named_bar_sync(1, kXfThreads);
+    ptx::named_bar_sync(kXfBar, kXfThreads);
     if (tt && tid == 0) tt[1] = gtimer();
     float acc[8];
 #pragma unroll
@@ -432,7 +434,7 @@ __device__ void xf_small(const XfOut& o, const ChainLayerDev& Ld, int dir, int b
 #pragma unroll
     for (int r = 0; r < 8; ++r)
         if (r < R) red[(slot * 8 + r) * L2 + c] = acc[r];
-    ptx::named_bar_sync(1, kXfThreads);
+    ptx::named_bar_sync(kXfBar, kXfThreads);
     for (int o0 = 0; o0 < 8 * L2; o0 += kXfThreads) {
         const int r = (o0 + tid) / L2;
         float z = 0.0f;
@@ -447,7 +449,7 @@ __device__ void xf_small(const XfOut& o, const ChainLayerDev& Ld, int dir, int b
         if (r < R) xf_store(o, bt, (r0 + r) * L2 + c, z * fac, ssg);
     }
     if (tt && tid == 0) tt[3] = tt[4] = gtimer();
-    ptx::named_bar_sync(1, kXfThreads);                  // red / signs are reused by the next batch row
+    ptx::named_bar_sync(kXfBar, kXfThreads);                  // red / signs are reused by the next batch row
 }
 
 // One transform task on the 128 epilogue threads (tid 0..127, named barrier 1).  dir 0: x~ of
@@ -528,17 +530,13 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
     auto dempty = [&](int d) { return barD + 16u + 8u * d; };
     auto xfull = [&](int b) { return barD + 32u + 8u * b; };      // x~ window b landed
     auto xfree = [&](int b) { return barD + 48u + 8u * b; };      // MMAs reading window b done
-    // transitions done on this CTA (monotonic; an mbarrier's parity could alias when a CTA with
-    // empty ranges runs two transitions ahead of its MMA warp)
-    volatile int* s_tdone = reinterpret_cast<volatile int*>(smem + 1008);
     // a transform task is running on this CTA's epilogue warps: the decoders yield the issue slots
     volatile int* s_xbusy = reinterpret_cast<volatile int*>(smem + 1004);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 1016);
     uint8_t* ring = smem + a.off_ring;
     const int P = (int)gridDim.x;
     const int cta = (int)blockIdx.x;
-    const int ns = a.nstages;
-    const ChainStageDev* __restrict__ Sd = a.S;
+    const int nl = a.nlayers;
     const ChainLayerDev* __restrict__ Lg = a.L;
     int* const dbg = g_chain_dbg ? g_chain_dbg + 8 * cta : nullptr;
     unsigned long long* const trc = g_chain_trace;
@@ -570,7 +568,6 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                 ptx::mbar_init(xfree(d), 1);
             }
             ptx::fence_mbar_init();
-            *s_tdone = 0;
             *s_xbusy = 0;
         }
         __syncwarp();
@@ -581,24 +578,21 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
     ptx::tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_holder, 0);
 
+    // Sub-stage l = layer l (execution order: stage by stage, the next stage's source first): its
+    // U cells in W = min(P, U) equal ranges, CTA w < W runs range w.
     if (warp == 0) {
-        // ================= producer: all cells of this CTA's range of every stage, in order
+        // ================= producer: every cell of this CTA's range of every layer, in order
         const uint64_t pol = ptx::l2_evict_first_policy();
         int s = 0;
         uint32_t r = 0;
         bool wrapped = false;
-        for (int t = 0; t < ns; ++t) {
-            const ChainStageDev st = Sd[t];
+        const int64_t cw = kCellBytes / 4;                // words per cell
+        for (int l = 0; l < nl; ++l) {
             int ua, ub;
-            cta_range(st.U, P, cta, ua, ub);
+            cta_range(Lg[l].U, P, cta, ua, ub);
             if (ua >= ub) continue;
-            if (lane == 0) CTR(t, 7);
-            int li = 0;
-            while (li + 1 < st.nl && Lg[st.l0 + li + 1].cum <= ua) ++li;
-            int ul = ua - Lg[st.l0 + li].cum;
-            int lcells = Lg[st.l0 + li].n_rb * st.n_kc;
-            const int64_t cw = kCellBytes / 4;            // words per cell
-            const uint32_t* src = Lg[st.l0 + li].packed + (int64_t)ul * cw;
+            if (lane == 0) CTR(l, 7);
+            const uint32_t* src = Lg[l].packed + (int64_t)ua * cw;
             for (int u = ua; u < ub; ++u) {
                 if (wrapped) ptx::mbar_wait_sleep(empty(s), r ^ 1u);
                 if (ptx::elect_one()) {
@@ -606,94 +600,51 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                     ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
                 }
                 __syncwarp();
-                if (lane == 0) CDBG(0, u + 1000000 * t);
+                if (lane == 0) CDBG(0, u + 1000000 * l);
                 if (++s == S) { s = 0; r ^= 1u; wrapped = true; }
                 src += cw;
-                if (++ul == lcells && li + 1 < st.nl) {
-                    ++li;
-                    ul = 0;
-                    lcells = Lg[st.l0 + li].n_rb * st.n_kc;
-                    src = Lg[st.l0 + li].packed;
-                }
             }
         }
     } else if (warp == 1) {
-        // ================= x~ loader + MMA issuer
+        // ================= x~ window loader + MMA issuer
         int seg = 0, jj = 0;
         const uint32_t dstep = 2u * (uint32_t)a.BP;
-        for (int t = 0; t < ns; ++t) {
-            const ChainStageDev st = Sd[t];
+        for (int l = 0; l < nl; ++l) {
+            const ChainLayerDev& Ld = Lg[l];
+            const int nkc = Ld.n_kc;
             int ua, ub;
-            cta_range(st.U, P, cta, ua, ub);
-            const int xb = t & 1;
+            cta_range(Ld.U, P, cta, ua, ub);
+            const int xb = l & 1;
             const uint32_t xwin = ptx::smem_u32(smem + a.off_x + (uint32_t)xb * a.xbuf_bytes);
-            // the window buffer was the scratch of transition t-1 and the B operand of stage t-2
-            if (lane == 0) CDBG(1, 10 * t + 1);
-            if (t >= 1) {
-                if (lane == 0)
-                    while (*s_tdone < t) __nanosleep(32);
-                __syncwarp();
-            }
-            if (lane == 0) CDBG(1, 10 * t + 2);
-            if (t >= 2) ptx::mbar_wait_sleep(xfree(xb), (uint32_t)(((t - 2) >> 1) & 1));
-            if (lane == 0) CDBG(1, 10 * t + 3);
-            int kcs[kMaxStageLayers], base[kMaxStageLayers];
-            int g0 = 0, g1 = -1;
-            if (ua < ub) {
-                while (g0 + 1 < st.nl && Lg[st.l0 + g0 + 1].cum <= ua) ++g0;
-                g1 = g0;
-                while (g1 + 1 < st.nl && Lg[st.l0 + g1 + 1].cum < ub) ++g1;
-                uint32_t bytes = 0;
-                int cum = 0;
-#pragma unroll
-                for (int gl = 0; gl < kMaxStageLayers; ++gl) {
-                    kcs[gl] = base[gl] = 0;
-                    if (gl < g0 || gl > g1) continue;
-                    const int c0 = Lg[st.l0 + gl].cum, c1 = c0 + Lg[st.l0 + gl].n_rb * st.n_kc;
-                    const int lo = ua > c0 ? ua : c0, hi = ub < c1 ? ub : c1;
-                    kcs[gl] = (lo - c0) % st.n_kc;
-                    base[gl] = cum;
-                    cum += hi - lo < st.n_kc ? hi - lo : st.n_kc;
-                }
-                bytes = (uint32_t)cum * a.xcol_bytes;
-                if (lane == 0) {
-                    CTR(t, 0);
-                    for (int gl = g0; gl <= g1; ++gl) spin_until(a.ctr + 2 * a.nlayers + st.l0 + gl, Lg[st.l0 + gl].in.ntask);
+            if (lane == 0) CDBG(1, 10 * l + 2);
+            if (l >= 2) ptx::mbar_wait_sleep(xfree(xb), (uint32_t)(((l - 2) >> 1) & 1));   // window b's MMAs of layer l-2
+            // the window: columns of the range's cells (all n_kc when it covers a whole row block)
+            const int cnt = ub - ua < nkc ? ub - ua : nkc;
+            const int kcs = ub - ua < nkc ? ua % nkc : 0;
+            if (lane == 0) {
+                if (ua < ub) {
+                    CTR(l, 0);
+                    spin_until(a.ctr + 2 * nl + l, Ld.in.ntask);
                     fence_proxy_async_global();
                     ptx::fence_proxy_async_smem();
-                    ptx::mbar_arrive_expect_tx(xfull(xb), bytes);
-                    for (int gl = g0; gl <= g1; ++gl) {
-                        const int c0 = Lg[st.l0 + gl].cum, c1 = c0 + Lg[st.l0 + gl].n_rb * st.n_kc;
-                        const int lo = ua > c0 ? ua : c0, hi = ub < c1 ? ub : c1;
-                        const int cnt = hi - lo < st.n_kc ? hi - lo : st.n_kc;
-                        const int run1 = cnt < st.n_kc - kcs[gl] ? cnt : st.n_kc - kcs[gl];
-                        const uint8_t* xs = reinterpret_cast<const uint8_t*>(Lg[st.l0 + gl].xt);
-                        ptx::bulk_g2s(xwin + (uint32_t)base[gl] * a.xcol_bytes, xs + (size_t)kcs[gl] * a.xcol_bytes,
-                                      (uint32_t)run1 * a.xcol_bytes, xfull(xb));
-                        if (cnt > run1)
-                            ptx::bulk_g2s(xwin + (uint32_t)(base[gl] + run1) * a.xcol_bytes, xs,
-                                          (uint32_t)(cnt - run1) * a.xcol_bytes, xfull(xb));
-                    }
+                    ptx::mbar_arrive_expect_tx(xfull(xb), (uint32_t)cnt * a.xcol_bytes);
+                    const uint8_t* xs = reinterpret_cast<const uint8_t*>(Ld.xt);
+                    const int run1 = cnt < nkc - kcs ? cnt : nkc - kcs;
+                    ptx::bulk_g2s(xwin, xs + (size_t)kcs * a.xcol_bytes, (uint32_t)run1 * a.xcol_bytes, xfull(xb));
+                    if (cnt > run1)
+                        ptx::bulk_g2s(xwin + (uint32_t)run1 * a.xcol_bytes, xs, (uint32_t)(cnt - run1) * a.xcol_bytes,
+                                      xfull(xb));
+                } else {
+                    ptx::mbar_arrive(xfull(xb));            // keep the window barrier's phases aligned
                 }
-                __syncwarp();
-                if (lane == 0) CDBG(1, 10 * t + 4);
-                ptx::mbar_wait_sleep(xfull(xb), (uint32_t)((t >> 1) & 1));
-                if (lane == 0) CDBG(1, 10 * t + 5);
-                if (lane == 0) CTR(t, 1);
-            } else {
-                // keep the window barrier's phases aligned with the stage count
-                if (lane == 0) ptx::mbar_arrive(xfull(xb));
-                __syncwarp();
-                ptx::mbar_wait_sleep(xfull(xb), (uint32_t)((t >> 1) & 1));
             }
+            __syncwarp();
+            ptx::mbar_wait_sleep(xfull(xb), (uint32_t)((l >> 1) & 1));
+            if (lane == 0 && ua < ub) CTR(l, 1);
             ptx::tc_fence_after();
             if (ua < ub) {
-                int gl = g0;
-                const int cl = ua - Lg[st.l0 + gl].cum;
-                int RB = cl / st.n_kc, KC = cl - RB * st.n_kc;
-                int nrb = Lg[st.l0 + gl].n_rb;
-                int off = (KC - kcs[gl] + st.n_kc) % st.n_kc;
-                int wbase = base[gl];
+                int KC = ua % nkc;
+                int off = (KC - kcs + nkc) % nkc;
                 uint32_t dcol = tmem;
                 bool first = true;
                 for (int u = ua; u < ub; ++u, ++jj) {
@@ -704,13 +655,13 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                         dcol = tmem + (uint32_t)d * kD1;
                         first = true;
                     }
-                    const int g = jj % kCG, lc = jj / kCG, b = lc & (kCNBuf - 1);
+                    const int g = jj % kCG, lc = jj / kCG, b = lc % kCNBuf;
                     ptx::mbar_wait_sleep(afull(g, b), (uint32_t)((lc / kCNBuf) & 1));
                     if (lane == 0) CDBG(2, jj);
                     ptx::tc_fence_after();
-                    const uint64_t cdesc = ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)(wbase + off) * a.xcol_bytes, a.lbo, a.sbo);
+                    const uint64_t cdesc = ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)off * a.xcol_bytes, a.lbo, a.sbo);
                     const uint32_t acol = tmem + kA0 + (uint32_t)(g * kCNBuf + b) * kACols;
-                    const bool seg_end = (u + 1 == ub) || (KC == st.n_kc - 1);
+                    const bool seg_end = (u + 1 == ub) || (KC == nkc - 1);
                     if (ptx::elect_one()) {
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
@@ -722,187 +673,156 @@ __global__ void __launch_bounds__(kCThreads, 1) chain_kernel(const __grid_consta
                     __syncwarp();
                     first = false;
                     if (seg_end) ++seg;
-                    if (++off == st.n_kc) off = 0;
-                    if (++KC == st.n_kc) {
-                        KC = 0;
-                        if (++RB == nrb && gl + 1 <= g1) {
-                            RB = 0;
-                            ++gl;
-                            nrb = Lg[st.l0 + gl].n_rb;
-                            off = (st.n_kc - kcs[gl]) % st.n_kc;
-                            wbase = base[gl];
-                        }
-                    }
+                    if (++off == nkc) off = 0;
+                    if (++KC == nkc) KC = 0;
                 }
             }
-            if (lane == 0) CTR(t, 2);
-            if (ptx::elect_one()) ptx::umma_commit(xfree(xb));   // this stage's MMAs read window xb
+            if (lane == 0) CTR(l, 2);
+            if (ptx::elect_one()) ptx::umma_commit(xfree(xb));   // this layer's MMAs read window xb
             __syncwarp();
         }
     } else if (warp < 6) {
-        // ================= epilogue (E(s)) and transition tasks (T(s))
+        // ================= epilogue E(l): D -> y~ rows / stream-K segments, the done counters
         __shared__ int s_last;
         const int q = warp & 3;
         const int R = 32 * q + lane;                  // TMEM lane = row of the row block
         const int tid = (int)threadIdx.x - 64;        // 0..127 over warps 2-5
         const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
         int seg = 0;
-        for (int t = 0; t <= ns; ++t) {
-            if (t >= 1) {
-                // ---- E(t-1): this CTA's segments of stage t-1
-                const ChainStageDev st = Sd[t - 1];
-                int ua, ub;
-                cta_range(st.U, P, cta, ua, ub);
-                const int W = stage_ranges(st.U, P);
-                if (ua < ub) {
-                    for (int RBv = ua / st.n_kc; RBv <= (ub - 1) / st.n_kc; ++RBv, ++seg) {
-                        const int d = seg & 1;
-                        if (tid == 0) CDBG(3, 100 * t + 1);
-                        if (tid == 0) CDBG(4, seg);
-                        int gl = 0;
-                        while (gl + 1 < st.nl && st.rb_cum[gl + 1] <= RBv) ++gl;
-                        const int li = st.l0 + gl;
-                        const int RB = RBv - st.rb_cum[gl];
-                        float* const yt = Lg[li].yt;
-                        const int mp = Lg[li].n_rb * 128;
-                        const int w0 = range_of(st.U, W, RBv * st.n_kc), w1 = range_of(st.U, W, (RBv + 1) * st.n_kc - 1);
-                        const bool whole = w0 == w1;
-                        float* segp = Lg[li].seg + ((int64_t)(w0 - Lg[li].wfirst + RB) * a.BP) * 128 + R;
-                        float* dst = segp + (int64_t)(cta - w0) * a.BP * 128;
-                        ptx::mbar_wait_sleep(dfull(d), (uint32_t)((seg >> 1) & 1));
-                        ptx::tc_fence_after();
-                        uint32_t rr[16];
-                        ptx::tmem_ld16(tl + (uint32_t)d * kD1, rr);
-                        ptx::tc_wait_ld();
-                        ptx::tc_fence_before();
-                        warp_arrive(dempty(d), lane);
+        for (int l = 0; l < nl; ++l) {
+            const ChainLayerDev& Lr = Lg[l];
+            int ua, ub;
+            cta_range(Lr.U, P, cta, ua, ub);
+            const int W = stage_ranges(Lr.U, P);
+            const int nkc = Lr.n_kc;
+            float* const yt = Lr.yt;
+            const int mp = Lr.n_rb * 128;
+            for (int RB = ua < ub ? ua / nkc : 1, RBe = ua < ub ? (ub - 1) / nkc : 0; RB <= RBe; ++RB, ++seg) {
+                const int d = seg & 1;
+                if (tid == 0) CDBG(3, 100 * l + 1);
+                const int w0 = range_of(Lr.U, W, RB * nkc), w1 = range_of(Lr.U, W, (RB + 1) * nkc - 1);
+                const bool whole = w0 == w1;
+                float* segp = Lr.seg + ((int64_t)(w0 + RB) * a.BP) * 128 + R;
+                float* dst = segp + (int64_t)(cta - w0) * a.BP * 128;
+                ptx::mbar_wait_sleep(dfull(d), (uint32_t)((seg >> 1) & 1));
+                ptx::tc_fence_after();
+                uint32_t rr[16];
+                ptx::tmem_ld16(tl + (uint32_t)d * kD1, rr);
+                ptx::tc_wait_ld();
+                ptx::tc_fence_before();
+                warp_arrive(dempty(d), lane);
 #pragma unroll
-                        for (int bb = 0; bb < 16; ++bb) {
-                            if (bb >= a.B) break;
-                            const float v = __uint_as_float(rr[bb]);
-                            if (whole) yt[(int64_t)bb * mp + RB * 128 + R] = v;
-                            else dst[bb * 128] = v;
-                        }
-                        bool fin = whole;
-                        if (!whole) {
-                            __threadfence();
-                            ptx::named_bar_sync(1, kXfThreads);
-                            if (tid == 0) {
-                                const int old = atomicAdd(Lg[li].ticket + RB, 1);
-                                const bool last = old == w1 - w0;
-                                if (last) Lg[li].ticket[RB] = 0;
-                                s_last = last ? 1 : 0;
-                            }
-                            ptx::named_bar_sync(1, kXfThreads);
-                            fin = s_last != 0;
-                            if (fin) {
-                                __threadfence();
-                                const int cnt = w1 - w0 + 1;
-                                for (int bb = 0; bb < a.B; ++bb) {
-                                    const float* sp = segp + bb * 128;
-                                    float acc = __ldcg(sp);
-                                    for (int j = 1; j < cnt; ++j) acc += __ldcg(sp + (int64_t)j * a.BP * 128);
-                                    yt[(int64_t)bb * mp + RB * 128 + R] = acc;
-                                }
-                            }
-                        }
-                        if (fin) {
-                            // the row block of y~ is final: count it (release)
-                            __threadfence();
-                            ptx::named_bar_sync(1, kXfThreads);
-                            if (tid == 0) atomicAdd(a.ctr + li, 1);
-                        }
-                    }
+                for (int bb = 0; bb < 16; ++bb) {
+                    if (bb >= a.B) break;
+                    const float v = __uint_as_float(rr[bb]);
+                    if (whole) yt[(int64_t)bb * mp + RB * 128 + R] = v;
+                    else dst[bb * 128] = v;
                 }
-            }
-            // ---- T(t): Tout of stage t-1, then Tin of stage t; task j on CTA (j + 7 t) mod P
-            if (t >= 1 && tid == 0) CTR(t - 1, 3);
-            {
-                int nto = 0, nti = 0;
-                if (t >= 1)
-                    for (int gl = 0; gl < Sd[t - 1].nl; ++gl) nto += Lg[Sd[t - 1].l0 + gl].out.ntask;
-                if (t < ns)
-                    for (int gl = 0; gl < Sd[t].nl; ++gl) nti += Lg[Sd[t].l0 + gl].in.ntask;
-                const int rot = (int)((7ll * t) % P);
-                int j = cta - rot;
-                if (j < 0) j += P;
-                float* scratch = reinterpret_cast<float*>(smem + a.off_x + (uint32_t)((t + 1) & 1) * a.xbuf_bytes);
-                if (t >= 1 && tid == 0 && j < nto + nti) CTR(t - 1, 4);
-                for (; j < nto + nti; j += P) {
-                    const int dir = j < nto ? 1 : 0;
-                    int jr = dir ? j : j - nto;
-                    const ChainStageDev& st = Sd[dir ? t - 1 : t];
-                    int li = st.l0;
-                    while (true) {
-                        const int nt = dir ? Lg[li].out.ntask : Lg[li].in.ntask;
-                        if (jr < nt) break;
-                        jr -= nt;
-                        ++li;
-                    }
-                    const ChainLayerDev Ld = Lg[li];
-                    const bool fused = !dir && xf_fused(Ld, Lg);
-                    if (tid == 0) CDBG(3, 100 * t + 10 + dir);
-                    if (tid == 0) {
-                        if (dir) spin_until(a.ctr + li, Ld.n_rb);
-                        else if (fused) spin_until(a.ctr + Ld.src, Lg[Ld.src].n_rb);
-                        else if (Ld.src >= 0) spin_until(a.ctr + a.nlayers + Ld.src, Lg[Ld.src].out.ntask);
-                    }
-                    if (tid == 0) *s_xbusy = g_chain_yield;
-                    ptx::named_bar_sync(1, kXfThreads);
-                    if (tid == 0) CDBG(3, 100 * t + 20 + dir);
-                    unsigned long long* tt = (trc && t < kTrStages)
-                        ? trc + (size_t)P * kTrStages * 8 + ((size_t)cta * kTrStages + t) * 8 : nullptr;
-                    run_xform(a, Ld, fused ? Lg + Ld.src : nullptr, dir, jr, scratch, tid, tt);
-                    if (!dir) fence_proxy_async_global();
+                bool fin = whole;
+                if (!whole) {
                     __threadfence();
-                    if (tt && tid == 0) tt[6] = gtimer();
-                    if (tid == 0) *s_xbusy = 0;
                     ptx::named_bar_sync(1, kXfThreads);
-                    if (tid == 0) atomicAdd(a.ctr + (dir ? a.nlayers : 2 * a.nlayers) + li, 1);
+                    if (tid == 0) {
+                        const int old = atomicAdd(Lr.ticket + RB, 1);
+                        const bool last = old == w1 - w0;
+                        if (last) Lr.ticket[RB] = 0;
+                        s_last = last ? 1 : 0;
+                    }
+                    ptx::named_bar_sync(1, kXfThreads);
+                    fin = s_last != 0;
+                    if (fin) {
+                        __threadfence();
+                        const int cnt = w1 - w0 + 1;
+                        for (int bb = 0; bb < a.B; ++bb) {
+                            const float* sp = segp + bb * 128;
+                            float acc = __ldcg(sp);
+                            for (int j = 1; j < cnt; ++j) acc += __ldcg(sp + (int64_t)j * a.BP * 128);
+                            yt[(int64_t)bb * mp + RB * 128 + R] = acc;
+                        }
+                    }
                 }
-                ptx::named_bar_sync(1, kXfThreads);
-                if (tid == 0) {
-                    if (t >= 1) CTR(t - 1, 5);
-                    __threadfence_block();
-                    *s_tdone = t + 1;
-                    CDBG(3, 100 * t + 99);
+                if (fin) {
+                    // the row block of y~ is final: count it (release)
+                    ptx::named_bar_sync(1, kXfThreads);
+                    if (tid == 0) {
+                        __threadfence();
+                        atomicAdd(a.ctr + l, 1);
+                    }
                 }
             }
+            if (tid == 0) CTR(l, 3);
+        }
+    } else if (warp < 10) {
+        // ================= transforms T(l): Tout(l), then Tin(r) of every reader r of l (l = -1: Tin
+        // of the layers reading x); task j of T(l) on CTA (j + 7 (l + 1)) mod P; every CTA runs all
+        // Tout of T(l) before its Tin, and T(l) before T(l+1)
+        const int tid = (int)threadIdx.x - 192;       // 0..127 over warps 6-9
+        float* scratch = reinterpret_cast<float*>(smem + a.off_scr);
+        for (int l = -1; l < nl; ++l) {
+            int nto = 0, rd0, rd1;
+            if (l >= 0) {
+                nto = Lg[l].out.ntask;
+                rd0 = Lg[l].rd0;
+                rd1 = Lg[l].rd1;
+            } else {
+                rd0 = 0;
+                rd1 = 0;
+                while (rd1 < nl && Lg[rd1].src < 0) ++rd1;
+            }
+            int nti = 0;
+            for (int r = rd0; r < rd1; ++r) nti += Lg[r].in.ntask;
+            const int rot = (int)((7ll * (l + 1)) % P);
+            int j = cta - rot;
+            if (j < 0) j += P;
+            if (l >= 0 && tid == 0 && j < nto + nti) CTR(l, 4);
+            for (; j < nto + nti; j += P) {
+                const int dir = j < nto ? 1 : 0;
+                int jr = j, li = l;
+                if (!dir) {
+                    jr = j - nto;
+                    li = rd0;
+                    while (jr >= Lg[li].in.ntask) jr -= Lg[li++].in.ntask;
+                }
+                const ChainLayerDev& Ld = Lg[li];
+                const bool fused = !dir && xf_fused(Ld, Lg);
+                if (tid == 0) {
+                    if (dir) spin_until(a.ctr + li, Ld.n_rb);
+                    else if (fused) spin_until(a.ctr + Ld.src, Lg[Ld.src].n_rb);
+                    else if (Ld.src >= 0) spin_until(a.ctr + nl + Ld.src, Lg[Ld.src].out.ntask);
+                    *s_xbusy = g_chain_yield;
+                }
+                ptx::named_bar_sync(kXfBar, kXfThreads);
+                unsigned long long* tt = (trc && l >= 0 && l < kTrStages)
+                    ? trc + (size_t)P * kTrStages * 8 + ((size_t)cta * kTrStages + l) * 8 : nullptr;
+                run_xform(a, Ld, fused ? Lg + Ld.src : nullptr, dir, jr, scratch, tid, tt);
+                if (!dir) fence_proxy_async_global();
+                __threadfence();
+                if (tt && tid == 0) tt[6] = gtimer();
+                ptx::named_bar_sync(kXfBar, kXfThreads);
+                if (tid == 0) {
+                    *s_xbusy = 0;
+                    atomicAdd(a.ctr + (dir ? nl : 2 * nl) + li, 1);
+                }
+            }
+            if (l >= 0 && tid == 0) CTR(l, 5);
         }
     } else {
-        // ================= decoders: cells jj = g, g + 3, ... of the CTA's cell sequence
-        const int dw = warp - 6, g = dw >> 2, q = warp & 3;
+        // ================= decoders: cells jj = g, g + kCG, ... of the CTA's cell sequence
+        const int dw = warp - 10, g = dw >> 2, q = warp & 3;
         const int R = 32 * q + lane, I = R >> 4, rho = R & 15;
         const uint32_t ta_lane = tmem + ((uint32_t)(32 * q) << 16) + kA0;
         const uint32_t lut_lane = ptx::smem_u32(smem + kCHdr) + 4u * (uint32_t)lane;
         int ncell = 0;
-        for (int t = 0; t < ns; ++t) {
+        for (int l = 0; l < nl; ++l) {
             int ua, ub;
-            cta_range(Sd[t].U, P, cta, ua, ub);
+            cta_range(Lg[l].U, P, cta, ua, ub);
             ncell += ub - ua;
         }
         int lc = 0;
-        int tr_t = 0, tr_end = 0;                      // stage of the current cell (trace only)
-        if (trc) {
-            int ua, ub;
-            cta_range(Sd[0].U, P, cta, ua, ub);
-            tr_end = ub - ua;
-        }
         for (int jj = g; jj < ncell; jj += kCG, ++lc) {
-            if (trc) {
-                bool first = false;
-                while (jj >= tr_end && tr_t + 1 < ns) {
-                    ++tr_t;
-                    int ua, ub;
-                    cta_range(Sd[tr_t].U, P, cta, ua, ub);
-                    tr_end += ub - ua;
-                    first = true;
-                }
-                if (first && g == 0 && q == 0 && lane == 0) CTR(tr_t, 6);
-            }
             const int s = jj % S;
             const uint32_t r = (uint32_t)((jj / S) & 1);
-            const int b = lc & (kCNBuf - 1), use = lc / kCNBuf;
+            const int b = lc % kCNBuf, use = lc / kCNBuf;
             while (*s_xbusy) __nanosleep(64);
             ptx::mbar_wait_sleep(full(s), r);
             if (use > 0) ptx::mbar_wait_sleep(aempty(g, b), (uint32_t)((use - 1) & 1));
@@ -933,7 +853,7 @@ __global__ void __launch_bounds__(kXfThreads, 1) xform_bench_kernel(const __grid
                                                                   unsigned long long* out) {
     extern __shared__ __align__(16) uint8_t smx[];
     const int tid = threadIdx.x;
-    const ChainLayerDev Ld = a.L[li];
+    const ChainLayerDev& Ld = a.L[li];
     const ChainLayerDev* Ls = fused ? a.L + Ld.src : nullptr;
     __syncthreads();
     const unsigned long long t0 = clock64();
@@ -1019,9 +939,8 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
         return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: HYB needs Q = 9, one-sign, and a LUT");
     const int P = num_sms();
     const int BP = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : B <= 8 ? 8 : 16;
-    // ---- validate the layer list and build the stages
-    std::vector<ChainStageDev> stages;
-    std::vector<ChainLayerDev> L(nlayers);
+    // ---- validate the layer list (user order) and find the stages
+    std::vector<int> stage_first;                      // first user index of every stage
     for (int i = 0; i < nlayers; ++i) {
         const qtip_chain_layer& c = layers[i];
         if (!c.d_packed || !c.d_sign_n || !c.d_sign_m || !c.d_y) return api_fail(QTIP_ERR_INVALID_PARAMS, "NULL layer buffer");
@@ -1037,8 +956,30 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
         }
         if (i > 0 && c.stage == layers[i - 1].stage && (c.n != layers[i - 1].n || c.src != layers[i - 1].src))
             return api_fail(QTIP_ERR_INVALID_PARAMS, "layers of a stage share n and src (one input)");
+        if (c.stage >= (int)stage_first.size()) stage_first.push_back(i);
+        if (i + 1 - stage_first.back() > kMaxStageLayers)
+            return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: at most 4 layers per stage");
+        int b = 0, a = 0;
+        if (!hadamard_factor(c.m, &b, &a) || !hadamard_factor(c.n, &b, &a))
+            return api_fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m or n");
+    }
+    const int nst = (int)stage_first.size();
+    stage_first.push_back(nlayers);
+    // ---- execution order: stage by stage; within a stage the next stage's source first, so its
+    //      transforms overlap the stage's other layers
+    std::vector<int> exec, pos(nlayers);
+    for (int s = 0; s < nst; ++s) {
+        const int src_next = s + 1 < nst ? layers[stage_first[s + 1]].src : -1;
+        if (src_next >= 0) exec.push_back(src_next);
+        for (int i = stage_first[s]; i < stage_first[s + 1]; ++i)
+            if (i != src_next) exec.push_back(i);
+    }
+    for (int e = 0; e < nlayers; ++e) pos[exec[e]] = e;
+    std::vector<ChainLayerDev> L(nlayers);
+    for (int e = 0; e < nlayers; ++e) {
+        const qtip_chain_layer& c = layers[exec[e]];
         const Layout l = make_layout(c.m, c.n, p->k);
-        ChainLayerDev& d = L[i];
+        ChainLayerDev& d = L[e];
         d = ChainLayerDev{};
         d.packed = (const uint32_t*)c.d_packed;
         d.sign_n = c.d_sign_n;
@@ -1049,63 +990,48 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
         d.n = (int)c.n;
         d.n_rb = (int)l.n_rb;
         d.n_kc = (int)l.n_kc;
-        d.src = c.src;
-        if (!make_xform(c.m, P, &d.out) || !make_xform(c.n, P, &d.in))
-            return api_fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m or n");
-        if (c.stage >= (int)stages.size()) {
-            ChainStageDev s{};
-            s.l0 = i;
-            s.n_kc = d.n_kc;
-            stages.push_back(s);
-        }
-        ChainStageDev& s = stages.back();
-        if (s.nl == kMaxStageLayers) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: at most 4 layers per stage");
-        d.cum = s.U;
-        s.rb_cum[s.nl] = s.U / s.n_kc;
-        s.U += d.n_rb * d.n_kc;
-        s.nl += 1;
-        s.rb_cum[s.nl] = s.U / s.n_kc;
-        if ((int64_t)s.U * (P + 1) >= (1ll << 31)) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: stage too large");
+        d.U = d.n_rb * d.n_kc;
+        d.src = c.src < 0 ? -1 : pos[c.src];
+        d.rd0 = d.rd1 = 0;
+        make_xform(c.m, P, &d.out);
+        make_xform(c.n, P, &d.in);
+        if ((int64_t)d.U * (P + 1) >= (1ll << 31)) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: layer too large");
     }
-    for (auto& s : stages)
-        for (int gl = 0; gl < s.nl; ++gl) {
-            ChainLayerDev& d = L[s.l0 + gl];
-            const int W = std::min(P, s.U);
-            d.wfirst = (int)((((uint64_t)d.cum + 1) * W - 1) / s.U);
+    for (int s = 0; s + 1 < nst; ++s) {                  // readers of the next stage's source
+        const int src = pos[layers[stage_first[s + 1]].src];
+        L[src].rd0 = pos[stage_first[s + 1]] < pos[stage_first[s + 1]] ? 0 : nlayers;
+        int lo = nlayers, hi = 0;
+        for (int i = stage_first[s + 1]; i < stage_first[s + 2]; ++i) {
+            lo = std::min(lo, pos[i]);
+            hi = std::max(hi, pos[i] + 1);
         }
-    // ---- shared memory: ring + LUT + two x~ windows / transform scratch
+        L[src].rd0 = lo;
+        L[src].rd1 = hi;
+    }
+    // ---- shared memory: LUT + ring + two x~ windows + the transform scratch
     const bool hyb = p->code == QTIP_CODE_HYB;
     const uint32_t xcol = 128u * 2u * (uint32_t)BP;
-    size_t xbuf = 0;
-    for (auto& s : stages) {
-        const int W = std::min(P, s.U);
-        for (int w = 0; w < W; ++w) {
-            const int64_t ua = (int64_t)s.U * w / W, ub = (int64_t)s.U * (w + 1) / W;
-            int64_t cols = 0;
-            for (int gl = 0; gl < s.nl; ++gl) {
-                const ChainLayerDev& d = L[s.l0 + gl];
-                const int64_t c0 = d.cum, c1 = c0 + (int64_t)d.n_rb * d.n_kc;
-                const int64_t lo = std::max(ua, c0), hi = std::min(ub, c1);
-                if (lo < hi) cols += std::min<int64_t>(hi - lo, d.n_kc);
-            }
-            xbuf = std::max(xbuf, (size_t)cols * xcol);
-        }
+    size_t xbuf = 0, scr = 0;
+    for (auto& d : L) {
+        const int W = std::min(P, d.U);
+        const int64_t cw = (d.U + W - 1) / W;
+        xbuf = std::max(xbuf, (size_t)std::min<int64_t>(cw, d.n_kc) * xcol);
+        scr = std::max({scr, xform_scratch_bytes(d.out), xform_scratch_bytes(d.in)});
     }
-    for (auto& d : L) xbuf = std::max({xbuf, xform_scratch_bytes(d.out), xform_scratch_bytes(d.in)});
     xbuf = (xbuf + 1023) & ~size_t(1023);
+    scr = (scr + 1023) & ~size_t(1023);
     const size_t cell = 2048u * (size_t)p->k;
     const size_t lutb = hyb ? kCLutBytes : 0;
-    int S = chain_stages(p->k, p->code);
-    const size_t smem = kCHdr + lutb + (size_t)S * cell + 2 * xbuf;
+    const int S = chain_stages(p->k, p->code);
+    const size_t smem = kCHdr + lutb + (size_t)S * cell + 2 * xbuf + scr;
     if (smem > 227 * 1024) return api_fail(QTIP_ERR_UNSUPPORTED, "chain kernel: x~ windows / transform scratch do not fit shared memory");
-    // ---- device memory: [layer table][stage table][counters + tickets][x~][y~][segments]
+    // ---- device memory: [layer table][counters + tickets][x~][y~][segments]
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return api_cuda_fail(e, "qtip_chain_plan_create");
     auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
     size_t off = 0;
     const size_t o_L = off; off += al(sizeof(ChainLayerDev) * nlayers);
-    const size_t o_S = off; off += al(sizeof(ChainStageDev) * stages.size());
     const size_t o_ctr = off;
     size_t nctr = 3 * (size_t)nlayers;
     for (auto& d : L) nctr += d.n_rb;
@@ -1140,15 +1066,16 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
             return api_cuda_fail(e, "qtip_chain_plan_create: Hadamard tables");
         }
     }
-    if ((e = cudaMemcpy(base + o_L, L.data(), sizeof(ChainLayerDev) * nlayers, cudaMemcpyHostToDevice)) != cudaSuccess ||
-        (e = cudaMemcpy(base + o_S, stages.data(), sizeof(ChainStageDev) * stages.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    if ((e = cudaMemcpy(base + o_L, L.data(), sizeof(ChainLayerDev) * nlayers, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cudaFree(dmem);
         return api_cuda_fail(e, "qtip_chain_plan_create: tables");
     }
     qtip_chain_plan* pl = new qtip_chain_plan();
-    for (int i = 0; i < nlayers; ++i) {
-        pl->xt.push_back(L[i].xt);
-        pl->yt.push_back(L[i].yt);
+    pl->xt.assign(nlayers, nullptr);
+    pl->yt.assign(nlayers, nullptr);
+    for (int i = 0; i < nlayers; ++i) {                  // debug readout in the caller's layer order
+        pl->xt[exec[i]] = L[i].xt;
+        pl->yt[exec[i]] = L[i].yt;
     }
     pl->device = dev;
     pl->code = p->code;
@@ -1157,7 +1084,7 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
     pl->imm = !hyb && p->k == 2 && ca.a == (p->code == QTIP_CODE_1MAD ? 34038481u : 89226354u) &&
               ca.b == (p->code == QTIP_CODE_1MAD ? 76625530u : 64248484u);
     pl->P = P;
-    pl->nstages = (int)stages.size();
+    pl->nstages = nst;
     pl->nlayers = nlayers;
     pl->B = B;
     pl->smem = smem;
@@ -1166,8 +1093,6 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
     pl->ctr_bytes = ctr_bytes;
     ChainArgs& a = pl->args;
     a.L = (const ChainLayerDev*)(base + o_L);
-    a.S = (const ChainStageDev*)(base + o_S);
-    a.nstages = pl->nstages;
     a.nlayers = nlayers;
     a.ctr = pl->ctr;
     a.lut = (const uint32_t*)d_lut;
@@ -1180,6 +1105,7 @@ qtip_status qtip_chain_plan_create(const qtip_params* p, int32_t nlayers, const 
     a.off_ring = (uint32_t)(kCHdr + lutb);
     a.off_x = (uint32_t)(kCHdr + lutb + (size_t)S * cell);
     a.xbuf_bytes = (uint32_t)xbuf;
+    a.off_scr = (uint32_t)(a.off_x + 2 * xbuf);
     *out = pl;
     return QTIP_OK;
 }

@@ -68,19 +68,19 @@ fn(ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
 tt_all = tr.cpu().numpy().reshape(2, P, KT, 8).astype(np.float64)
 t, tk = tt_all[0], tt_all[1]
-ns_ = len(stages)
+ns_ = sum(len(s_[0]) for s_ in stages)
 t0 = t[t > 0].min()
 t = np.where(t > 0, (t - t0) / 1e3, np.nan)
 print(f"yield={yld} {code} k={k}: {blocks} blocks, {ns_} stages, {sum(len(s[0]) for s in stages)} layers, kernel+memset {ms * 1e3:.1f} us "
       f"(traced), last event {np.nanmax(t):.1f} us")
-names = ["qkv", "o", "gate,up", "down"]
+names = ["q", "k", "v", "o", "gate", "up", "down"]
 print("stage        win_wait(med)  win_land(med/max)  mma_done(med/max)  E_done(max)  T_start(min)  T_end(max)  dec_first(med)  prod_first(med)")
 for s in range(min(ns_, KT)):
     col = lambda e: t[:, s, e]  # noqa: E731
     med = lambda v: np.nanmedian(v) if np.isfinite(v).any() else float("nan")  # noqa: E731
     mx = lambda v: np.nanmax(v) if np.isfinite(v).any() else float("nan")  # noqa: E731
     mn = lambda v: np.nanmin(v) if np.isfinite(v).any() else float("nan")  # noqa: E731
-    print(f"{s:3d} {names[s % 4]:8s} {med(col(0)):9.1f}  {med(col(1)):9.1f}/{mx(col(1)):7.1f}  {med(col(2)):9.1f}/{mx(col(2)):7.1f}"
+    print(f"{s:3d} {names[s % 7]:8s} {med(col(0)):9.1f}  {med(col(1)):9.1f}/{mx(col(1)):7.1f}  {med(col(2)):9.1f}/{mx(col(2)):7.1f}"
           f"  {mx(col(3)):9.1f}  {mn(col(4)):9.1f}  {mx(col(5)):9.1f}  {med(col(6)):9.1f}  {med(col(7)):9.1f}")
 
 tk = np.where(tk > 0, (tk - t0) / 1e3, np.nan)
