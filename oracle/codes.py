@@ -11,6 +11,10 @@ Paper passages:
   P:298-321             HYB: x <- x*x + x mod 2^32; v <- C[(x >> (15-Q)) & (2^Q - 1)];
                         v <- v XOR (x & (1 << 15)); "two sign flip" also XORs bit 31.
   P:309                 LUT initialised by k-means on 2-D i.i.d. Gaussian samples.
+  P:607-609             HYB with a 1-D codebook (Q = 6, V = 1): the same hash, index and sign
+                        flip with a 2^Q-entry table of single values (v XOR (x & (1 << 15))).
+  P:751-798             lookup-only code: the value of state x is LUT[x], a 2^L-entry table
+                        (L = 14, V = 1, T_x = 32, T_y = 8; "~ N(0, 1)", tunable).
 
 Output precision readings:
   * 1MAD returns the IEEE binary16 round-to-nearest-even of the exact rational
@@ -177,6 +181,23 @@ def decode_hyb(x, lut, Q, two_sign=False):
                     axis=-1)
 
 
+def decode_hyb1(x, lut1, Q):
+    """HYB with a 1-D codebook (V = 1): Alg. 3's hash and index, lut1 uint16 (2^Q,)
+    binary16 patterns; the value's sign bit is XORed with bit 15 of the hash (P:317 with a
+    16-bit v).  Returns uint16 (...)."""
+    lut1 = np.asarray(lut1, dtype=np.uint16)
+    h = hyb_hash(x)
+    idx = hyb_index(h, Q)
+    return (lut1[idx].astype(np.uint64) ^ (h & np.uint64(1 << 15))).astype(np.uint16)
+
+
+def decode_lut(x, lut):
+    """Lookup-only code: the value of state x (L bits) is lut[x]; lut uint16
+    (2^L,) binary16 patterns.  Returns uint16 (...)."""
+    lut = np.asarray(lut, dtype=np.uint16)
+    return lut[np.asarray(x, dtype=np.int64)]
+
+
 def kmeans_lut(Q, seed=4000, n_samples=1 << 18, iters=40):
     """k-means (Lloyd) with 2^Q centroids on i.i.d. N(0, I_2) samples.
     Deterministic given seed; init = a random subset of the samples; an empty cluster
@@ -215,6 +236,10 @@ def code_table(code, L, lut=None, Q=9, two_sign=False):
         return f16_to_f64(decode_3inst(xs))
     if code == "hyb":
         return f16_to_f64(decode_hyb(xs, lut, Q, two_sign))
+    if code == "hyb1":
+        return f16_to_f64(decode_hyb1(xs, lut, Q))
+    if code == "lut":
+        return f16_to_f64(decode_lut(xs, lut))
     raise ValueError(code)
 
 

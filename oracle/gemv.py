@@ -7,8 +7,10 @@ Paper passages:
   P:121-123  the reconstruction concatenates node values along the walk (V values per node).
   P:96-97    RHT: W = S_m H_m^T W~ H_n S_n (orthonormal H), see oracle.rht.
 
+  P:787-791  the lookup-only code uses T_x = 32, T_y = 8 blocks: position p = 8 r + c.
+
 The plain definition this module writes out:
-    W~[16I + r, 16J + c] = code(state_p(tile I,J)),  p = 16 r + c   (V = 1)
+    W~[T_x I + r, T_y J + c] = code(state_p(tile I,J)),  p = T_y r + c   (V = 1)
     (W~[.., 2t], W~[.., 2t+1]) = code(state_t)                       (V = 2, HYB)
     y = scale * S_m H_m^T W~ H_n S_n x   evaluated in float64.
 Logical tile format: kT bits, MSB-first (oracle.trellis), i.e. 32k bytes per tile,
@@ -28,11 +30,13 @@ class Params:
     L: int = 16
     k: int = 2
     V: int = 1
-    code: str = "3inst"          # "1mad" | "3inst" | "hyb"
+    code: str = "3inst"          # "1mad" | "3inst" | "hyb" (V = 2) | "hyb1" (HYB, V = 1) | "lut"
     Q: int = 9
-    lut: np.ndarray = None       # uint16 (2^Q, 2) for HYB
+    lut: np.ndarray = None       # uint16 (2^Q, 2) for HYB, (2^Q,) for hyb1, (2^L,) for lut
     two_sign: bool = False
     tail_biting: bool = True
+    Tx: int = 16
+    Ty: int = 16
 
 
 def tile_values(tile_bytes, p: Params):
@@ -45,17 +49,21 @@ def tile_values(tile_bytes, p: Params):
     elif p.code == "hyb":
         v = codes.f16_to_f64(codes.decode_hyb(st.astype(np.uint64), p.lut, p.Q, p.two_sign))
         v = v.reshape(v.shape[:-2] + (T,))                         # (t, 2) -> positions 2t, 2t+1
+    elif p.code == "hyb1":
+        v = codes.f16_to_f64(codes.decode_hyb1(st.astype(np.uint64), p.lut, p.Q))
+    elif p.code == "lut":
+        v = codes.f16_to_f64(codes.decode_lut(st, p.lut))
     else:
         raise ValueError(p.code)
     return v
 
 
 def dense_decode(tiles, p: Params):
-    """tiles: uint8 (m/16, n/16, 32k) -> float64 W~ (m, n) (exact fp16 values)."""
+    """tiles: uint8 (m/Tx, n/Ty, 32k) -> float64 W~ (m, n) (exact fp16 values)."""
     tiles = np.asarray(tiles, dtype=np.uint8)
     mt, nt = tiles.shape[:2]
-    v = tile_values(tiles, p).reshape(mt, nt, TX, TY)               # [I, J, r, c]
-    return v.transpose(0, 2, 1, 3).reshape(mt * TX, nt * TY)
+    v = tile_values(tiles, p).reshape(mt, nt, p.Tx, p.Ty)           # [I, J, r, c]
+    return v.transpose(0, 2, 1, 3).reshape(mt * p.Tx, nt * p.Ty)
 
 
 def decode_rows(tiles, p: Params, rows):
@@ -63,8 +71,8 @@ def decode_rows(tiles, p: Params, rows):
     tiles = np.asarray(tiles, dtype=np.uint8)
     out = []
     for i in rows:
-        I, r = divmod(int(i), TX)
-        v = tile_values(tiles[I], p).reshape(-1, TX, TY)            # [J, r, c]
+        I, r = divmod(int(i), p.Tx)
+        v = tile_values(tiles[I], p).reshape(-1, p.Tx, p.Ty)        # [J, r, c]
         out.append(v[:, r, :].reshape(-1))
     return np.stack(out)
 

@@ -18,10 +18,10 @@ def tile_bytes(k, T=256):
     return k * T // 8
 
 
-def random_tiles(m, n, k, seed=1000):
-    """uint8 (m/16, n/16, 32k): logical tail-biting tile streams, MSB-first."""
+def random_tiles(m, n, k, seed=1000, Tx=TILE, Ty=TILE):
+    """uint8 (m/Tx, n/Ty, 32k): logical tail-biting tile streams (T = Tx Ty = 256), MSB-first."""
     rng = np.random.default_rng(seed)
-    return rng.integers(0, 256, size=(m // TILE, n // TILE, tile_bytes(k)), dtype=np.uint8)
+    return rng.integers(0, 256, size=(m // Tx, n // Ty, tile_bytes(k)), dtype=np.uint8)
 
 
 def random_x(B, n, seed=2000):
@@ -41,6 +41,13 @@ def gaussian_lut(Q, seed=4000):
     LUT; the k-means LUT of P:309 lives in oracle.codes)."""
     rng = np.random.default_rng(seed)
     return rng.standard_normal((1 << Q, 2)).astype(np.float16).view(np.uint16)
+
+
+def gaussian_table(nbits, seed=4001):
+    """A (2^nbits,) binary16 table of i.i.d. N(0, 1) draws: the 1-D codebook of HYB with V = 1
+     or the lookup-only code's 2^L table ("~ N(0, 1)")."""
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal(1 << nbits).astype(np.float16).view(np.uint16)
 
 
 def gaussian_source(nseq, T, seed=5000):
