@@ -48,24 +48,29 @@ typedef enum {
     QTIP_ERR_WORKSPACE = -7       /* workspace too small (see qtip_matvec_workspace_bytes)   */
 } qtip_status;
 
-typedef enum { QTIP_CODE_1MAD = 1, QTIP_CODE_3INST = 2, QTIP_CODE_HYB = 3 } qtip_code;
+/* QTIP_CODE_LUT: the lookup-only code: value of state x = LUT[x], a 2^L-entry
+ * binary16 table (L = 14: 32 KB), V = 1, blocks T_x x T_y = 32 x 8 or 16 x 16. */
+typedef enum { QTIP_CODE_1MAD = 1, QTIP_CODE_3INST = 2, QTIP_CODE_HYB = 3, QTIP_CODE_LUT = 4 } qtip_code;
 
 /* Trellis + code parameters (PAPER.md:121 (L,k,V); :260, :267 LCG constants; :303 Q). */
 typedef struct {
-    int32_t L;            /* state bits; the device path supports L = 16          */
+    int32_t L;            /* state bits: 16; the LUT code takes kV <= L <= 16 (14) */
     int32_t k;            /* bits per weight, 1..4 (device path: 2, 3, 4)                         */
-    int32_t V;            /* values per trellis step: 1 for 1MAD/3INST, 2 for HYB                 */
+    int32_t V;            /* values per trellis step: 1 for 1MAD/3INST/LUT; HYB 2, or 1 with a 1-D  */
+                          /* codebook (Q = 6, V = 1)                                    */
     int32_t code;         /* qtip_code                                                            */
-    int32_t Q;            /* HYB LUT index bits; 9 -> 2 KiB table; must be 9      */
+    int32_t Q;            /* HYB LUT index bits; 9 -> 2 KiB table; V = 1: 1..14    */
     int32_t tail_biting;  /* must be 1: kT bits per tile                              */
-    int32_t Tx, Ty;       /* must be 16, 16 (T = 256, one 16x16 tile per sequence)     */
+    int32_t Tx, Ty;       /* 16, 16 (T = 256, one 16x16 tile per sequence); the LUT code */
+                          /* also 32, 8; m must then be a multiple of 32               */
     uint32_t lcg_a;       /* 1MAD: 34038481; 3INST: 89226354                      */
     uint32_t lcg_b;       /* 1MAD: 76625530;         3INST: 64248484                              */
     uint32_t m_fp16;      /* 3INST magic m as binary16 bits: 0x3B60 = fp16(0.922)  */
     int32_t hyb_two_sign; /* HYB: also XOR bit 31; default 0 (the paper's numbers)    */
 } qtip_params;
 
-/* Fill *p with the paper's defaults for `code` at k bits (L=16, V=1 or 2, Q=9, T=16x16). */
+/* Fill *p with the paper's defaults for `code` at k bits (L=16, V=1 or 2, Q=9, T=16x16; the LUT
+ * code: L = 14, V = 1, T = 32x8). */
 void qtip_params_default(qtip_params* p, int32_t code, int32_t k);
 
 /* Validate *p for the device path.  QTIP_OK or QTIP_ERR_INVALID_PARAMS/UNSUPPORTED. */
@@ -90,7 +95,8 @@ qtip_status qtip_pack_states(const qtip_params* p, int64_t m, int64_t n, const u
                              void* d_packed, void* stream);
 
 /* Dense RHT-domain weights W~ (raw code values, no scale; P:123 reconstruction).
- *   d_lut: HYB only, DEVICE uint16[2^Q][2] binary16 (c0, c1) pairs (else NULL).
+ *   d_lut: HYB, DEVICE uint16[2^Q][2] binary16 (c0, c1) pairs; HYB with V = 1: uint16[2^Q];
+ *     the LUT code: uint16[2^L]; NULL for 1MAD/3INST.  (16-byte aligned for the matvec.)
  *   out_dtype 0: binary16 (normative, bit-exact vs the oracle); 1: float32 = exact widening.
  *   d_out: DEVICE [m][n] row-major. */
 qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* d_packed,

@@ -31,6 +31,12 @@ qtip_status cuda_fail(cudaError_t e, const char* where) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// m, n multiples of the block (16 x 16, or T_x x T_y for the LUT code)
+qtip_status check_block(const qtip_params* p, int64_t m, int64_t n) {
+    if (m % p->Tx || n % p->Ty) return fail(QTIP_ERR_SHAPE, "m, n must be multiples of T_x, T_y");
+    return QTIP_OK;
+}
+
 CodeArgs code_args(const qtip_params* p) {
     CodeArgs c;
     c.a = p->lcg_a;
@@ -92,20 +98,34 @@ void qtip_params_default(qtip_params* p, int32_t code, int32_t k) {
     if (code == QTIP_CODE_3INST) { p->lcg_a = 89226354u; p->lcg_b = 64248484u; }
     p->m_fp16 = 0x3B60u;                                                            // fp16(0.922)
     p->hyb_two_sign = 0;
+    if (code == QTIP_CODE_LUT) {
+        p->L = 14;
+        p->Tx = 32;
+        p->Ty = 8;
+    }
 }
 
 qtip_status qtip_params_check(const qtip_params* p) {
     if (!p) return fail(QTIP_ERR_INVALID_PARAMS, "params is NULL");
-    if (p->code != QTIP_CODE_1MAD && p->code != QTIP_CODE_3INST && p->code != QTIP_CODE_HYB)
+    if (p->code != QTIP_CODE_1MAD && p->code != QTIP_CODE_3INST && p->code != QTIP_CODE_HYB && p->code != QTIP_CODE_LUT)
         return fail(QTIP_ERR_INVALID_PARAMS, "unknown code");
     if (p->k < 1 || p->k > 4) return fail(QTIP_ERR_INVALID_PARAMS, "k must be in 1..4");
-    if ((p->code == QTIP_CODE_HYB) != (p->V == 2) || (p->V != 1 && p->V != 2))
-        return fail(QTIP_ERR_INVALID_PARAMS, "1MAD/3INST need V=1, HYB needs V=2");
+    if (p->V != 1 && p->V != 2) return fail(QTIP_ERR_INVALID_PARAMS, "V must be 1 or 2");
+    if (p->code != QTIP_CODE_HYB && p->V != 1) return fail(QTIP_ERR_INVALID_PARAMS, "1MAD/3INST/LUT need V=1, HYB V=2 (or 1)");
     if (p->L < p->k * p->V || p->L > 32) return fail(QTIP_ERR_INVALID_PARAMS, "need kV <= L <= 32");
     if (p->code == QTIP_CODE_HYB && (p->Q < 1 || p->Q > 15)) return fail(QTIP_ERR_INVALID_PARAMS, "HYB needs 1 <= Q <= 15");
-    if (p->L != 16) return fail(QTIP_ERR_UNSUPPORTED, "device path implements L = 16 (PAPER.md:415, :573)");
+    if (p->Tx * p->Ty != 256 || p->Tx < 1 || p->Ty < 1) return fail(QTIP_ERR_INVALID_PARAMS, "need Tx * Ty = T = 256");
     if (!p->tail_biting) return fail(QTIP_ERR_UNSUPPORTED, "device path needs tail-biting tiles (kT bits)");
-    if (p->Tx != 16 || p->Ty != 16) return fail(QTIP_ERR_UNSUPPORTED, "device path needs Tx = Ty = 16");
+    if (p->code == QTIP_CODE_LUT) {
+        if (p->L > 16) return fail(QTIP_ERR_UNSUPPORTED, "LUT code: L <= 16 (a 2^L binary16 table in shared memory)");
+        if (!((p->Tx == 16 && p->Ty == 16) || (p->Tx == 32 && p->Ty == 8)))
+            return fail(QTIP_ERR_UNSUPPORTED, "LUT code: T_x x T_y = 16 x 16 or 32 x 8 (PAPER.md:787)");
+        return QTIP_OK;
+    }
+    if (p->L != 16) return fail(QTIP_ERR_UNSUPPORTED, "device path implements L = 16 (PAPER.md:415, :573)");
+    if (p->Tx != 16 || p->Ty != 16) return fail(QTIP_ERR_UNSUPPORTED, "device path needs Tx = Ty = 16 (32 x 8: the LUT code)");
+    if (p->code == QTIP_CODE_HYB && p->V == 1 && (p->Q > 14 || p->hyb_two_sign))
+        return fail(QTIP_ERR_UNSUPPORTED, "HYB with V = 1: Q <= 14, one sign (PAPER.md:607-609)");
     return QTIP_OK;
 }
 
@@ -122,17 +142,22 @@ qtip_status qtip_pack(const qtip_params* p, int64_t m, int64_t n, const uint8_t*
     if ((st = check_shape(m, n)) != QTIP_OK) return st;
     if (!h_tiles || !d_packed) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
     if (!aligned16(d_packed)) return fail(QTIP_ERR_ALIGNMENT, "d_packed must be 16-byte aligned");
+    if ((st = check_block(p, m, n)) != QTIP_OK) return st;
     const Layout l = make_layout(m, n, p->k);
     const int64_t tile_bytes = 4 * l.tw;
-    const int64_t mt = m / kTile, nt = n / kTile;
+    // T_x x T_y blocks: block (I_l, J_l) of a cell goes to slot s = I_l (128 / T_y) + J_l, stored at
+    // the 16 x 16 position (s / 8, s % 8) (for 16 x 16 blocks: (I_l, J_l) itself)
+    const int cr = kCellRows / p->Tx, cc = kCellCols / p->Ty;
+    const int64_t mt = m / p->Tx, nt = n / p->Ty;
     std::vector<uint32_t> buf((size_t)(l.n_rb * l.n_kc * l.cell_words), 0u);
     auto work = [&](int64_t t0, int64_t t1) {
         for (int64_t Ig = t0; Ig < t1; ++Ig) {
-            const int64_t RB = Ig / kCellTileRows;
-            const int I = (int)(Ig % kCellTileRows);
+            const int64_t RB = Ig / cr;
+            const int Il = (int)(Ig % cr);
             for (int64_t Jg = 0; Jg < nt; ++Jg) {
-                const int64_t KC = Jg / kCellTileCols;
-                const int J = (int)(Jg % kCellTileCols);
+                const int64_t KC = Jg / cc;
+                const int slot = Il * cc + (int)(Jg % cc);
+                const int I = slot >> 3, J = slot & 7;
                 const uint8_t* src = h_tiles + (Ig * nt + Jg) * tile_bytes;
                 uint32_t* cell = buf.data() + (RB * l.n_kc + KC) * l.cell_words;
                 for (int w = 0; w < l.tw; ++w) {
@@ -167,7 +192,8 @@ qtip_status qtip_pack_states(const qtip_params* p, int64_t m, int64_t n, const u
     const int L = p->L, kv = p->k * p->V, steps = 256 / p->V;
     const uint32_t lmask = (L == 32) ? 0xFFFFFFFFu : ((1u << L) - 1u);
     const uint32_t omask = (1u << (L - kv)) - 1u;
-    const int64_t ntiles = (m / kTile) * (n / kTile);
+    if ((st = check_block(p, m, n)) != QTIP_OK) return st;
+    const int64_t ntiles = (m / p->Tx) * (n / p->Ty);
     const int tile_bytes = p->k * 32;
     std::vector<uint8_t> bytes((size_t)(ntiles * tile_bytes), 0);
     for (int64_t t = 0; t < ntiles; ++t) {
@@ -194,10 +220,17 @@ qtip_status qtip_decode(const qtip_params* p, int64_t m, int64_t n, const void* 
     qtip_status st = qtip_params_check(p);
     if (st != QTIP_OK) return st;
     if ((st = check_shape(m, n)) != QTIP_OK) return st;
-    if (!d_packed || !d_out || (p->code == QTIP_CODE_HYB && !d_lut)) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (!d_packed || !d_out || ((p->code == QTIP_CODE_HYB || p->code == QTIP_CODE_LUT) && !d_lut))
+        return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
     if (out_dtype != 0 && out_dtype != 1) return fail(QTIP_ERR_INVALID_PARAMS, "out_dtype must be 0 or 1");
     if (!aligned16(d_packed) || !aligned16(d_out)) return fail(QTIP_ERR_ALIGNMENT, "buffers must be 16-byte aligned");
+    if ((st = check_block(p, m, n)) != QTIP_OK) return st;
     const Layout l = make_layout(m, n, p->k);
+    if (is_variant(p)) {
+        const cudaError_t ev = launch_variant_decode(p, l, d_packed, d_lut, out_dtype, d_out, (cudaStream_t)stream);
+        if (ev != cudaSuccess) return cuda_fail(ev, "qtip_decode");
+        return QTIP_OK;
+    }
     cudaError_t e = launch_decode(l, p->code, p->V, code_args(p), d_packed, d_lut, out_dtype, d_out, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_decode");
     return QTIP_OK;
@@ -259,6 +292,7 @@ static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
 int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B) {
     if (G < 2 || G > kMaxGroup || qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1 || B > 64)
         return 0;
+    if (is_variant(p)) return 0;                                   // per-layer calls (k_variant.cu)
     const Layout l = make_layout(m, n, p->k);
     if (use_umma(p, l, B, G)) return 1;
     if (!(g_impl == 0 || g_impl == 6)) return 0;
@@ -426,7 +460,7 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     if ((st = check_shape(m, n)) != QTIP_OK) return st;
     if (B < 1 || B > 64) return fail(QTIP_ERR_INVALID_PARAMS, "batch must be in 1..64");
     if (flags & ~(QTIP_RHT_IN | QTIP_RHT_OUT | QTIP_XT_READY)) return fail(QTIP_ERR_INVALID_PARAMS, "unknown flags");
-    if (!d_packed || !d_x || !d_y || !d_workspace || (p->code == QTIP_CODE_HYB && !d_lut))
+    if (!d_packed || !d_x || !d_y || !d_workspace || ((p->code == QTIP_CODE_HYB || p->code == QTIP_CODE_LUT) && !d_lut))
         return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
     if (((flags & QTIP_RHT_IN) && !(flags & QTIP_XT_READY) && !d_sign_n) || ((flags & QTIP_RHT_OUT) && !d_sign_m))
         return fail(QTIP_ERR_INVALID_PARAMS, "NULL sign vector");
@@ -454,6 +488,36 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const bool rin = (flags & QTIP_RHT_IN) != 0, rout = (flags & QTIP_RHT_OUT) != 0;
     const int64_t rb0 = row_begin / kCellRows, rb1 = (row_end + kCellRows - 1) / kCellRows;
     cudaError_t e;
+    if (is_variant(p)) {
+        // the NEXT-3 code variants (k_variant.cu): RHT-in -> fused decode-GEMV with the whole table
+        // in shared memory -> fixed-order split-K reduction -> RHT-out
+        if ((st = check_block(p, m, n)) != QTIP_OK) return st;
+        if (variant_gemv_smem(p, B) > 227 * 1024) return fail(QTIP_ERR_UNSUPPORTED, "table + x~ slice exceed shared memory");
+        float* vpart = (float*)(ws + o.partial);
+        float* vyt = (float*)(ws + o.yt);
+        e = cudaSuccess;
+        if (!(flags & QTIP_XT_READY)) {
+            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, 0, l.n_pad);
+            else e = launch_convert(d_x, n, n, B, xt, l.n_pad, 0, l.n_pad, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
+        const bool prof = g_prof_start && g_prof_stop;
+        if (prof) record_event(g_prof_start, s);
+        e = launch_variant_gemv(p, l, d_packed, d_lut, (const float*)xt, B, rb0, rb1, vpart, s);
+        if (prof) {
+            record_event(g_prof_stop, s);
+            g_prof_start = g_prof_stop = nullptr;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec variant gemv");
+        if (rout) {
+            e = launch_reduce(vpart, l.n_kc, B, l.m_pad, 0, m, 1.0f, vyt, l.m_pad, s);
+            if (e == cudaSuccess) e = launch_rht(pm, B, d_sign_m, vyt, l.m_pad, d_y, m, 1, scale, s);
+        } else {
+            e = launch_reduce(vpart, l.n_kc, B, l.m_pad, row_begin, row_end, scale, d_y, row_end - row_begin, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec epilogue");
+        return QTIP_OK;
+    }
     const bool umma_ok = umma_supported(l, p->code, ca, B, 1);
     if (g_impl == 7 && !umma_ok)
         return fail(QTIP_ERR_UNSUPPORTED, "tcgen05 stream-K kernel: needs 2 <= k <= 4, B <= 64, HYB Q = 9 one-sign");

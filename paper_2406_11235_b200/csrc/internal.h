@@ -179,6 +179,16 @@ cudaError_t launch_umma(const Layout& lay, int code, const CodeArgs& ca, int G, 
                         float* const* yout, const float* yscale, int64_t ys, int64_t rows, int64_t B, int64_t rb0,
                         int64_t rb1, cudaStream_t s);
 
+// The code variants of NEXT-3 (k_variant.cu): the lookup-only code and HYB with V = 1.  Decode, and
+// the fused decode-GEMV partial[kc][b][row] over row blocks [rb0, rb1) with x~ float32 (row stride
+// n_pad); the whole table is staged in shared memory (variant_gemv_smem bytes).
+bool is_variant(const qtip_params* p);
+cudaError_t launch_variant_decode(const qtip_params* p, const Layout& lay, const void* packed, const uint16_t* lut,
+                                  int out_f32, void* out, cudaStream_t s);
+cudaError_t launch_variant_gemv(const qtip_params* p, const Layout& lay, const void* packed, const uint16_t* lut,
+                                const float* xt, int64_t B, int64_t rb0, int64_t rb1, float* partial, cudaStream_t s);
+size_t variant_gemv_smem(const qtip_params* p, int64_t B);
+
 // Tail-biting trellis quantizer (k_viterbi.cu): Algorithm 4 per sequence of T source values (in
 // code units), binary32 DP.  ws: viterbi_workspace_bytes(T) bytes (backpointers, per CTA).
 bool viterbi_supported(int code, int k, int V, int L, int Q, int two_sign);

@@ -27,14 +27,14 @@ class QTIPLinear:
 
     # ------------------------------------------------------------------ loading
     def load_tiles(self, tiles, sign_m, sign_n, scale=1.0, lut=None):
-        """tiles: numpy uint8 (m/16, n/16, 32k) logical tail-biting streams; signs: bit-packed
-        numpy uint8; lut: numpy uint16 (2^Q, 2) binary16 (HYB only)."""
+        """tiles: numpy uint8 (m/Tx, n/Ty, 32k) logical tail-biting streams; signs: bit-packed
+        numpy uint8; lut: numpy uint16 binary16 -- (2^Q, 2) for HYB, (2^Q,) for "hyb1", (2^L,) for "lut"."""
         qtip.qtip_pack(self.p, self.m, self.n, tiles, self.packed)
         self.sign_m.copy_(torch.from_numpy(np.ascontiguousarray(sign_m, dtype=np.uint8)))
         self.sign_n.copy_(torch.from_numpy(np.ascontiguousarray(sign_n, dtype=np.uint8)))
-        if self.code == "hyb":
+        if self.code in ("hyb", "hyb1", "lut"):
             if lut is None:
-                raise ValueError("HYB needs a LUT")
+                raise ValueError(f"{self.code} needs a LUT")
             self.lut = torch.from_numpy(np.ascontiguousarray(lut, dtype=np.uint16).view(np.int16)).to(self.device)
         self.scale = float(scale)
         return self

@@ -14,8 +14,11 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libqtip.so")
 
-QTIP_CODE_1MAD, QTIP_CODE_3INST, QTIP_CODE_HYB = 1, 2, 3
-CODES = {"1mad": QTIP_CODE_1MAD, "3inst": QTIP_CODE_3INST, "hyb": QTIP_CODE_HYB}
+QTIP_CODE_1MAD, QTIP_CODE_3INST, QTIP_CODE_HYB, QTIP_CODE_LUT = 1, 2, 3, 4
+# "hyb1": HYB with a 1-D codebook (V = 1, Q = 6); "lut": the lookup-only code
+# (L = 14, V = 1, T_x x T_y = 32 x 8)
+CODES = {"1mad": QTIP_CODE_1MAD, "3inst": QTIP_CODE_3INST, "hyb": QTIP_CODE_HYB, "hyb1": QTIP_CODE_HYB,
+         "lut": QTIP_CODE_LUT}
 QTIP_RHT_IN, QTIP_RHT_OUT = 1, 2
 QTIP_XT_READY = 4          # kernel benchmarking: reuse the x~ already in the workspace
 IMPL_AUTO, IMPL_SIMPLE, IMPL_TC, IMPL_MMA = 0, 1, 2, 3
@@ -149,6 +152,8 @@ class Config:
         p = QtipParams()
         load().qtip_params_default(ctypes.byref(p), CODES[self.code], self.k)
         p.hyb_two_sign = int(self.two_sign)
+        if self.code == "hyb1":
+            p.V, p.Q = 1, 6
         return p
 
 

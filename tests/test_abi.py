@@ -50,6 +50,8 @@ def test_params_check_errors(lib):
     assert qtip.params_check(p) == -1
     p = qtip.params_default("hyb", 4)
     p.V = 1
+    assert qtip.params_check(p) == 0             # HYB with a 1-D codebook, k_variant.cu
+    p.V = 3
     assert qtip.params_check(p) == -1
     p = qtip.params_default("3inst", 2)
     p.L = 12
@@ -204,3 +206,30 @@ def test_chain_plan_validation(lib):
     assert lib.qtip_chain_run(None, None, None) == -1
     lib.qtip_chain_plan_destroy(None)
     assert lib.qtip_chain_plan_stages(None) == 0
+
+
+def test_params_check_code_variants(lib):
+    """NEXT-3 variants: the lookup-only code (L <= 16, 16x16 or 32x8 blocks) and HYB with V = 1."""
+    p = qtip.params_default("lut", 2)
+    assert (p.L, p.V, p.Tx, p.Ty, p.code) == (14, 1, 32, 8, 4)
+    assert qtip.params_check(p) == 0
+    p.Tx, p.Ty = 16, 16
+    assert qtip.params_check(p) == 0
+    p.Tx, p.Ty = 64, 4
+    assert qtip.params_check(p) == -5
+    p.Tx, p.Ty = 32, 16
+    assert qtip.params_check(p) == -1                         # T = Tx Ty must be 256
+    p = qtip.params_default("lut", 2)
+    p.L = 17
+    assert qtip.params_check(p) == -5
+    p = qtip.params_default("hyb1", 2)
+    assert (p.V, p.Q, p.code) == (1, 6, 3) and qtip.params_check(p) == 0
+    p.Q = 15
+    assert qtip.params_check(p) == -5
+    p = qtip.params_default("3inst", 2)
+    p.Tx, p.Ty = 32, 8
+    assert qtip.params_check(p) == -5                         # 32 x 8 blocks: the LUT code only
+    # 32 x 8 blocks need m % 32 == 0
+    p = qtip.params_default("lut", 2)
+    assert lib.qtip_pack(ctypes.byref(p), 48, 64, np.zeros(64 * 48 // 256 * 64, np.uint8).ctypes.data_as(ctypes.c_void_p),
+                         ctypes.c_void_p(16), None) == -2
