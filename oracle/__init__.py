@@ -24,4 +24,6 @@ Modules
   gemv      dense decode of a packed matrix + float64 y = W x
   viterbi   Viterbi DP, constrained DP + Alg. 4 tail-biting,
             brute force.  DP core in plain C (viterbi.c).
+  ldlq      BlockLDLQ with QTIP rounding (Algorithm 5): T_y-block LDL, error feedback,
+            synthetic AR(1) proxy Hessians.
 """
