@@ -219,7 +219,7 @@ qtip_status qtip_hadamard_order(int64_t n, int32_t* b, int32_t* a);
  * (reading R3: bottom L-kV bits of the rotated walk's state at 1-indexed group floor(T/(2V))),
  * then run the Viterbi on the original sequence with the first state's top and the last state's
  * bottom L-kV bits both equal to O (a tail-biting walk).
- *   p: L = 16 and either 3INST/1MAD with V = 1, k in {2, 3}, or HYB with V = 2, k in {2, 3, 4},
+ *   p: L = 16 and either 3INST/1MAD with V = 1, k in {2, 3, 4}, or HYB with V = 2, k in {2, 3, 4},
  *     Q = 9, one-sign (else QTIP_ERR_UNSUPPORTED).  T % V == 0.
  *   d_source: DEVICE float32 [nseq][T], already in code units (the caller scales the source by
  *     the code's state standard deviation, reading R9); d_lut: HYB table as for qtip_decode (DEVICE

@@ -698,7 +698,7 @@ qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T,
     if (st != QTIP_OK) return st;
     if (!viterbi_supported(p->code, p->k, p->V, p->L, p->Q, p->hyb_two_sign))
         return fail(QTIP_ERR_UNSUPPORTED,
-                    "GPU quantizer: L = 16; 3INST/1MAD V = 1, k in {2, 3}; HYB V = 2, k in {2, 3, 4}, Q = 9, one sign");
+                    "GPU quantizer: L = 16; 3INST/1MAD V = 1, k in {2, 3, 4}; HYB V = 2, k in {2, 3, 4}, Q = 9, one sign");
     if (nseq < 1 || T < 2 || T > 4096 || nseq > (1 << 30) || T % p->V) return fail(QTIP_ERR_SHAPE, "need nseq >= 1, 2 <= T <= 4096, V | T");
     if (!d_source || !d_states || !d_cost || !d_workspace || (p->code == QTIP_CODE_HYB && !d_lut))
         return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");

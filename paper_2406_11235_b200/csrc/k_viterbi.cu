@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi_kernel(const ViterbiArgs
 // (entries 512..1023 carry -c1), replicated 32-fold in shared memory (index bits 6..15 of h).
 // Group minima live in two swapped shared-memory arrays, base-major (position b 2^kV + c) so a
 // thread's c run is contiguous; backpointers are one byte per group per step.
-template <int KV>
+// V1 = true: the same de Bruijn ownership for V = 1 codes with kV = 4 (3INST / 1MAD at k = 4): one
+// source value per step, the computed code of the state (bit-exact with qtip_decode) instead of the
+// HYB pair, d = (C_y - s_t)^2 (reading R17's binary32 order), seam at group floor(T / 2) (R3).
+template <int KV, bool V1 = false>
 __global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArgs args) {
     constexpr int L = 16;
     constexpr int SH = L - KV;
@@ -251,16 +254,18 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArg
     __shared__ uint32_t red_i[32];
     __shared__ uint32_t s_state;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int T = args.T, nsteps = T / 2;
+    const int T = args.T, nsteps = V1 ? T : T / 2;
     uint8_t* bp = reinterpret_cast<uint8_t*>(args.bp) + (size_t)blockIdx.x * nsteps * NG;
     const int b = tid / TPB;
     const int jbase = TPB > NC ? (tid % TPB) / CSPLIT : (tid % TPB) * JT;
     const int cbase = TPB > NC ? (tid % CSPLIT) * CT : 0;
-    for (int i = tid; i < 1024 * 32; i += kVThreads) {
-        const int e = i >> 5;
-        uint32_t w = args.lut[e & 511];
-        if (e & 512) w ^= 0x80000000u;                                 // c1 negated (Alg. 3 bit 15)
-        lut[i] = w;
+    if constexpr (!V1) {
+        for (int i = tid; i < 1024 * 32; i += kVThreads) {
+            const int e = i >> 5;
+            uint32_t w = args.lut[e & 511];
+            if (e & 512) w ^= 0x80000000u;                             // c1 negated (Alg. 3 bit 15)
+            lut[i] = w;
+        }
     }
     const uint32_t lut_lane = (uint32_t)__cvta_generic_to_shared(lut) + 4u * lane;
     auto pos = [](int q) { return (q % NB) * NC + q / NB; };            // base-major group position
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArg
             // V_{t-1}(y) = m_{t-1}(q(y)) + d(y, t-1) folded into m_t((b << KV) | j)
             auto step = [&](int t, auto kFirst, auto kLast, float& fbest, uint32_t& fy) {
                 constexpr bool first = decltype(kFirst)::value, last = decltype(kLast)::value;
-                const float s0 = s_src[2 * (t - 1)], s1 = s_src[2 * (t - 1) + 1];
+                const float s0 = V1 ? s_src[t - 1] : s_src[2 * (t - 1)], s1 = V1 ? 0.0f : s_src[2 * (t - 1) + 1];
                 const float* M = Mbuf + cur * NG;
                 float* Mn = Mbuf + (cur ^ 1) * NG;
 #pragma unroll 1
@@ -288,12 +293,18 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArg
                     for (int cc = 0; cc < CT; ++cc) {
                         const int c = cbase + cc;
                         const uint32_t y = ((uint32_t)(c * NB + b) << KV) | (uint32_t)j;
-                        const uint32_t h2 = y * (y + y + 2u);            // 2 (y^2 + y) mod 2^32
-                        uint32_t v;
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut_lane + (h2 & 0x1FF80u)));
-                        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&v));
-                        const float e0 = __fsub_rn(f.x, s0), e1 = __fsub_rn(f.y, s1);
-                        const float d = __fadd_rn(__fmul_rn(e0, e0), __fmul_rn(e1, e1));
+                        float d;
+                        if constexpr (V1) {
+                            const float e0 = __fsub_rn(__half2float(code_half(y, args.ca, args.code)), s0);
+                            d = __fmul_rn(e0, e0);
+                        } else {
+                            const uint32_t h2 = y * (y + y + 2u);        // 2 (y^2 + y) mod 2^32
+                            uint32_t v;
+                            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(lut_lane + (h2 & 0x1FF80u)));
+                            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&v));
+                            const float e0 = __fsub_rn(f.x, s0), e1 = __fsub_rn(f.y, s1);
+                            d = __fadd_rn(__fmul_rn(e0, e0), __fmul_rn(e1, e1));
+                        }
                         float x;
                         if constexpr (first) x = (pass == 0 || (uint32_t)(c * NB + b) == O) ? d : INFINITY;
                         else x = __fadd_rn(M[b * NC + c], d);
@@ -359,7 +370,7 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArg
                     uint32_t y = by;
                     // Alg. 4 seam: 1-indexed group floor(T/(2V)) (R3); for T = 2 that is index -1, which the
                     // oracle (Python indexing) reads as the last state
-                    const int g = T / 4, gi = g >= 1 ? g - 1 : nsteps - 1;
+                    const int g = V1 ? T / 2 : T / 4, gi = g >= 1 ? g - 1 : nsteps - 1;
                     if (pass == 1) {
                         args.states[(size_t)seq * nsteps + nsteps - 1] = y;
                         args.cost[seq] = best;
@@ -390,7 +401,7 @@ size_t viterbi_workspace_bytes(int T) { return (size_t)num_sms() * T * kVThreads
 bool viterbi_supported(int code, int k, int V, int L, int Q, int two_sign) {
     if (L != 16) return false;
     if (code == QTIP_CODE_HYB) return V == 2 && Q == 9 && !two_sign && (k == 2 || k == 3 || k == 4);
-    return V == 1 && (k == 2 || k == 3) && (code == QTIP_CODE_3INST || code == QTIP_CODE_1MAD);
+    return V == 1 && (k == 2 || k == 3 || k == 4) && (code == QTIP_CODE_3INST || code == QTIP_CODE_1MAD);
 }
 
 cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, const uint16_t* lut, int nseq, int T,
@@ -425,6 +436,8 @@ cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* sr
         if (kv == 4) e = go2(viterbi2_kernel<4>, 12);
         else if (kv == 6) e = go2(viterbi2_kernel<6>, 10);
         else if (kv == 8) e = go2(viterbi2_kernel<8>, 8);
+    } else if (kv == 4) {
+        e = go2(viterbi2_kernel<4, true>, 12);
     } else if (kv == 2) e = go(viterbi_kernel<2>, 14);
     else if (kv == 3) e = go(viterbi_kernel<3>, 13);
     count_launch(1);

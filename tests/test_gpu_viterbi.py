@@ -19,7 +19,9 @@ def _src(code, nseq, T, seed):
 
 
 @pytest.mark.parametrize("code,k,nseq,T", [("3inst", 2, 64, 256), ("1mad", 2, 40, 256), ("3inst", 3, 24, 128),
-                                           ("1mad", 3, 9, 256), ("3inst", 2, 300, 64), ("3inst", 2, 3, 2)])
+                                           ("1mad", 3, 9, 256), ("3inst", 2, 300, 64), ("3inst", 2, 3, 2),
+                                           ("3inst", 4, 6, 256), ("1mad", 4, 4, 128), ("3inst", 4, 5, 2),
+                                           ("1mad", 4, 3, 16)])
 def test_viterbi_matches_oracle_bit_exact(cuda_lib, code, k, nseq, T):
     from paper_2406_11235_b200.quantize import QTIPQuantizer
     src, tab = _src(code, nseq, T, seed=5000 + T + k)
