@@ -142,8 +142,11 @@ def test_degenerate_arguments_are_refused(lib):
     assert vt(nseq=0) == -2 and vt(T=1) == -2 and vt(T=4097) == -2
     ph = qtip.params_default("hyb", 2)
     assert vt(T=255, pp=ph) == -2                                  # V = 2 must divide T
-    p4 = qtip.params_default("3inst", 4)
-    assert vt(pp=p4) == -5                                         # V = 1 Viterbi: k in {2, 3}
+    p1 = qtip.params_default("3inst", 1)
+    assert vt(pp=p1) == -5                                         # V = 1 Viterbi: k in {2, 3, 4}
+    pq = qtip.params_default("hyb", 2)
+    pq.Q = 6
+    assert vt(pp=pq) == -5                                         # HYB Viterbi: Q = 9
 
 
 
