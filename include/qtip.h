@@ -236,6 +236,18 @@ qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T,
                                   const uint16_t* d_lut, uint32_t* d_states, float* d_cost, void* d_workspace,
                                   size_t workspace_bytes, void* stream);
 
+/* Quantize a whole RHT-domain matrix (the step before qtip_pack_states): every T_x x T_y block of
+ * d_W is one sequence in row-major scan, multiplied by source_scale (reading R9:
+ * the code's state standard deviation, so the source is in code units), then Algorithm 4 as
+ * qtip_viterbi_tailbite (same support, same binary32 arithmetic).
+ *   d_W: DEVICE float32 [m][n]; d_states: DEVICE uint32 [m/T_x][n/T_y][T/V] (the layout
+ *   qtip_pack_states reads after a copy to the host); d_cost: DEVICE float32 [m/T_x][n/T_y];
+ *   d_workspace: qtip_quantize_workspace_bytes(p, m, n) bytes, caller-owned. */
+size_t qtip_quantize_workspace_bytes(const qtip_params* p, int64_t m, int64_t n);
+qtip_status qtip_quantize_matrix(const qtip_params* p, int64_t m, int64_t n, const float* d_W, float source_scale,
+                                 const uint16_t* d_lut, uint32_t* d_states, float* d_cost, void* d_workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* Selects the matvec kernel: 0 = auto (the measured-fastest supported kernel), 1 = CUDA-core
  * reference kernel, 2 = tcgen05 kernel (A in TMEM, per-cell split-K), 3 = register-fed mma.sync
  * kernel with split-K over 128-column cells, 4 = row-tile mma.sync kernel (one CTA per 16 rows,

@@ -284,7 +284,10 @@ static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
     // layers); short single launches keep the row-tile kernel (fixed start-up + stream-K fix-up cost).
     // For 3INST / 1MAD the decode (5 instructions per weight), not the MMA, bounds it: only the 70B
     // layers (>= 40 cells per SM) gain (C4 8192 x 28672: 69.6 -> 66.7 us)
+    // 3INST / 1MAD at batch >= 8: impl 7 beats the split-K / CUDA-core kernels on the 7B step at every
+    // measured batch (B = 8 / 16 / 32: 265 -> 300, 160 -> 193, 42 -> 70 GB/s, profiles/r2/batch_*)
     const int64_t cells = (int64_t)G * l.n_rb * l.n_kc;
+    if (p->code != QTIP_CODE_HYB && B >= 8) return true;
     const int64_t min_cells = (p->code == QTIP_CODE_HYB ? 10 : 40) * (int64_t)num_sms();
     return B <= 8 && cells >= min_cells;
 }
@@ -706,6 +709,35 @@ qtip_status qtip_viterbi_tailbite(const qtip_params* p, int64_t nseq, int64_t T,
     const cudaError_t e = launch_viterbi(p->code, p->k * p->V, code_args(p), d_source, d_lut, (int)nseq, (int)T, d_states,
                                          d_cost, d_workspace, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_viterbi_tailbite");
+    return QTIP_OK;
+}
+
+size_t qtip_quantize_workspace_bytes(const qtip_params* p, int64_t m, int64_t n) {
+    if (qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK) return 0;
+    return align256(viterbi_workspace_bytes(p->Tx * p->Ty)) + align256((size_t)m * n * 4);
+}
+
+qtip_status qtip_quantize_matrix(const qtip_params* p, int64_t m, int64_t n, const float* d_W, float source_scale,
+                                 const uint16_t* d_lut, uint32_t* d_states, float* d_cost, void* d_workspace,
+                                 size_t workspace_bytes, void* stream) {
+    qtip_status st = qtip_params_check(p);
+    if (st != QTIP_OK) return st;
+    if ((st = check_shape(m, n)) != QTIP_OK) return st;
+    if ((st = check_block(p, m, n)) != QTIP_OK) return st;
+    if (!viterbi_supported(p->code, p->k, p->V, p->L, p->Q, p->hyb_two_sign))
+        return fail(QTIP_ERR_UNSUPPORTED,
+                    "GPU quantizer: L = 16; 3INST/1MAD V = 1, k in {2, 3, 4}; HYB V = 2, k in {2, 3, 4}, Q = 9, one sign");
+    if (!d_W || !d_states || !d_cost || !d_workspace || (p->code == QTIP_CODE_HYB && !d_lut))
+        return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
+    if (workspace_bytes < qtip_quantize_workspace_bytes(p, m, n)) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
+    const int T = p->Tx * p->Ty;
+    const int64_t nseq = (m / p->Tx) * (n / p->Ty);
+    cudaStream_t s = (cudaStream_t)stream;
+    float* seqs = (float*)((char*)d_workspace + align256(viterbi_workspace_bytes(T)));
+    cudaError_t e = launch_gather_sequences(d_W, m, n, p->Tx, p->Ty, source_scale, seqs, s);
+    if (e == cudaSuccess)
+        e = launch_viterbi(p->code, p->k * p->V, code_args(p), seqs, d_lut, (int)nseq, T, d_states, d_cost, d_workspace, s);
+    if (e != cudaSuccess) return cuda_fail(e, "qtip_quantize_matrix");
     return QTIP_OK;
 }
 

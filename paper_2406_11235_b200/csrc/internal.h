@@ -193,6 +193,9 @@ size_t variant_gemv_smem(const qtip_params* p, int64_t B);
 // code units), binary32 DP.  ws: viterbi_workspace_bytes(T) bytes (backpointers, per CTA).
 bool viterbi_supported(int code, int k, int V, int L, int Q, int two_sign);
 size_t viterbi_workspace_bytes(int T);
+// The sequences of a matrix (T_x x T_y blocks in row-major scan, scaled): out[(I n/T_y + J) T + p].
+cudaError_t launch_gather_sequences(const float* W, int64_t m, int64_t n, int Tx, int Ty, float scale, float* out,
+                                    cudaStream_t s);
 cudaError_t launch_viterbi(int code, int kv, const CodeArgs& ca, const float* src, const uint16_t* lut, int nseq, int T,
                            uint32_t* states, float* cost, void* ws, cudaStream_t s);
 

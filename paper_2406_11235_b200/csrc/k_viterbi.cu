@@ -394,7 +394,25 @@ __global__ void __launch_bounds__(kVThreads, 1) viterbi2_kernel(const ViterbiArg
     }
 }
 
+// the T_x x T_y block (I, J) of W is one sequence, rows concatenated (row-major
+// scan); R9: the source enters in code units (multiplied by the code's state standard deviation).
+__global__ void gather_sequences_kernel(const float* __restrict__ W, int64_t m, int64_t n, int Tx, int Ty, float scale,
+                                        float* __restrict__ out) {
+    const int64_t seq = blockIdx.x;
+    const int64_t nb = n / Ty;
+    const int64_t I = seq / nb, J = seq % nb;
+    for (int p = threadIdx.x; p < Tx * Ty; p += blockDim.x)
+        out[seq * Tx * Ty + p] = W[(I * Tx + p / Ty) * n + J * Ty + p % Ty] * scale;
+}
+
 }  // namespace
+
+cudaError_t launch_gather_sequences(const float* W, int64_t m, int64_t n, int Tx, int Ty, float scale, float* out,
+                                    cudaStream_t s) {
+    gather_sequences_kernel<<<(unsigned)((m / Tx) * (n / Ty)), 256, 0, s>>>(W, m, n, Tx, Ty, scale, out);
+    count_launch(1);
+    return cudaGetLastError();
+}
 
 size_t viterbi_workspace_bytes(int T) { return (size_t)num_sms() * T * kVThreads * 4; }   // >= V = 2 needs
 

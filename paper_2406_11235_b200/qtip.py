@@ -31,7 +31,7 @@ EXPORTS = ["qtip_params_default", "qtip_params_check", "qtip_packed_bytes", "qti
            "qtip_set_matvec_impl", "qtip_get_matvec_impl", "qtip_status_string", "qtip_last_error",
            "qtip_launch_count", "qtip_profile_events", "qtip_set_pdl", "qtip_viterbi_workspace_bytes",
            "qtip_viterbi_tailbite", "qtip_chain_plan_create", "qtip_chain_run", "qtip_chain_plan_destroy",
-           "qtip_chain_plan_stages"]
+           "qtip_chain_plan_stages", "qtip_quantize_workspace_bytes", "qtip_quantize_matrix"]
 
 
 class QtipParams(ctypes.Structure):
@@ -112,6 +112,10 @@ def load(path=LIB_PATH):
     lib.qtip_profile_events.restype = None
     lib.qtip_set_pdl.argtypes = [ctypes.c_int]
     lib.qtip_set_pdl.restype = None
+    lib.qtip_quantize_workspace_bytes.argtypes = [P, i64, i64]
+    lib.qtip_quantize_workspace_bytes.restype = ctypes.c_size_t
+    lib.qtip_quantize_matrix.argtypes = [P, i64, i64, vp, ctypes.c_float, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.qtip_quantize_matrix.restype = ctypes.c_int
     lib.qtip_chain_plan_create.argtypes = [P, i32, ctypes.POINTER(ChainLayer), i64, vp, ctypes.POINTER(vp)]
     lib.qtip_chain_plan_create.restype = ctypes.c_int
     lib.qtip_chain_run.argtypes = [vp, vp, vp]
@@ -228,6 +232,16 @@ def qtip_viterbi_tailbite(p, nseq, T, d_source, d_states, d_cost, d_workspace, d
     _check("qtip_viterbi_tailbite", load().qtip_viterbi_tailbite(
         ctypes.byref(p), nseq, T, _ptr(d_source), _ptr(d_lut), _ptr(d_states), _ptr(d_cost), _ptr(d_workspace),
         d_workspace.numel() * d_workspace.element_size(), _stream(stream)))
+
+
+def quantize_workspace_bytes(p, m, n):
+    return int(load().qtip_quantize_workspace_bytes(ctypes.byref(p), m, n))
+
+
+def qtip_quantize_matrix(p, m, n, d_W, source_scale, d_states, d_cost, d_workspace, d_lut=None, stream=None):
+    _check("qtip_quantize_matrix", load().qtip_quantize_matrix(
+        ctypes.byref(p), m, n, _ptr(d_W), float(source_scale), _ptr(d_lut), _ptr(d_states), _ptr(d_cost),
+        _ptr(d_workspace), d_workspace.numel() * d_workspace.element_size(), _stream(stream)))
 
 
 def qtip_chain_plan_create(p, layers, B, d_lut=None):

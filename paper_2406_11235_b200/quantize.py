@@ -1,10 +1,9 @@
 """QTIPQuantizer: tail-biting trellis quantization of RHT-domain weight tiles on the GPU
 (Algorithm 4), producing the packed stream QTIPLinear decodes.
 
-All arithmetic runs in libqtip (qtip_viterbi_tailbite, k_viterbi.cu); this module only moves
-buffers: it scales the source into code units (reading R9: the code is normalised to unit
-state variance, i.e. the source is multiplied by the code's state standard deviation), calls the
-kernel, and hands the walks to qtip_pack_states.
+All arithmetic runs in libqtip (qtip_viterbi_tailbite / qtip_quantize_matrix, k_viterbi.cu): the
+block scan of P:833 and the scaling into code units (reading R9) happen in the library's gather
+kernel; this module only moves buffers and hands the walks to qtip_pack_states.
 """
 import numpy as np
 import torch
@@ -45,10 +44,13 @@ class QTIPQuantizer:
 
     def quantize_tiles(self, W_tilde, code_std):
         """W_tilde: float32 [m][n] RHT-domain weights (m, n multiples of 16), each 16 x 16 tile one
-        T = 256 sequence in row-major scan.  Returns the host walks
-        (uint32 [m/16][n/16][256]) for qtip_pack_states and the per-tile costs."""
+        T = 256 sequence in row-major scan, scaled by code_std into code units in
+        the library (qtip_quantize_matrix).  Returns the host walks (uint32 [m/16][n/16][256/V]) for
+        qtip_pack_states and the per-tile costs (CUDA)."""
         m, n = W_tilde.shape
-        tiles = (W_tilde.reshape(m // 16, 16, n // 16, 16).permute(0, 2, 1, 3).reshape(-1, 256)
-                 .to(torch.float32) * np.float32(code_std)).contiguous()
-        states, cost = self.encode(tiles.to(self.device))
-        return states.cpu().numpy().astype(np.uint32).reshape(m // 16, n // 16, 256 // self.V), cost
+        W = W_tilde.to(device=self.device, dtype=torch.float32).contiguous()
+        states = torch.empty((m // 16, n // 16, 256 // self.V), dtype=torch.int32, device=self.device)
+        cost = torch.empty((m // 16, n // 16), dtype=torch.float32, device=self.device)
+        ws = torch.empty(qtip.quantize_workspace_bytes(self.p, m, n), dtype=torch.uint8, device=self.device)
+        qtip.qtip_quantize_matrix(self.p, m, n, W, code_std, states, cost, ws, d_lut=self.lut)
+        return states.cpu().numpy().astype(np.uint32), cost.reshape(-1)

@@ -97,3 +97,20 @@ def test_no_sequences_is_a_no_op(cuda_lib):
     c0 = cuda_lib.launch_count()
     w, c = q.encode(torch.empty((0, 256), dtype=torch.float32, device="cuda"))
     assert tuple(w.shape) == (0, 256) and tuple(c.shape) == (0,) and cuda_lib.launch_count() == c0
+
+
+@pytest.mark.parametrize("code,k", [("3inst", 2), ("1mad", 4)])
+def test_quantize_matrix_scan_and_scale_bit_exact(cuda_lib, code, k):
+    """qtip_quantize_matrix does the block scan (16 x 16 tiles, row-major) and the scaling into
+    code units (R9) in the library: its walks and costs equal the oracle's binary32 Algorithm 4 on the
+    sequences cut and scaled on the host."""
+    from paper_2406_11235_b200.quantize import QTIPQuantizer
+    m, n = 64, 48
+    tab = codes.code_table(code, 16)
+    sd = np.float32(tab.std())
+    W = synth.gaussian_source(m, n, seed=5100 + k).astype(np.float32)
+    walks, cost = QTIPQuantizer(code, k).quantize_tiles(torch.from_numpy(W), sd)
+    seqs = (W.reshape(m // 16, 16, n // 16, 16).transpose(0, 2, 1, 3).reshape(-1, 256) * sd).astype(np.float32)
+    ref_st, ref_cost = viterbi.tailbite_encode_f32_batch(seqs, 16, k, 1, tab.astype(np.float32))
+    assert np.array_equal(walks.reshape(-1, 256), ref_st)
+    assert np.array_equal(cost.cpu().numpy(), ref_cost)
