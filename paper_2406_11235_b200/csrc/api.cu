@@ -345,8 +345,8 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
         return QTIP_OK;
     }
     RhtPlan pn{}, pm{};
-    if (rin && !xready && make_rht_plan(n, &pn, 128 / G) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
-    if (rout && make_rht_plan(m, &pm, 128 / G) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
+    if (rin && !xready && make_rht_plan(n, &pn, 128 / G, B) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
+    if (rout && make_rht_plan(m, &pm, 128 / G, B) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
     cudaStream_t s = (cudaStream_t)stream;
     const WsLayout o = ws_layout(p, l, B);
     const float* xin[kMaxGroup];
@@ -477,9 +477,9 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     const size_t need = qtip_matvec_workspace_bytes(p, m, n, B);
     if (workspace_bytes < need) return fail(QTIP_ERR_WORKSPACE, "workspace too small");
     RhtPlan pn{}, pm{};
-    if ((flags & QTIP_RHT_IN) && !(flags & QTIP_XT_READY) && make_rht_plan(n, &pn) != cudaSuccess)
+    if ((flags & QTIP_RHT_IN) && !(flags & QTIP_XT_READY) && make_rht_plan(n, &pn, 128, B) != cudaSuccess)
         return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
-    if ((flags & QTIP_RHT_OUT) && make_rht_plan(m, &pm) != cudaSuccess)
+    if ((flags & QTIP_RHT_OUT) && make_rht_plan(m, &pm, 128, B) != cudaSuccess)
         return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for m");
 
     const Layout l = make_layout(m, n, p->k);
@@ -683,7 +683,7 @@ qtip_status qtip_rht(int64_t n, int64_t B, const uint8_t* d_sign, const float* d
     if (!d_sign || !d_in || !d_out) return fail(QTIP_ERR_INVALID_PARAMS, "NULL buffer");
     if (d_in == d_out) return fail(QTIP_ERR_INVALID_PARAMS, "qtip_rht is out-of-place (d_in != d_out)");
     RhtPlan plan{};
-    if (make_rht_plan(n, &plan) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
+    if (make_rht_plan(n, &plan, 128, B) != cudaSuccess) return fail(QTIP_ERR_SHAPE, "no supported Hadamard order for n");
     cudaError_t e = launch_rht(plan, B, d_sign, d_in, n, d_out, n, inverse ? 1 : 0, 1.0f, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_rht");
     return QTIP_OK;

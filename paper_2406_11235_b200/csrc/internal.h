@@ -85,7 +85,7 @@ struct RhtPlan {
 };
 // min_ctas: rows of D per CTA are chosen so that one transform still has >= min_ctas CTAs (a grouped
 // launch of G transforms passes 128 / G to stay within one wave).
-cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas = 128);
+cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas = 128, int64_t B = 1);
 // out[bt][i] = scale * (M v)[i] / sqrt(n) with v = in * s (forward) or in (inverse, then * s).
 // in/out batch strides in elements.  out_mode 0 float32, 1 binary16 duplicated per 32-bit word,
 // 2 binary16; elements [n, pad_to) of every output row are written as zero.

@@ -155,11 +155,25 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
         int j = j_lo;
         auto step = [&](const float (&v)[E], int jj) {
             const float* d = Dsm + jj * R + ro * RA;
+            if constexpr (RA % 4 == 0) {
+                // four rows of D per (broadcast) LDS.128: with one LDS per FFMA the shared-memory pipe,
+                // not the FMAs, bound the batched transforms (n = 11008, B = 16: RA = 16)
 #pragma unroll
-            for (int q = 0; q < RA; ++q) {
-                const float dq = d[q];
+                for (int q4 = 0; q4 < RA; q4 += 4) {
+                    const float4 d4 = *reinterpret_cast<const float4*>(d + q4);
+                    const float dq[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-                for (int e = 0; e < E; ++e) acc[q][e] = fmaf(dq, v[e], acc[q][e]);
+                    for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc[q4 + qq][e] = fmaf(dq[qq], v[e], acc[q4 + qq][e]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < RA; ++q) {
+                    const float dq = d[q];
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[q][e] = fmaf(dq, v[e], acc[q][e]);
+                }
             }
         };
         auto load = [&](float (&v)[E], int jj) {
@@ -182,10 +196,15 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
 #pragma unroll
             for (int u = 0; u < U; ++u) step(v[u], j + u);
         }
-        for (; j < j_hi; ++j) {
-            float v[E];
-            load(v, j);
-            step(v, j);
+        if (j < j_hi) {                                      // the tail: one predicated round, not one
+            const int rem = j_hi - j;                        // L2 round trip per row (n = 11008: 43 rows
+            float v[U][E];                                   // per warp = 2 rounds + 11 singles before)
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < rem) load(v[u], j + u);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < rem) step(v[u], j + u);
         }
     };
     if (inverse) slice(std::integral_constant<int, 0>{});
@@ -197,9 +216,8 @@ __global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __
         for (int e = 0; e < E; ++e) red[(warp * R + ro * RA + q) * L2 + c + 32 * e] = acc[q][e];
     __syncthreads();
 
-    // rows ro RA + q of pass `warp` (RA passes): sum the 8 slices in order, FWHT, store
-    if (warp < RA) {
-        const int q = warp;
+    // rows ro RA + q, q = warp, warp + 8, ...: sum the 8 slices in order, FWHT, store
+    for (int q = warp; q < RA; q += kRhtWarps) {
         const int rl = ro * RA + q, r = r0 + rl;
         float u[E];
 #pragma unroll
@@ -256,7 +274,7 @@ __global__ void convert_kernel(const float* __restrict__ in, int64_t n, int64_t 
 
 constexpr int64_t kRhtMaxN = 48 * 1024;
 
-cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas) {
+cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas, int64_t B) {
     int b, a;
     if (!hadamard_factor(n, &b, &a)) return cudaErrorInvalidValue;
     if (n > kRhtMaxN) return cudaErrorInvalidValue;
@@ -271,11 +289,14 @@ cudaError_t make_rht_plan(int64_t n, RhtPlan* plan, int min_ctas) {
     plan->f = (int)(n >> plan->a2);
     plan->E = L2 >= 32 ? L2 / 32 : 1;
     const int rpw = L2 >= 32 ? 1 : 32 / L2;
-    // rows per lane: amortise the D loads, but keep at least ~one CTA per SM when f allows
+    // rows per lane: amortise the D loads, but keep at least ~one CTA per SM when f allows.  Every
+    // CTA reads its whole input vector from L2, so the L2 traffic is (CTAs per vector) x B x 4n:
+    // with a batch the CTAs take more rows of D (up to 16) while B x (CTAs per vector) >= min_ctas
+    // (n = 11008, B = 16: 172 -> 22 CTAs per vector, 121 -> 15 MB of L2 reads)
     int RA = 1;
-    if (plan->E <= 2) {
-        RA = 4;
-        while (RA > 1 && (plan->f + RA * rpw - 1) / (RA * rpw) < min_ctas) RA /= 2;
+    if (plan->E <= 2 || B > 1) {
+        RA = B <= 1 ? 4 : (plan->E == 1 ? 16 : plan->E == 2 ? 8 : 4);
+        while (RA > 1 && B * ((plan->f + RA * rpw - 1) / (RA * rpw)) < min_ctas) RA /= 2;
     }
     plan->RA = RA;
     plan->rows_per_cta = RA * rpw;
@@ -313,8 +334,9 @@ static cudaError_t launch_rht_io(const RhtPlan& plan, int G, int64_t B, const Rh
     cudaError_t e = cudaErrorInvalidValue;
 #define QTIP_RHT_CASE(EE, RR) \
     if (plan.E == EE && plan.RA == RR) e = launch_rht_t<EE, RR>(plan, G, B, io, in_stride, out_stride, inverse, s, out_mode, pad, zero_ptr, zero_n);
-    QTIP_RHT_CASE(1, 1) QTIP_RHT_CASE(1, 2) QTIP_RHT_CASE(1, 4) QTIP_RHT_CASE(2, 1) QTIP_RHT_CASE(2, 2)
-    QTIP_RHT_CASE(2, 4) QTIP_RHT_CASE(4, 1) QTIP_RHT_CASE(8, 1)
+    QTIP_RHT_CASE(1, 1) QTIP_RHT_CASE(1, 2) QTIP_RHT_CASE(1, 4) QTIP_RHT_CASE(1, 8) QTIP_RHT_CASE(1, 16)
+    QTIP_RHT_CASE(2, 1) QTIP_RHT_CASE(2, 2) QTIP_RHT_CASE(2, 4) QTIP_RHT_CASE(2, 8) QTIP_RHT_CASE(4, 1)
+    QTIP_RHT_CASE(4, 2) QTIP_RHT_CASE(4, 4) QTIP_RHT_CASE(8, 1) QTIP_RHT_CASE(8, 2) QTIP_RHT_CASE(8, 4)
 #undef QTIP_RHT_CASE
     count_launch(1);
     return e;

@@ -4,15 +4,19 @@
 //
 // Work = the launch's 128 x 128 cells (8 x 8 tiles of T = 256), of G same-shape
 // layers stacked into one "virtual" matrix (grouped q,k,v / gate,up launches).  The U cells are cut
-// into W = P * npass equal contiguous ranges in row-major order (stream-K): range w is
-// [U w / W, U (w+1) / W), CTA i runs ranges i, i + P, ...  Every CTA gets the same number of cells
+// into W = P equal contiguous ranges in row-major order (stream-K): range w is
+// [U w / W, U (w+1) / W), CTA i runs range i.  Every CTA gets the same number of cells
 // (+-1), whatever the shape: no tile-row imbalance and no one-wave rule.
 //
 // One CTA per SM, 18 warps:
-//   warp 0      producer: cp.async.bulk of each cell (2048k bytes, L2 evict-first) into an S-stage
-//               ring.  The weights do not depend on the previous kernel, so the ring fills before
-//               (and while) the previous kernel finishes (PDL).
-//               It also loads each range's x~ window into shared memory, after the PDL wait.
+//   warp 0      producer: one TMA stream of (x~ slab, weight cell) pairs.  Weight cells (2048k bytes,
+//               L2 evict-first) go into an S-stage ring; the first S are requested before the PDL
+//               wait (the weights do not depend on the previous kernel), so the ring fills while it
+//               finishes.  After the wait, the x~ slab of each cell's column (128 columns x BP batch
+//               rows, binary16) goes into an XS-slot ring just ahead of the cell's weights; a slot is
+//               refilled once the MMAs that read it completed.  The slab ring replaces a whole-range
+//               x~ window: any batch width fits shared memory in one pass, so no pass boundary drains
+//               the pipeline (HYB B = 16: 3 passes before).
 //   warp 1      MMA issuer (one elected thread): for every cell, waits for its decoded A operand in
 //               TMEM and issues 8 tcgen05.mma (kind::f16, M = 128, N = 16/64, K = 16, A from TMEM,
 //               B = x~ from shared memory, D in TMEM) -- asynchronous, so the tensor core never
@@ -40,10 +44,11 @@
 // SM count).  Segment ids are w - w_first(layer) + row block (injective because ranges are ordered).
 //
 // x~ in shared memory, the UMMA B operand (K-major, SWIZZLE_NONE): element k of batch row r at byte
-// (k / 8) * 16 BP + 16 r + 2 (k % 8), BP = batch padded to a power of two.  The descriptor's leading
-// byte offset (K direction) is 16 BP: for BP < 8 the core matrices' rows >= BP overlap the next K
-// chunks -- they only feed accumulator columns >= B, which are never read -- so x~ costs exactly
-// 2 BP bytes per column and a whole 28672-long x~ fits.
+// (k / 8) * 16 BP + 16 r + 2 (k % 8) of its cell column's slab, BP = batch padded to a power of two.
+// The descriptor's leading byte offset (K direction) is 16 BP: for BP < 8 the core matrices' rows
+// >= BP overlap the next K chunks (or, for the last chunk of a slab, the next slot / the ring's
+// padding) -- they only feed accumulator columns >= B, which are never read -- so a slab costs
+// exactly 256 BP bytes.
 #include <algorithm>
 
 #include "internal.h"
@@ -55,6 +60,7 @@ namespace {
 constexpr int kUG = 3;                       // decoder groups
 constexpr int kUWarps = 6 + 4 * kUG;
 constexpr int kUThreads = 32 * kUWarps;      // 576
+constexpr int kMaxXS = 32;                   // x~ slab slots (at most)
 constexpr uint32_t kLutQ = 9;
 constexpr uint32_t kLutBytes = (1u << (kLutQ + 1)) * 128u;   // 1024 sign-folded entries x 32 replicas x 4 B
 constexpr uint32_t kHdr = 1024;              // barriers, TMEM base
@@ -82,7 +88,8 @@ struct UmmaArgs {
     int B, BP;
     float code_factor;
     uint32_t off_ring, off_x;                // shared-memory offsets (LUT at kHdr)
-    uint32_t xcol_bytes;                     // x~ bytes per cell column
+    uint32_t xcol_bytes;                     // x~ bytes per cell column (one slab)
+    int XS;                                  // x~ slab slots
     uint32_t lbo, sbo;
 };
 
@@ -130,13 +137,14 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
     const uint32_t barD = bar0 + 8u * (2 * S + 2 * kUG * kNBuf);
     auto dfull = [&](int d) { return barD + 8u * d; };
     auto dempty = [&](int d) { return barD + 16u + 8u * d; };
-    const uint32_t xfull = barD + 32u, xempty = barD + 40u;
+    auto xfull = [&](int x) { return barD + 32u + 8u * x; };
+    auto xempty = [&](int x) { return barD + 32u + 8u * (kMaxXS + x); };
+    const int XS = a.XS;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + 1016);
     uint8_t* ring = smem + a.off_ring;
     const uint32_t xwin = ptx::smem_u32(smem + a.off_x);
     const int n_kc = (int)a.lay.n_kc;
     const int Ul = a.nrb * n_kc;                              // cells per layer
-    const int nrb = (int)a.nrb;
     const int P = (int)gridDim.x;
 
     // ---------------- setup (static data only: overlaps the previous kernel under PDL)
@@ -166,8 +174,10 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
                 ptx::mbar_init(dfull(d), 1);
                 ptx::mbar_init(dempty(d), 4);
             }
-            ptx::mbar_init(xfull, 1);
-            ptx::mbar_init(xempty, 1);
+            for (int x = 0; x < XS; ++x) {
+                ptx::mbar_init(xfull(x), 1);
+                ptx::mbar_init(xempty(x), 1);
+            }
             ptx::fence_mbar_init();
         }
         __syncwarp();
@@ -184,158 +194,115 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
     // MMAs) and advances its counters incrementally: a 64-bit division or lane-0-only code per cell
     // costs hundreds of cycles.
     if (warp == 0) {
-        // ================= producer: every cell of every pass, in order (the cells of a range are
-        // contiguous in memory within a layer: row-block-major cells), and each pass's x~ window.
-        // Pass 0: the first S cells are requested before the PDL wait (the weights do not depend on
-        // the previous kernel), then x~ (its output).  Later passes reload the window once the
-        // previous pass's MMAs completed.
+        // ================= producer: one TMA stream of (x~ slab, weight cell) pairs in the CTA's cell
+        // order.  The weights do not depend on the previous kernel: the first S cells are requested
+        // before the PDL wait; the x~ slabs (the previous kernel's output) after it, each one ahead of
+        // its cell's weights, so a slab never waits behind later weight cells in the SM's TMA queue
+        // (a separate x~ warp's copies did: traced MMA cadence 700 -> 1000 cycles per cell).
         const uint64_t pol = ptx::l2_evict_first_policy();
-        int s = 0, p = 0;
+        const int ua = range_lo(a.U, a.W, blockIdx.x), ub = range_lo(a.U, a.W, blockIdx.x + 1);
+        const int nc = ub - ua, pre = nc < S ? nc : S;
+        int gw = (int)(ua / Ul), ulw = ua - gw * Ul;          // weight cursor (layer, cell in layer)
+        const uint32_t* src = a.packed[gw] + (a.rb0 * n_kc + ulw) * a.lay.cell_words;
+        int s = 0;
         uint32_t r = 0;                                       // fills of stage s so far, mod 2
-        bool wrapped = false;
-        auto load_x = [&](int ua, int ub) {
-            const int g0 = (int)(ua / Ul), g1 = (int)((ub - 1) / Ul);
-            uint32_t bytes = 0;
-            for (int g = g0; g <= g1; ++g) {
-                const int lo = ua > g * Ul ? ua : g * Ul, hi = ub < (g + 1) * Ul ? ub : (g + 1) * Ul;
-                bytes += (uint32_t)(hi - lo < n_kc ? hi - lo : n_kc) * a.xcol_bytes;
-            }
+        auto issue_w = [&](int j) {
+            if (j >= S) ptx::mbar_wait(empty(s), r ^ 1u);
             if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(xfull, bytes);
-                int cum = 0;
-                for (int g = g0; g <= g1; ++g) {
-                    const int lo = ua > g * Ul ? ua : g * Ul, hi = ub < (g + 1) * Ul ? ub : (g + 1) * Ul;
-                    const int cnt = (int)(hi - lo < n_kc ? hi - lo : n_kc);
-                    const int kcs = (int)((lo - g * Ul) % n_kc);
-                    const int run1 = cnt < n_kc - kcs ? cnt : n_kc - kcs;
-                    const uint8_t* src = a.xt[g];
-                    ptx::bulk_g2s(xwin + (uint32_t)cum * a.xcol_bytes, src + (size_t)kcs * a.xcol_bytes,
-                                  (uint32_t)run1 * a.xcol_bytes, xfull);
-                    if (cnt > run1)
-                        ptx::bulk_g2s(xwin + (uint32_t)(cum + run1) * a.xcol_bytes, src,
-                                      (uint32_t)(cnt - run1) * a.xcol_bytes, xfull);
-                    cum += cnt;
-                }
+                ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
+                ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
             }
             __syncwarp();
+            if (++s == S) { s = 0; r ^= 1u; }
+            src += a.lay.cell_words;
+            if (++ulw == Ul && gw + 1 < a.G) {
+                ulw = 0;
+                ++gw;
+                src = a.packed[gw] + a.rb0 * n_kc * a.lay.cell_words;
+            }
         };
-        for (int w = blockIdx.x; w < a.W; w += P, ++p) {
-            const int ua = range_lo(a.U, a.W, w), ub = range_lo(a.U, a.W, w + 1);
-            if (p > 0) {
-                ptx::mbar_wait(xempty, (uint32_t)((p - 1) & 1));
-                load_x(ua, ub);
+        for (int j = 0; j < pre; ++j) issue_w(j);
+        ptx::pdl_wait();                                      // x~ is the previous kernel's output
+        int gx = (int)(ua / Ul), ulx = ua - gx * Ul, KC = ulx % n_kc;   // x~ cursor
+        for (int j = 0; j < nc; ++j) {
+            const int x = j % XS;
+            if (j >= XS) ptx::mbar_wait(xempty(x), (uint32_t)(((j / XS) - 1) & 1));
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(xfull(x), a.xcol_bytes);
+                ptx::bulk_g2s(xwin + (uint32_t)x * a.xcol_bytes, a.xt[gx] + (size_t)KC * a.xcol_bytes, a.xcol_bytes, xfull(x));
             }
-            int g = (int)(ua / Ul);
-            int ul = ua - g * Ul;                             // cell index within layer g
-            const uint32_t* src = a.packed[g] + (a.rb0 * n_kc + ul) * a.lay.cell_words;
-            const int pre = p == 0 ? (ub - ua < S ? ub - ua : S) : 0;
-            for (int u = ua; u < ub; ++u) {
-                if (p == 0 && u - ua == pre) {
-                    ptx::pdl_wait();
-                    load_x(ua, ub);
-                }
-                if (wrapped) ptx::mbar_wait(empty(s), r ^ 1u);
-                if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
-                    ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
-                }
-                __syncwarp();
-                if (++s == S) { s = 0; r ^= 1u; wrapped = true; }
-                src += a.lay.cell_words;
-                if (++ul == Ul && g + 1 < a.G) {
-                    ul = 0;
-                    ++g;
-                    src = a.packed[g] + a.rb0 * n_kc * a.lay.cell_words;
-                }
+            __syncwarp();
+            if (lane == 0) utrace(9, j);
+            if (++KC == n_kc) KC = 0;
+            if (++ulx == Ul && gx + 1 < a.G) {
+                ulx = 0;
+                ++gx;
+                KC = 0;
             }
-            if (p == 0 && pre == ub - ua) {                   // the whole pass fit the ring
-                ptx::pdl_wait();
-                load_x(ua, ub);
-            }
+            if (j >= pre) issue_w(j);
         }
     } else if (warp == 1) {
-        // ================= MMA issuer
-        int seg = 0, p = 0;
-        int jj = 0;                                           // CTA-local cell counter
-        for (int w = blockIdx.x; w < a.W; w += P, ++p) {
-            const int ua = range_lo(a.U, a.W, w), ub = range_lo(a.U, a.W, w + 1);
-            const int g0 = (int)(ua / Ul), g1 = (int)((ub - 1) / Ul);
-            int kcs[kMaxGroup], base[kMaxGroup];
-            {
-                int cum = 0;
-#pragma unroll
-                for (int gl = 0; gl < kMaxGroup; ++gl) {
-                    kcs[gl] = base[gl] = 0;
-                    if (gl < g0 || gl > g1) continue;
-                    const int lo = ua > gl * Ul ? ua : gl * Ul, hi = ub < (gl + 1) * Ul ? ub : (gl + 1) * Ul;
-                    kcs[gl] = (int)((lo - gl * Ul) % n_kc);
-                    base[gl] = cum;
-                    cum += (int)(hi - lo < n_kc ? hi - lo : n_kc);
-                }
-            }
-            int gl = g0;
-            int RB = (ua - gl * Ul) / n_kc;
-            int KC = ua - gl * Ul - RB * n_kc;
-            int off = (KC - kcs[0] + n_kc) % n_kc;
-#pragma unroll
-            for (int q = 1; q < kMaxGroup; ++q)
-                if (gl == q) off = (KC - kcs[q] + n_kc) % n_kc;
-            int wbase = base[0];
-#pragma unroll
-            for (int q = 1; q < kMaxGroup; ++q)
-                if (gl == q) wbase = base[q];
-            uint32_t dcol = tmem;
-            bool first = true;
-            const uint32_t dstep = 2u * (uint32_t)a.BP;       // B descriptor step per MMA (16 K)
-            // (all index math above before the wait: x~ is usually the last input to arrive)
-            ptx::mbar_wait(xfull, (uint32_t)(p & 1));
-            if (lane == 0) utrace(7, 1);
-            ptx::tc_fence_after();
-            for (int u = ua; u < ub; ++u, ++jj) {
-                if (u == ua || KC == 0) {                      // a new segment (row block) starts
-                    const int d = seg & 1;
-                    if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
-                    ptx::tc_fence_after();
-                    dcol = tmem + (uint32_t)d * kD1;
-                    first = true;
-                }
-                const int g = jj % kUG, lc = jj / kUG, b = lc & (kNBuf - 1);
-                ptx::mbar_wait(afull(g, b), (uint32_t)((lc / kNBuf) & 1));
-                if (lane == 0) utrace(4, jj);
+        // ================= MMA issuer.  This warp shares its SM sub-partition with three decoder warps
+        // and gets ~1/4 of its issue slots, so its per-cell path is kept short: incremental counters
+        // (no runtime divisions), descriptors advanced by constants, tracing behind one uniform test
+        // (traced before: ~180 instructions and ~650 cycles per cell, the kernel's bottleneck).
+        const int ua = range_lo(a.U, a.W, blockIdx.x), ub = range_lo(a.U, a.W, blockIdx.x + 1);
+        const int ncell = ub - ua;
+        const uint32_t dstep = 2u * (uint32_t)a.BP;           // B descriptor step per MMA (16 K)
+        const uint64_t cdesc0 = ptx::smem_desc_kmajor_noswizzle(xwin, a.lbo, a.sbo);
+        const uint64_t cslot = (uint64_t)(a.xcol_bytes >> 4);  // descriptor start-address step per slot
+        const bool tr = trc != nullptr;
+        int KC = (ua - (ua / Ul) * Ul) % n_kc;
+        int ul = ua - (ua / Ul) * Ul, gl = ua / Ul;
+        int seg = 0;
+        uint32_t dcol = tmem;
+        bool first = true;
+        int xs = 0;                                           // x~ slot of cell jj, its fill parity
+        uint32_t xph = 0;
+        int g = 0, b = 0;                                     // decoder group / A buffer of cell jj, buffer parity
+        uint32_t aph = 0;
+        for (int jj = 0; jj < ncell; ++jj) {
+            if (jj == 0 || KC == 0) {                          // a new segment (row block) starts
+                const int d = seg & 1;
+                if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
                 ptx::tc_fence_after();
-                const uint64_t cdesc =
-                    ptx::smem_desc_kmajor_noswizzle(xwin + (uint32_t)(wbase + off) * a.xcol_bytes, a.lbo, a.sbo);
-                const uint32_t acol = tmem + kA0 + (uint32_t)(g * kNBuf + b) * kACols;
-                if (ptx::elect_one()) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        ptx::umma_f16_ts(dcol, acol + 8u * (uint32_t)i, cdesc + (uint64_t)(dstep * (uint32_t)i), idesc,
-                                         (first && i == 0) ? 0u : 1u);
-                    ptx::umma_commit(aempty(g, b));
-                    if (u + 1 == ub || KC == n_kc - 1) ptx::umma_commit(dfull(seg & 1));
-                }
-                __syncwarp();
-                if (lane == 0) utrace(5, jj);
-                first = false;
-                if (u + 1 == ub || KC == n_kc - 1) ++seg;
-                // advance (layer, row block, cell column) and the window column
-                if (++off == n_kc) off = 0;
-                if (++KC == n_kc) {
-                    KC = 0;
-                    if (++RB == nrb) {
-                        RB = 0;
-                        ++gl;
-#pragma unroll
-                        for (int q = 1; q < kMaxGroup; ++q)
-                            if (gl == q) {
-                                off = (n_kc - kcs[q]) % n_kc;
-                                wbase = base[q];
-                            }
-                    }
-                }
+                dcol = tmem + (uint32_t)d * kD1;
+                first = true;
             }
-            if (ptx::elect_one()) ptx::umma_commit(xempty);   // this pass's MMAs read the window
+            ptx::mbar_wait(xfull(xs), xph);
+            ptx::mbar_wait(afull(g, b), aph);
+            if (tr && lane == 0) {
+                if (jj == 0) utrace(7, 1);
+                utrace(4, jj);
+            }
+            ptx::tc_fence_after();
+            const uint64_t cdesc = cdesc0 + cslot * (uint64_t)xs;
+            const uint32_t acol = tmem + kA0 + (uint32_t)(g * kNBuf + b) * kACols;
+            const bool seg_end = jj + 1 == ncell || KC == n_kc - 1;
+            if (ptx::elect_one()) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    ptx::umma_f16_ts(dcol, acol + 8u * (uint32_t)i, cdesc + (uint64_t)(dstep * (uint32_t)i), idesc,
+                                     (first && i == 0) ? 0u : 1u);
+                ptx::umma_commit(aempty(g, b));
+                if (jj + XS < ncell) ptx::umma_commit(xempty(xs));
+                if (seg_end) ptx::umma_commit(dfull(seg & 1));
+            }
             __syncwarp();
+            if (tr && lane == 0) utrace(5, jj);
+            first = false;
+            if (seg_end) ++seg;
+            if (++KC == n_kc) KC = 0;
+            if (++ul == Ul && gl + 1 < a.G) {
+                ul = 0;
+                ++gl;
+                KC = 0;
+            }
+            if (++xs == XS) { xs = 0; xph ^= 1u; }
+            if (++g == kUG) {
+                g = 0;
+                if (++b == kNBuf) { b = 0; aph ^= 1u; }
+            }
         }
     } else if (warp < 6) {
         // ================= epilogue warpgroup (warps 2-5: the four TMEM lane quadrants): D (thread =
@@ -455,7 +422,7 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
 }
 
 struct UmmaPlan {
-    int S, BP, N;
+    int S, BP, N, XS;
     int64_t P, W, U;
     uint32_t xcol, off_ring, off_x;
     size_t smem;
@@ -471,21 +438,18 @@ bool umma_plan(const Layout& lay, int code, int64_t B, int G, int64_t nrb, UmmaP
     const size_t max_smem = 225 * 1024;                               // + the kernel's static shared memory
     pl->U = (int64_t)G * nrb * lay.n_kc;
     pl->P = std::min<int64_t>(num_sms(), pl->U);
+    pl->W = pl->P;                                                    // one range per CTA, every range >= 1 cell
     const int S = umma_stages(lay.k, code);
     pl->S = S;
-    const size_t fixed = kHdr + lutb + (size_t)S * cell + 512;
+    const size_t pad = 512;                                           // the last slab's overlapping core-matrix rows
+    const size_t fixed = kHdr + lutb + (size_t)S * cell + pad;
     if (fixed >= max_smem) return false;
-    const int64_t fit = (int64_t)((max_smem - fixed) / pl->xcol) - G;   // x~ window columns per range
-    if (fit < 1) return false;
-    const int64_t c = (pl->U + pl->P - 1) / pl->P;
-    const int64_t need = std::min<int64_t>(c, (int64_t)G * lay.n_kc);
-    const int64_t npass = need <= fit ? 1 : (pl->U + pl->P * fit - 1) / (pl->P * fit);
-    pl->W = std::min<int64_t>(pl->P * npass, pl->U);                  // every range holds >= 1 cell
+    const int64_t fit = (int64_t)((max_smem - fixed) / pl->xcol);
+    pl->XS = (int)std::min<int64_t>(fit, kMaxXS);
+    if (pl->XS < 2) return false;
     pl->off_ring = (uint32_t)(kHdr + lutb);
     pl->off_x = (uint32_t)(kHdr + lutb + (size_t)S * cell);
-    const int64_t cw = (pl->U + pl->W - 1) / pl->W;
-    const int64_t win = std::min<int64_t>(cw, (int64_t)G * lay.n_kc) + G;
-    pl->smem = pl->off_x + (size_t)win * pl->xcol + 512;
+    pl->smem = pl->off_x + (size_t)pl->XS * pl->xcol + pad;
     if ((uint64_t)pl->U * (uint64_t)(pl->W + 1) >= (1ull << 31)) return false;   // 32-bit index math in the kernel
     return pl->smem <= max_smem;
 }
@@ -554,6 +518,7 @@ cudaError_t launch_umma(const Layout& lay, int code, const CodeArgs& ca, int G, 
     a.off_ring = pl.off_ring;
     a.off_x = pl.off_x;
     a.xcol_bytes = pl.xcol;
+    a.XS = pl.XS;
     a.lbo = 16u * (uint32_t)pl.BP;
     a.sbo = 128u;
     const bool imm = code != QTIP_CODE_HYB && lay.k == 2 &&

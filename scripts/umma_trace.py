@@ -36,10 +36,11 @@ t = buf.cpu().numpy().reshape(16, 64).astype(np.int64)
 t0 = t[7, 0]
 names = ["prod issue", "dec full", "dec aempty", "dec handoff", "mma afull", "mma issued", "epi dfull"]
 print(f"misc: start 0, x~ ready {t[7,1]-t0}, end {t[7,2]-t0}")
-print("cell grp  full-seen  aempty-ok  handoff | mma-seen  mma-issued | decode  mma-issue")
+print("cell grp  full-seen  aempty-ok  handoff | x-issued  x-seen  mma-seen  mma-issued | decode  mma-issue")
 for c in range(64):
     if not t[3, c]:
         continue
-    r = [int(t[kk, c] - t0) if t[kk, c] else -1 for kk in (1, 2, 3, 4, 5)]
-    print(f"{c:4d} {c % 3:3d} {r[0]:10d} {r[1]:10d} {r[2]:8d} | {r[3]:8d} {r[4]:11d} | {r[2]-r[1]:6d} {r[4]-r[3]:6d}")
+    r = [int(t[kk, c] - t0) if t[kk, c] else -1 for kk in (1, 2, 3, 9, 8, 4, 5)]
+    print(f"{c:4d} {c % 3:3d} {r[0]:10d} {r[1]:10d} {r[2]:8d} | {r[3]:8d} {r[4]:7d} {r[5]:9d} {r[6]:11d} | "
+          f"{r[2]-r[1]:6d} {r[6]-r[5]:6d}")
 print("epilogue segments:", " ".join(str(int(v - t0)) for v in t[6] if v))
