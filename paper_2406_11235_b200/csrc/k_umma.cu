@@ -199,20 +199,23 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
         // before the PDL wait; the x~ slabs (the previous kernel's output) after it, each one ahead of
         // its cell's weights, so a slab never waits behind later weight cells in the SM's TMA queue
         // (a separate x~ warp's copies did: traced MMA cadence 700 -> 1000 cycles per cell).
+        // Its per-cell path is kept short (incremental cursors, one elected issue block): the warp
+        // shares its sub-partition with three decoder warps (traced: ~350 cycles per bulk-copy issue
+        // with per-cell divisions, which paced the whole pipeline).
         const uint64_t pol = ptx::l2_evict_first_policy();
+        const bool tr = trc != nullptr;
         const int ua = range_lo(a.U, a.W, blockIdx.x), ub = range_lo(a.U, a.W, blockIdx.x + 1);
         const int nc = ub - ua, pre = nc < S ? nc : S;
         int gw = (int)(ua / Ul), ulw = ua - gw * Ul;          // weight cursor (layer, cell in layer)
         const uint32_t* src = a.packed[gw] + (a.rb0 * n_kc + ulw) * a.lay.cell_words;
+        const uint32_t ring0 = ptx::smem_u32(ring);
         int s = 0;
         uint32_t r = 0;                                       // fills of stage s so far, mod 2
-        auto issue_w = [&](int j) {
-            if (j >= S) ptx::mbar_wait(empty(s), r ^ 1u);
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
-                ptx::bulk_g2s_policy(ptx::smem_u32(ring + (size_t)s * kCellBytes), src, kCellBytes, full(s), pol);
-            }
-            __syncwarp();
+        auto issue_w = [&]() {                                // (elected lane) weight cell -> stage s
+            ptx::mbar_arrive_expect_tx(full(s), kCellBytes);
+            ptx::bulk_g2s_policy(ring0 + (uint32_t)s * kCellBytes, src, kCellBytes, full(s), pol);
+        };
+        auto advance_w = [&]() {
             if (++s == S) { s = 0; r ^= 1u; }
             src += a.lay.cell_words;
             if (++ulw == Ul && gw + 1 < a.G) {
@@ -221,25 +224,40 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
                 src = a.packed[gw] + a.rb0 * n_kc * a.lay.cell_words;
             }
         };
-        for (int j = 0; j < pre; ++j) issue_w(j);
+        for (int j = 0; j < pre; ++j) {
+            if (ptx::elect_one()) issue_w();
+            __syncwarp();
+            advance_w();
+        }
         ptx::pdl_wait();                                      // x~ is the previous kernel's output
         int gx = (int)(ua / Ul), ulx = ua - gx * Ul, KC = ulx % n_kc;   // x~ cursor
+        const uint8_t* xsrc = a.xt[gx] + (size_t)KC * a.xcol_bytes;
+        int xs = 0;                                           // x~ slot of cell j, its use parity
+        uint32_t xph = 0;
         for (int j = 0; j < nc; ++j) {
-            const int x = j % XS;
-            if (j >= XS) ptx::mbar_wait(xempty(x), (uint32_t)(((j / XS) - 1) & 1));
+            if (j >= XS) ptx::mbar_wait(xempty(xs), xph ^ 1u);
+            const bool w = j >= pre;
+            if (w && j >= S) ptx::mbar_wait(empty(s), r ^ 1u);
             if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(xfull(x), a.xcol_bytes);
-                ptx::bulk_g2s(xwin + (uint32_t)x * a.xcol_bytes, a.xt[gx] + (size_t)KC * a.xcol_bytes, a.xcol_bytes, xfull(x));
+                ptx::mbar_arrive_expect_tx(xfull(xs), a.xcol_bytes);
+                ptx::bulk_g2s(xwin + (uint32_t)xs * a.xcol_bytes, xsrc, a.xcol_bytes, xfull(xs));
+                if (w) issue_w();
             }
             __syncwarp();
-            if (lane == 0) utrace(9, j);
-            if (++KC == n_kc) KC = 0;
+            if (tr && lane == 0) utrace(9, j);
+            if (w) advance_w();
+            if (++xs == XS) { xs = 0; xph ^= 1u; }
+            xsrc += a.xcol_bytes;
+            if (++KC == n_kc) {
+                KC = 0;
+                xsrc = a.xt[gx];
+            }
             if (++ulx == Ul && gx + 1 < a.G) {
                 ulx = 0;
                 ++gx;
                 KC = 0;
+                xsrc = a.xt[gx];
             }
-            if (j >= pre) issue_w(j);
         }
     } else if (warp == 1) {
         // ================= MMA issuer.  This warp shares its SM sub-partition with three decoder warps
@@ -256,42 +274,11 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
         int ul = ua - (ua / Ul) * Ul, gl = ua / Ul;
         int seg = 0;
         uint32_t dcol = tmem;
-        bool first = true;
         int xs = 0;                                           // x~ slot of cell jj, its fill parity
         uint32_t xph = 0;
         int g = 0, b = 0;                                     // decoder group / A buffer of cell jj, buffer parity
         uint32_t aph = 0;
-        for (int jj = 0; jj < ncell; ++jj) {
-            if (jj == 0 || KC == 0) {                          // a new segment (row block) starts
-                const int d = seg & 1;
-                if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
-                ptx::tc_fence_after();
-                dcol = tmem + (uint32_t)d * kD1;
-                first = true;
-            }
-            ptx::mbar_wait(xfull(xs), xph);
-            ptx::mbar_wait(afull(g, b), aph);
-            if (tr && lane == 0) {
-                if (jj == 0) utrace(7, 1);
-                utrace(4, jj);
-            }
-            ptx::tc_fence_after();
-            const uint64_t cdesc = cdesc0 + cslot * (uint64_t)xs;
-            const uint32_t acol = tmem + kA0 + (uint32_t)(g * kNBuf + b) * kACols;
-            const bool seg_end = jj + 1 == ncell || KC == n_kc - 1;
-            if (ptx::elect_one()) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    ptx::umma_f16_ts(dcol, acol + 8u * (uint32_t)i, cdesc + (uint64_t)(dstep * (uint32_t)i), idesc,
-                                     (first && i == 0) ? 0u : 1u);
-                ptx::umma_commit(aempty(g, b));
-                if (jj + XS < ncell) ptx::umma_commit(xempty(xs));
-                if (seg_end) ptx::umma_commit(dfull(seg & 1));
-            }
-            __syncwarp();
-            if (tr && lane == 0) utrace(5, jj);
-            first = false;
-            if (seg_end) ++seg;
+        auto advance = [&]() {
             if (++KC == n_kc) KC = 0;
             if (++ul == Ul && gl + 1 < a.G) {
                 ul = 0;
@@ -303,6 +290,62 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
                 g = 0;
                 if (++b == kNBuf) { b = 0; aph ^= 1u; }
             }
+        };
+        // Two cells per iteration when the second continues the first's segment (row block): one round
+        // of bookkeeping for 16 MMAs (the loop's instruction count, not the tensor core, set the rate).
+        for (int jj = 0; jj < ncell;) {
+            const bool first = jj == 0 || KC == 0;            // a new segment (row block) starts
+            if (first) {
+                const int d = seg & 1;
+                if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
+                ptx::tc_fence_after();
+                dcol = tmem + (uint32_t)d * kD1;
+            }
+            const bool pair = jj + 1 < ncell && KC + 1 < n_kc && !(ul + 1 == Ul && gl + 1 < a.G);
+            const int xs1 = xs + 1 == XS ? 0 : xs + 1;
+            const uint32_t xph1 = xs + 1 == XS ? xph ^ 1u : xph;
+            const int g1 = g + 1 == kUG ? 0 : g + 1;
+            const int b1 = g + 1 == kUG ? (b + 1 == kNBuf ? 0 : b + 1) : b;
+            const uint32_t aph1 = (g + 1 == kUG && b + 1 == kNBuf) ? aph ^ 1u : aph;
+            ptx::mbar_wait(xfull(xs), xph);
+            ptx::mbar_wait(afull(g, b), aph);
+            if (pair) {
+                ptx::mbar_wait(xfull(xs1), xph1);
+                ptx::mbar_wait(afull(g1, b1), aph1);
+            }
+            if (tr && lane == 0) {
+                if (jj == 0) utrace(7, 1);
+                utrace(4, jj);
+            }
+            ptx::tc_fence_after();
+            const int ncl = pair ? 2 : 1;
+            const bool seg_end = jj + ncl == ncell || KC + ncl == n_kc || (pair ? (ul + 2 == Ul) : (ul + 1 == Ul));
+            if (ptx::elect_one()) {
+                const uint64_t cd0 = cdesc0 + cslot * (uint64_t)xs;
+                const uint32_t ac0 = tmem + kA0 + (uint32_t)(g * kNBuf + b) * kACols;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    ptx::umma_f16_ts(dcol, ac0 + 8u * (uint32_t)i, cd0 + (uint64_t)(dstep * (uint32_t)i), idesc,
+                                     (first && i == 0) ? 0u : 1u);
+                ptx::umma_commit(aempty(g, b));
+                if (jj + XS < ncell) ptx::umma_commit(xempty(xs));
+                if (pair) {
+                    const uint64_t cd1 = cdesc0 + cslot * (uint64_t)xs1;
+                    const uint32_t ac1 = tmem + kA0 + (uint32_t)(g1 * kNBuf + b1) * kACols;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        ptx::umma_f16_ts(dcol, ac1 + 8u * (uint32_t)i, cd1 + (uint64_t)(dstep * (uint32_t)i), idesc, 1u);
+                    ptx::umma_commit(aempty(g1, b1));
+                    if (jj + 1 + XS < ncell) ptx::umma_commit(xempty(xs1));
+                }
+                if (seg_end) ptx::umma_commit(dfull(seg & 1));
+            }
+            __syncwarp();
+            if (tr && lane == 0) utrace(5, jj);
+            if (seg_end) ++seg;
+            advance();
+            if (pair) advance();
+            jj += ncl;
         }
     } else if (warp < 6) {
         // ================= epilogue warpgroup (warps 2-5: the four TMEM lane quadrants): D (thread =

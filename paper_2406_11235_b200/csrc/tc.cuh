@@ -121,6 +121,11 @@ __device__ __forceinline__ void bulk_g2s_policy(uint32_t dst, const void* src, u
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
 }
+// L2 prefetch of a global range (no shared memory, no completion): keeps HBM requests in flight beyond
+// what a shared-memory ring can hold
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async16_stream(uint32_t dst, const void* src, uint64_t pol) {
 #if QTIP_EVICT_FIRST
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");

@@ -1,0 +1,9 @@
+O=gpurun_out/r2s3h
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bench_path.py -q -x -m gpu -k "umma or impl7 or 7 or bench" > $O/pytest.txt 2>&1
+timeout 120 python scripts/umma_trace.py hyb 4 12288 4096 1 > $O/trace_hyb4_b1.txt 2>&1
+timeout 300 python scripts/stage_flags.py hyb 4 1 7 > $O/flags_hyb4_b1_impl7.txt 2>&1
+timeout 300 python scripts/stage_flags.py hyb 4 16 7 > $O/flags_hyb4_b16_impl7.txt 2>&1
+timeout 300 python scripts/stage_flags.py 3inst 2 1 7 > $O/flags_3inst_b1_impl7.txt 2>&1
+timeout 300 python bench.py --no-cpu-baseline --no-70b --code hyb --k 4 --steps 10 > $O/hyb4_auto.json 2>&1
+timeout 300 python bench.py --no-cpu-baseline --no-70b --steps 10 --matvec-impl 7 > $O/3inst_impl7.json 2>&1

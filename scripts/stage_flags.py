@@ -33,12 +33,17 @@ def make(m, n, i):
 
 IN, OUT, XR = qtip.QTIP_RHT_IN, qtip.QTIP_RHT_OUT, qtip.QTIP_XT_READY
 modes = (("full", IN | OUT), ("in+gemv", IN), ("gemv+out", IN | XR | OUT), ("gemv", IN | XR))
-stages = {"qkv": [(4096, 4096)] * 3, "o": [(4096, 4096)], "gateup": [(11008, 4096)] * 2, "down": [(4096, 11008)]}
+stages = {"qkv": [(4096, 4096)] * 3, "o": [(4096, 4096)], "gateup": [(11008, 4096)] * 2, "down": [(4096, 11008)],
+          "big": [(12288, 4096)]}
 s = torch.cuda.Stream()
 for name, shp in stages.items():
-    if only and name not in only:
+    if (only and name not in only) or (not only and name == "big"):
         continue
     reps = [[make(m, n, 10 * r + j) for j, (m, n) in enumerate(shp)] for r in range(R)]
+    if code == "hyb":                                   # one LUT per group, as bench.py (the grouped launch)
+        for ls in reps:
+            for l_ in ls[1:]:
+                l_.lut = ls[0].lut
     n = shp[0][1]
     x = torch.from_numpy(synth.random_x(B, n, seed=1)).cuda()
     outs = [[torch.empty((B, m), device="cuda") for (m, _) in shp] for _ in range(R)]
