@@ -286,10 +286,15 @@ static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
     // layers (>= 40 cells per SM) gain (C4 8192 x 28672: 69.6 -> 66.7 us)
     // 3INST / 1MAD at batch >= 8: impl 7 beats the split-K / CUDA-core kernels on the 7B step at every
     // measured batch (B = 8 / 16 / 32: 265 -> 300, 160 -> 193, 42 -> 70 GB/s, profiles/r2/batch_*)
+    // HYB at any batch once every SM has >= 10 cells: the x~ slab ring (round 2) removed the batch
+    // limit (B = 16: q,k,v 39.1 -> 27.4 us, gate,up 62.1 -> 28.9 us, down 33.0 -> 23.0 us vs the
+    // split-K kernel, profiles/r2s3/)
     const int64_t cells = (int64_t)G * l.n_rb * l.n_kc;
     if (p->code != QTIP_CODE_HYB && B >= 8) return true;
-    const int64_t min_cells = (p->code == QTIP_CODE_HYB ? 10 : 40) * (int64_t)num_sms();
-    return B <= 8 && cells >= min_cells;
+    // 3INST / 1MAD at batch 1-7: >= 20 cells per SM (the grouped q,k,v and gate,up launches: 17.6 ->
+    // 17.2 us, 26.8 -> 25.6 us with the selector pair sum; single 4096-row layers keep impls 3/4)
+    const int64_t min_cells = (p->code == QTIP_CODE_HYB ? 10 : 20) * (int64_t)num_sms();
+    return (p->code == QTIP_CODE_HYB || B <= 8) && cells >= min_cells;
 }
 
 int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B) {

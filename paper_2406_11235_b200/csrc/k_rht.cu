@@ -82,8 +82,9 @@ struct RhtIO {
     int zero_n;
 };
 
+// the batched plans (E = 1, RA >= 8: n = 11008, B = 16 -> 352 CTAs) fit one wave at 3 CTAs per SM
 template <int E, int RA>
-__global__ void __launch_bounds__(kRhtThreads) rht_kernel(RhtPlan plan, const __grid_constant__ RhtIO io,
+__global__ void __launch_bounds__(kRhtThreads, (E == 1 && RA >= 8) ? 3 : 1) rht_kernel(RhtPlan plan, const __grid_constant__ RhtIO io,
                                                            int64_t in_stride, int64_t out_stride, int inverse,
                                                            int out_mode, int64_t pad_to,
                                                            int* __restrict__ zero_ptr, int zero_n) {

@@ -13,11 +13,19 @@
 namespace qtip {
 namespace udec {
 
-// binary16 sums of the two halves of za and of zb, packed (lo: za, hi: zb): HADD2 with RNE
+// binary16 sums of the two halves of za and of zb, packed (lo: za, hi: zb), RNE.  Two scalar half adds
+// whose operands are half-selectors of one register each (HADD2 Rz.H0_H0, Rz.H1_H1) and one PRMT to
+// pack: 1 FMA-pipe + 0.5 ALU instruction per weight, instead of two PRMT transposes + one HADD2
+// (1 ALU + 0.5 FMA) -- the ALU pipe is the 3INST decode's binding one (DESIGN 5.5)
 __device__ __forceinline__ uint32_t pair_sum(uint32_t za, uint32_t zb) {
-    const uint32_t lo = __byte_perm(za, zb, 0x5410), hi = __byte_perm(za, zb, 0x7632);
     uint32_t r;
-    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(lo), "r"(hi));
+    asm("{\n\t.reg .f16 a0, a1, b0, b1, s0, s1;\n\t"
+        "mov.b32 {a0, a1}, %1;\n\t"
+        "mov.b32 {b0, b1}, %2;\n\t"
+        "add.rn.f16 s0, a0, a1;\n\t"
+        "add.rn.f16 s1, b0, b1;\n\t"
+        "mov.b32 %0, {s0, s1};\n\t}"
+        : "=r"(r) : "r"(za), "r"(zb));
     return r;
 }
 
