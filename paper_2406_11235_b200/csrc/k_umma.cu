@@ -150,13 +150,20 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
     // ---------------- setup (static data only: overlaps the previous kernel under PDL)
     if constexpr (kHyb) {
         // entry e = idx | sign << 9 -> (c0, c1) with c1 negated for sign (Alg. 3), replica r at
-        // word 32 e + r: conflict-free LDS for any entries
+        // word 32 e + r: conflict-free LDS for any entries.  512 threads x 16 consecutive-lane vector
+        // stores, all 16 loads issued first (one dependent L2 load per store was ~10 % of a launch:
+        // ncu, profiles/r2s3)
         uint4* lt = reinterpret_cast<uint4*>(smem + kHdr);
-        for (int i = threadIdx.x; i < (1 << (kLutQ + 1)) * 8; i += kUThreads) {
-            const int e = i >> 3;
-            uint32_t w = __ldg(a.lut + (e & ((1 << kLutQ) - 1)));
-            if (e >> kLutQ) w ^= 0x80000000u;
-            lt[i] = make_uint4(w, w, w, w);
+        constexpr int kFill = (1 << (kLutQ + 1)) * 8 / 512;  // 16
+        if (threadIdx.x < 512) {
+            uint32_t w[kFill];
+#pragma unroll
+            for (int k = 0; k < kFill; ++k) {
+                const int e = (threadIdx.x + 512 * k) >> 3;
+                w[k] = __ldg(a.lut + (e & ((1 << kLutQ) - 1))) ^ ((e >> kLutQ) ? 0x80000000u : 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < kFill; ++k) lt[threadIdx.x + 512 * k] = make_uint4(w[k], w[k], w[k], w[k]);
         }
     }
     if (warp == 0) {
@@ -235,9 +242,9 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
         int xs = 0;                                           // x~ slot of cell j, its use parity
         uint32_t xph = 0;
         for (int j = 0; j < nc; ++j) {
-            if (j >= XS) ptx::mbar_wait(xempty(xs), xph ^ 1u);
+            if (j >= XS) ptx::mbar_wait_sleep(xempty(xs), xph ^ 1u);
             const bool w = j >= pre;
-            if (w && j >= S) ptx::mbar_wait(empty(s), r ^ 1u);
+            if (w && j >= S) ptx::mbar_wait_sleep(empty(s), r ^ 1u);
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(xfull(xs), a.xcol_bytes);
                 ptx::bulk_g2s(xwin + (uint32_t)xs * a.xcol_bytes, xsrc, a.xcol_bytes, xfull(xs));
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
             const bool first = jj == 0 || KC == 0;            // a new segment (row block) starts
             if (first) {
                 const int d = seg & 1;
-                if (seg >= 2) ptx::mbar_wait(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
+                if (seg >= 2) ptx::mbar_wait_sleep(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
                 ptx::tc_fence_after();
                 dcol = tmem + (uint32_t)d * kD1;
             }
@@ -307,11 +314,11 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
             const int g1 = g + 1 == kUG ? 0 : g + 1;
             const int b1 = g + 1 == kUG ? (b + 1 == kNBuf ? 0 : b + 1) : b;
             const uint32_t aph1 = (g + 1 == kUG && b + 1 == kNBuf) ? aph ^ 1u : aph;
-            ptx::mbar_wait(xfull(xs), xph);
-            ptx::mbar_wait(afull(g, b), aph);
+            ptx::mbar_wait_sleep(xfull(xs), xph);
+            ptx::mbar_wait_sleep(afull(g, b), aph);
             if (pair) {
-                ptx::mbar_wait(xfull(xs1), xph1);
-                ptx::mbar_wait(afull(g1, b1), aph1);
+                ptx::mbar_wait_sleep(xfull(xs1), xph1);
+                ptx::mbar_wait_sleep(afull(g1, b1), aph1);
             }
             if (tr && lane == 0) {
                 if (jj == 0) utrace(7, 1);
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
             const int ua = range_lo(a.U, a.W, w), ub = range_lo(a.U, a.W, w + 1);
             for (int RBv = ua / n_kc; RBv <= (ub - 1) / n_kc; ++RBv, ++seg) {
                 const int d = seg & 1;
-                ptx::mbar_wait(dfull(d), (uint32_t)((seg >> 1) & 1));
+                ptx::mbar_wait_sleep(dfull(d), (uint32_t)((seg >> 1) & 1));
                 if (R == 0) utrace(6, seg);
                 ptx::tc_fence_after();
                 const int g = RBv / a.nrb, RB = RBv - g * a.nrb;
@@ -438,9 +445,9 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
             const uint32_t r = (uint32_t)((jj / S) & 1);
             const int b = lc & (kNBuf - 1), use = lc / kNBuf;
             const bool tr = lane == 0 && dw == 4 * g;
-            ptx::mbar_wait(full(s), r);
+            ptx::mbar_wait_sleep(full(s), r);
             if (tr) utrace(1, jj);
-            if (use > 0) ptx::mbar_wait(aempty(g, b), (uint32_t)((use - 1) & 1));
+            if (use > 0) ptx::mbar_wait_sleep(aempty(g, b), (uint32_t)((use - 1) & 1));
             if (tr) utrace(2, jj);
             ptx::tc_fence_after();
             const uint32_t* cellw = reinterpret_cast<const uint32_t*>(ring + (size_t)s * kCellBytes);

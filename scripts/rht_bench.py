@@ -2,7 +2,7 @@
 """Time qtip_rht (forward and inverse, fp32 out) per call for the 7B / 70B orders and batch widths:
 a CUDA graph of 50 back-to-back calls, CUDA events.
 
-usage: python scripts/rht_bench.py [B list, comma-separated]
+usage: python scripts/rht_bench.py [B list, comma-separated] [n list, comma-separated]
 """
 import os
 import sys
@@ -17,7 +17,8 @@ qtip.load()
 Bs = [int(b) for b in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 2, 4, 8, 16]
 R = 50
 st = torch.cuda.Stream()
-for n in [4096, 11008, 8192, 28672]:
+Ns = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [4096, 11008, 8192, 28672]
+for n in Ns:
     for B in Bs:
         s = torch.from_numpy(synth.random_sign_bytes(n, 1)).cuda()
         x = torch.from_numpy(synth.random_x(B, n, seed=2)).cuda()
