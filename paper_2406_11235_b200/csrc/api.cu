@@ -291,9 +291,10 @@ static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
     // split-K kernel, profiles/r2s3/)
     const int64_t cells = (int64_t)G * l.n_rb * l.n_kc;
     if (p->code != QTIP_CODE_HYB && B >= 8) return true;
-    // 3INST / 1MAD at batch 1-7: >= 20 cells per SM (the grouped q,k,v and gate,up launches: 17.6 ->
-    // 17.2 us, 26.8 -> 25.6 us with the selector pair sum; single 4096-row layers keep impls 3/4)
-    const int64_t min_cells = (p->code == QTIP_CODE_HYB ? 10 : 20) * (int64_t)num_sms();
+    // 3INST at batch 1-7: >= 20 cells per SM (the grouped q,k,v and gate,up launches: 17.6 -> 17.2 us,
+    // 26.8 -> 25.6 us with the selector pair sum; single 4096-row layers keep impls 3/4); 1MAD >= 40
+    // (its 7B step lost 534 -> 521 GB/s at 20)
+    const int64_t min_cells = (p->code == QTIP_CODE_HYB ? 10 : p->code == QTIP_CODE_3INST ? 20 : 40) * (int64_t)num_sms();
     return (p->code == QTIP_CODE_HYB || B <= 8) && cells >= min_cells;
 }
 

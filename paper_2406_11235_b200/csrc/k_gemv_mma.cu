@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, (K == 2 && NG == 1) ? 8 : (NG 
     int j = 0;
     for (;; ++j) {
         const int st = j % kMmaStages;
-        ptx::mbar_wait(ptx::smem_u32(full + st), (j / kMmaStages) & 1);
+        ptx::mbar_wait_sleep(ptx::smem_u32(full + st), (j / kMmaStages) & 1);
         const int64_t u = s_unit[st];
         if (u < 0) break;
         const int64_t RB = args.rb0 + u / n_kc, KC = u % n_kc;

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(32 * kRowMaxWarps, 2) gemv_row_kernel(const Ro
     float acc[1][4] = {{0.0f, 0.0f, 0.0f, 0.0f}};
     for (int j = 0; j < ncells; ++j) {
         const int st = j % S;
-        ptx::mbar_wait(ptx::smem_u32(full + st), (j / S) & 1);
+        ptx::mbar_wait_sleep(ptx::smem_u32(full + st), (j / S) & 1);
         const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring + st * stage_bytes);
         const uint32_t* xs = reinterpret_cast<const uint32_t*>(ring + st * stage_bytes + kChunkBytes);
 #pragma unroll

@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_kernel(const __grid_consta
         uint32_t phase = 0;
         for (UnitIt it = first; it.L < L1i; it.step(n_units)) {
             float acc[2][1][4] = {{{0.f, 0.f, 0.f, 0.f}}, {{0.f, 0.f, 0.f, 0.f}}};
-            ptx::mbar_wait(full0 + 8 * st, phase);
+            ptx::mbar_wait_sleep(full0 + 8 * st, phase);
             const uint32_t* chunk = reinterpret_cast<const uint32_t*>(ring0 + (size_t)st * chunk_bytes);
             const uint32_t* xu = xsl + ustride * it.u;              // x~ of the unit's 8 tile columns
             // all shared-memory operands of the unit are loaded up front (the decode then never waits

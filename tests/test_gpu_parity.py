@@ -94,7 +94,7 @@ def test_c1_viterbi_quantized_tiles_through_pack_states(cuda_lib):
 
 
 @pytest.mark.parametrize("n", [256, 4096, 8192, 11008, 28672, 12 * 16, 28 * 8, 20 * 256])
-@pytest.mark.parametrize("B", [1, 3])
+@pytest.mark.parametrize("B", [1, 3, 8, 16])  # 8, 16: the batched plans (rows of D per CTA up to 16)
 def test_rht_matches_oracle(cuda_lib, n, B):
     from paper_2406_11235_b200 import qtip
     x = synth.random_x(B, n, seed=2000 + n)
