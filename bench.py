@@ -475,6 +475,35 @@ def run_ours(args):
         us = max_over_ranks(1e3 * e0.elapsed_time(e1) / (max(1, args.steps // 2) * len(idx)))
         per_layer[f"{m}x{n}"] = {"us_per_layer": round(us, 3),
                                  "GBps": round(m * n * k / 8 / (us * 1e-6) / 1e9, 1)}
+        if world == 1:
+            # spread over single-layer replays (each bracketed by its own events, which add a few us of
+            # event overhead: a distribution, not the step's per-layer time) and one cold call (L2
+            # flushed by a 256 MB write, eager launches)
+            l0 = layers[idx[0]]
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g1, stream=s):
+                    l0.forward(xs[n], out=outs[idx[0]])
+            torch.cuda.current_stream().wait_stream(s)
+            g1.replay()
+            single = []
+            for _ in range(20):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record()
+                g1.replay()
+                a1.record()
+                torch.cuda.synchronize()
+                single.append(1e3 * a0.elapsed_time(a1))
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+            flush.fill_(1)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            l0.forward(xs[n], out=outs[idx[0]])
+            a1.record()
+            torch.cuda.synchronize()
+            del flush, g1
+            per_layer[f"{m}x{n}"].update({"single_replay_us_p10_p50_p90": [round(float(v), 2) for v in np.percentile(single, [10, 50, 90])],
+                                          "cold_call_us": round(1e3 * a0.elapsed_time(a1), 2)})
 
     # ---- dominant kernel (fused decode-GEMV): the step's GEMV launches alone, back to back in a
     #      graph (each layer's x~ is already in its workspace: QTIP_XT_READY skips the RHT-in;

@@ -254,7 +254,8 @@ qtip_status qtip_quantize_matrix(const qtip_params* p, int64_t m, int64_t n, con
  * B <= 4), 5 = fused single-launch layer kernel (RHT-in, GEMV, RHT-out with in-kernel grid
  * barriers), 6 = RHT kernels around the persistent row-owning GEMV of 5, 7 = RHT kernels around the
  * stream-K tcgen05 GEMV (k_umma.cu: decoded binary16 weights in TMEM, asynchronous UMMA, equal
- * cell ranges per SM; auto for HYB at B <= 8 with >= 10 cells per SM).
+ * cell ranges per SM, one x~ slab per cell; auto for HYB at every batch with >= 10 cells per SM,
+ * for 3INST with >= 20 cells per SM below batch 8 and at every size from batch 8, for 1MAD with >= 40).
  * Process-wide; for ablations and tests. */
 void qtip_set_matvec_impl(int impl);
 int qtip_get_matvec_impl(void);

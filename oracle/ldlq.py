@@ -75,16 +75,6 @@ def proxy_loss(W, What, H):
     return float(np.trace(E @ np.asarray(H, dtype=np.float64) @ E.T))
 
 
-def synthetic_hessian(n, N=None, rho=0.9, damp=1e-2, seed=6000):
-    """A proxy Hessian H = X^T X / N + damp * mean(diag) I of N activation rows drawn from an AR(1)
-    Gaussian (correlation rho^|i-j|): PSD, correlated like real layer inputs (no trained weights or
-    datasets are available here)."""
-    rng = np.random.default_rng(seed)
-    N = N or 4 * n
-    Z = rng.standard_normal((N, n))
-    X = np.empty_like(Z)
-    X[:, 0] = Z[:, 0]
-    for i in range(1, n):
-        X[:, i] = rho * X[:, i - 1] + np.sqrt(1 - rho * rho) * Z[:, i]
-    H = X.T @ X / N
-    return H + damp * np.mean(np.diag(H)) * np.eye(n)
+# the synthetic proxy Hessian is an input recipe (no method arithmetic): it lives in synth/, shared
+# by the oracle's tests and the GPU tests
+from synth import synthetic_hessian  # noqa: E402,F401

@@ -53,3 +53,18 @@ def gaussian_table(nbits, seed=4001):
 def gaussian_source(nseq, T, seed=5000):
     rng = np.random.default_rng(seed)
     return rng.standard_normal((nseq, T))
+
+
+def synthetic_hessian(n, N=None, rho=0.9, damp=1e-2, seed=6000):
+    """A proxy Hessian H = X^T X / N + damp * mean(diag) I of N activation rows drawn from an AR(1)
+    Gaussian (correlation rho^|i-j|): PSD, correlated like real layer inputs (no trained weights or
+    datasets are available here; reading R21)."""
+    rng = np.random.default_rng(seed)
+    N = N or 4 * n
+    Z = rng.standard_normal((N, n))
+    X = np.empty_like(Z)
+    X[:, 0] = Z[:, 0]
+    for i in range(1, n):
+        X[:, i] = rho * X[:, i - 1] + np.sqrt(1 - rho * rho) * Z[:, i]
+    H = X.T @ X / N
+    return H + damp * np.mean(np.diag(H)) * np.eye(n)
