@@ -275,6 +275,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     qtip.load()
     qtip.set_matvec_impl(args.matvec_impl)
+    if os.environ.get("QTIP_L2_PREFETCH") is not None:       # ablation: MiB of weights the RHT-in prefetches (0 = off)
+        qtip.load().qtip_internal_set_knob(4, int(os.environ["QTIP_L2_PREFETCH"]))
 
     nblocks, shapes, dcode, dk = WORKLOADS[args.workload]
     if args.blocks:

@@ -22,6 +22,8 @@ impl = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 only = sys.argv[5].split(",") if len(sys.argv) > 5 else None
 qtip.load()
 qtip.set_matvec_impl(impl)
+if os.environ.get("QTIP_L2_PREFETCH") is not None:
+    qtip.load().qtip_internal_set_knob(4, int(os.environ["QTIP_L2_PREFETCH"]))
 lut = synth.gaussian_lut(9) if code == "hyb" else None
 R = 32
 
