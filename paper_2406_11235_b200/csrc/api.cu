@@ -63,6 +63,8 @@ void count_launch(int n) { g_launches += (uint64_t)n; }
 bool g_pdl = true;
 bool g_fused_reduce = false;
 bool g_layer_auto = false;     // auto-pick the fused layer kernel (knob 3)
+int g_l2_prefetch = 0;         // knob 4: RHT-in L2-prefetches up to this many MiB of the layer's weights (0 = off;
+                               // measured: 542 -> 536 GB/s 3INST, 1153 -> 1124 HYB at 64 MiB, profiles/r2s3/)
 bool pdl_enabled() { return g_pdl; }
 
 void prefer_max_smem(const void* kern) {
@@ -298,6 +300,21 @@ static bool use_umma(const qtip_params* p, const Layout& l, int64_t B, int G) {
     return (p->code == QTIP_CODE_HYB || B <= 8) && cells >= min_cells;
 }
 
+// The RHT-in launch that precedes a GEMV prefetches the GEMV's weights (row blocks [rb0, rb1) of
+// each layer, at most g_l2_prefetch MiB per layer) into L2 before its PDL wait (DESIGN 5.4).
+static void prefetch_weights(const Layout& l, int G, const void* const* packed, int64_t rb0, int64_t rb1) {
+    if (g_l2_prefetch <= 0) return;
+    const void* ptr[kMaxGroup];
+    uint64_t bytes[kMaxGroup];
+    const uint64_t cellb = (uint64_t)l.cell_words * 4u, cap = (uint64_t)g_l2_prefetch << 20;
+    for (int g = 0; g < G; ++g) {
+        ptr[g] = (const char*)packed[g] + (uint64_t)rb0 * (uint64_t)l.n_kc * cellb;
+        const uint64_t b = (uint64_t)(rb1 - rb0) * (uint64_t)l.n_kc * cellb;
+        bytes[g] = b < cap ? b : cap;
+    }
+    rht_set_prefetch(G, ptr, bytes);
+}
+
 int qtip_matvec_group_fused(const qtip_params* p, int G, int64_t m, int64_t n, int64_t B) {
     if (G < 2 || G > kMaxGroup || qtip_params_check(p) != QTIP_OK || check_shape(m, n) != QTIP_OK || B < 1 || B > 64)
         return 0;
@@ -371,6 +388,7 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
         for (int g = 0; g < G; ++g) tk0[g] = (int*)((char*)d_workspace[g] + o.cnt);
         if (!xready) {
             if (rin) {
+                prefetch_weights(l, G, d_packed, 0, l.n_rb);
                 e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, bp, 0, std::vector<float>(G, 1.0f).data(), s, xmode,
                                      l.n_pad, tk0, (int)l.n_rb);
             } else {
@@ -430,6 +448,7 @@ qtip_status qtip_matvec_group(const qtip_params* p, int G, int64_t m, int64_t n,
     }
     if (!xready) {                                                // also clears the barrier / ticket words
         if (rin) {
+            prefetch_weights(l, G, d_packed, 0, l.n_rb);
             e = launch_rht_group(pn, G, B, d_sign_n, xin, n, xt, l.n_pad, 0, std::vector<float>(G, 1.0f).data(), s,
                                  xmode6, l.n_pad, (int* const*)bar, 256);
         } else {
@@ -539,7 +558,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         int* tk0 = (int*)(ws + o.cnt);                   // the GEMV's row-block tickets: cleared here
         const int ntk = (int)(rb1 - rb0);
         if (!(flags & QTIP_XT_READY)) {
-            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, bp, 0, 1.0f, s, xmode, l.n_pad, tk0, ntk);
+            if (rin) {
+                prefetch_weights(l, 1, &d_packed, rb0, rb1);
+                e = launch_rht(pn, B, d_sign_n, d_x, n, xt, bp, 0, 1.0f, s, xmode, l.n_pad, tk0, ntk);
+            }
             else e = launch_convert(d_x, n, n, B, xt, bp, xmode, l.n_pad, s, tk0, ntk);
         }
         if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
@@ -602,7 +624,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
         const int xmode6 = p->code == QTIP_CODE_HYB ? 5 : xmode;   // HYB fast path: swapped pairs
         e = cudaSuccess;
         if (!(flags & QTIP_XT_READY)) {                          // also clears the barrier / ticket words
-            if (rin) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode6, l.n_pad, (int*)bar, 256);
+            if (rin) {
+                prefetch_weights(l, 1, &d_packed, rb0, rb1);
+                e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode6, l.n_pad, (int*)bar, 256);
+            }
             else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode6, l.n_pad, s, (int*)bar, 256);
         }
         if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
@@ -637,7 +662,10 @@ qtip_status qtip_matvec(const qtip_params* p, int64_t m, int64_t n, int64_t B, c
     }
     // the input kernel also clears the GEMV's split-K arrival counters (workspace is caller memory)
     if (flags & QTIP_XT_READY) e = cudaSuccess;          // counters are left zero by every GEMV
-    else if (flags & QTIP_RHT_IN) e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 2);
+    else if (flags & QTIP_RHT_IN) {
+        prefetch_weights(l, 1, &d_packed, rb0, rb1);
+        e = launch_rht(pn, B, d_sign_n, d_x, n, xt, l.n_pad, 0, 1.0f, s, xmode, l.n_pad, cnt, n_rb + 2);
+    }
     else e = launch_convert(d_x, n, n, B, xt, l.n_pad, xmode, l.n_pad, s, cnt, n_rb + 2);
     if (e != cudaSuccess) return cuda_fail(e, "qtip_matvec rht_in");
     const bool prof = g_prof_start && g_prof_stop;
@@ -794,6 +822,7 @@ extern "C" int qtip_internal_set_knob(int key, int value) {
     if (key == 1) { g_fused_reduce = value != 0; return 0; }
     if (key == 2) { qtip::g_layer_debug = value; return 0; }
     if (key == 3) { g_layer_auto = value != 0; return 0; }
+    if (key == 4) { g_l2_prefetch = value; return 0; }
     return -1;
 }
 

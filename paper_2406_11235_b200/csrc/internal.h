@@ -99,6 +99,9 @@ cudaError_t launch_rht_group(const RhtPlan& plan, int G, int64_t B, const uint8_
                              int64_t in_stride, void* const* out, int64_t out_stride, int inverse, const float* scale,
                              cudaStream_t s, int out_mode = 0, int64_t pad_to = 0, int* const* zero = nullptr,
                              int zero_n = 0);
+// The next launch_rht / launch_rht_group on this host thread L2-prefetches bytes[g] from ptr[g]
+// (its transform g) before its PDL wait: the weights of the GEMV that follows it.
+void rht_set_prefetch(int G, const void* const* ptr, const uint64_t* bytes);
 // x (float32) -> out_mode encoding, zero padded to pad_to (used when RHT-in is off).
 cudaError_t launch_convert(const float* in, int64_t n, int64_t in_stride, int64_t B, void* out, int64_t out_stride,
                            int out_mode, int64_t pad_to, cudaStream_t s, int* zero_ptr = nullptr, int zero_n = 0);

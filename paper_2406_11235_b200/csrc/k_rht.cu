@@ -80,7 +80,21 @@ struct RhtIO {
     float out_scale[kMaxGroup];
     int* zero[kMaxGroup];                                    // cleared after the PDL wait (the GEMV's counters)
     int zero_n;
+    const uint8_t* pf[kMaxGroup];                            // L2 prefetch of the next GEMV's weights (or null)
+    uint64_t pf_bytes[kMaxGroup];
 };
+
+// Pending L2 prefetch for the next RHT launch on this host thread (rht_set_prefetch): the RHT-in
+// kernel of a layer prefetches that layer's packed weights into L2 before its PDL wait -- the
+// weights are static, so the prefetch overlaps the previous kernels, and the GEMV that follows
+// starts on L2 hits instead of HBM latency.
+static thread_local RhtIO t_pf{};
+void rht_set_prefetch(int G, const void* const* ptr, const uint64_t* bytes) {
+    for (int g = 0; g < kMaxGroup; ++g) {
+        t_pf.pf[g] = g < G ? (const uint8_t*)ptr[g] : nullptr;
+        t_pf.pf_bytes[g] = g < G ? bytes[g] : 0;
+    }
+}
 
 // the batched plans (E = 1, RA >= 8: n = 11008, B = 16 -> 352 CTAs) fit one wave at 3 CTAs per SM
 template <int E, int RA>
@@ -111,6 +125,13 @@ __global__ void __launch_bounds__(kRhtThreads, (E == 1 && RA >= 8) ? 3 : 1) rht_
     CtaTrace trace{trace_ts};
     trace.entry(g_rht_trace);
 
+    // L2 prefetch of the next GEMV's weights (static data: before the PDL wait), one slice per CTA
+    if (tid == 0 && io.pf[z] != nullptr) {
+        const uint64_t ncta = (uint64_t)gridDim.x * gridDim.y, cid = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        const uint64_t per = ((io.pf_bytes[z] + ncta - 1) / ncta + 15) & ~15ull;
+        const uint64_t lo = cid * per, hi = lo + per < io.pf_bytes[z] ? lo + per : io.pf_bytes[z];
+        for (uint64_t o = lo; o < hi; o += 65536) ptx::bulk_prefetch_l2(io.pf[z] + o, (uint32_t)(hi - o < 65536 ? hi - o : 65536));
+    }
     // D rows of this CTA (static tables only: overlaps the previous kernel under PDL)
     {
         const uint32_t* hb = inverse ? plan.hbt : plan.hb;
@@ -330,9 +351,16 @@ static cudaError_t launch_rht_t(const RhtPlan& plan, int G, int64_t B, const Rht
                       zero_ptr, zero_n);
 }
 
-static cudaError_t launch_rht_io(const RhtPlan& plan, int G, int64_t B, const RhtIO& io, int64_t in_stride,
+static cudaError_t launch_rht_io(const RhtPlan& plan, int G, int64_t B, const RhtIO& io_in, int64_t in_stride,
                                  int64_t out_stride, int inverse, cudaStream_t s, int out_mode, int64_t pad_to,
                                  int* zero_ptr, int zero_n) {
+    RhtIO io = io_in;
+    for (int g = 0; g < kMaxGroup; ++g) {                   // take (and clear) the pending prefetch
+        io.pf[g] = t_pf.pf[g];
+        io.pf_bytes[g] = t_pf.pf_bytes[g];
+        t_pf.pf[g] = nullptr;
+        t_pf.pf_bytes[g] = 0;
+    }
     const int64_t pad = pad_to < plan.n ? plan.n : pad_to;
     cudaError_t e = cudaErrorInvalidValue;
 #define QTIP_RHT_CASE(EE, RR) \
