@@ -77,6 +77,29 @@ def test_bench_step_calls_every_row_vs_oracle(cuda_lib, code, k, what, m, n, G):
         assert rel_l2(y, ref) <= TOL
 
 
+@pytest.mark.parametrize("code,k,B", [("hyb", 4, 16), ("hyb", 4, 64), ("3inst", 2, 64)])
+def test_batched_tcgen05_slab_ring_wraps_vs_oracle(cuda_lib, code, k, B):
+    """The stream-K tcgen05 kernel (impl 7) at batch 16 / 64 on a 4096 x 8192 layer: 2048 cells over
+    the SMs is ~14 per CTA, more than the x~ slab slots that fit next to the HYB LUT at B = 16 (11) or
+    at B = 64 (2 with the LUT, 10 without), so every slot is refilled while the ring runs; every row
+    of every batch column vs the float64 oracle."""
+    from paper_2406_11235_b200 import qtip
+    m, n = 4096, 8192
+    layers, lut = _layers(cuda_lib, code, k, m, n, 1, seed0=1700 + B)
+    lay, tiles, sm, sn = layers[0]
+    x = synth.random_x(B, n, seed=2100 + B)
+    qtip.set_matvec_impl(7)
+    try:
+        y = lay(torch.from_numpy(x).cuda()).cpu().numpy()
+    finally:
+        qtip.set_matvec_impl(0)
+    p = gemv.Params(k=k, V=2 if code == "hyb" else 1, code=code, lut=lut)
+    ref = oracle_matvec_blocked(tiles, p, x, sn, sm, 1.0)
+    assert y.shape == ref.shape
+    for b in range(B):
+        assert rel_l2(y[b], ref[b]) <= TOL, b
+
+
 def _tile_positions(m, n, j):
     """(I, J, r, c) of the weights W~[:, j] and their sequence positions p = 16 r + c."""
     rows = np.arange(m)
