@@ -87,7 +87,7 @@ struct UmmaArgs {
     int W;                                   // ranges
     int B, BP;
     float code_factor;
-    uint32_t off_ring, off_x;                // shared-memory offsets (LUT at kHdr)
+    uint32_t off_ring, off_x, off_rec;       // shared-memory offsets (LUT at kHdr; MMA cell records)
     uint32_t xcol_bytes;                     // x~ bytes per cell column (one slab)
     int XS;                                  // x~ slab slots
     uint32_t lbo, sbo;
@@ -268,91 +268,82 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
         }
     } else if (warp == 1) {
         // ================= MMA issuer.  This warp shares its SM sub-partition with three decoder warps
-        // and gets ~1/4 of its issue slots, so its per-cell path is kept short: incremental counters
-        // (no runtime divisions), descriptors advanced by constants, tracing behind one uniform test
-        // (traced before: ~180 instructions and ~650 cycles per cell, the kernel's bottleneck).
+        // and gets ~1/4 of its issue slots, so its per-cell path is kept short: every cell's metadata
+        // (A buffer, x~ slot, barrier phases, segment flags) is computed up front by the 32 lanes into
+        // an 8-byte shared-memory record, and the loop only reads two records, waits and issues the
+        // MMAs of one or two cells (two when the second continues the first's row block).  (Traced:
+        // the incremental-counter loop was ~130 SASS instructions per cell, ~650 cycles, and paced
+        // the kernel.)
         const int ua = range_lo(a.U, a.W, blockIdx.x), ub = range_lo(a.U, a.W, blockIdx.x + 1);
         const int ncell = ub - ua;
         const uint32_t dstep = 2u * (uint32_t)a.BP;           // B descriptor step per MMA (16 K)
         const uint64_t cdesc0 = ptx::smem_desc_kmajor_noswizzle(xwin, a.lbo, a.sbo);
         const uint64_t cslot = (uint64_t)(a.xcol_bytes >> 4);  // descriptor start-address step per slot
         const bool tr = trc != nullptr;
-        int KC = (ua - (ua / Ul) * Ul) % n_kc;
-        int ul = ua - (ua / Ul) * Ul, gl = ua / Ul;
-        int seg = 0;
+        uint2* rec = reinterpret_cast<uint2*>(smem + a.off_rec);
+        {
+            const int KC0 = (ua - (ua / Ul) * Ul) % n_kc;     // row blocks are whole within a layer, so
+            for (int jj = lane; jj < ncell; jj += 32) {       // the segment of cell jj is (KC0 + jj) / n_kc
+                const int KC = (KC0 + jj) % n_kc, seg = (KC0 + jj) / n_kc;
+                const int xs = jj % XS, lc = jj / kUG, ab = (jj % kUG) * kNBuf + (lc & (kNBuf - 1));
+                const uint32_t first = (jj == 0 || KC == 0) ? 1u : 0u;
+                const uint32_t meta = (uint32_t)xs | ((uint32_t)ab << 6) | ((uint32_t)((jj / XS) & 1) << 9) |
+                                      ((uint32_t)((lc / kNBuf) & 1) << 10) | (first << 11) |
+                                      ((jj + 1 == ncell || KC == n_kc - 1) ? 1u << 12 : 0u) |
+                                      ((jj + XS < ncell) ? 1u << 13 : 0u) | ((uint32_t)(seg & 1) << 14) |
+                                      ((first && seg >= 2) ? 1u << 15 : 0u) | ((uint32_t)(((seg >> 1) - 1) & 1) << 16);
+                rec[jj] = make_uint2(tmem + kA0 + (uint32_t)ab * kACols, meta);
+            }
+            __syncwarp();
+        }
+        constexpr uint32_t kFirst = 1u << 11, kSegEnd = 1u << 12, kCommitX = 1u << 13, kDWait = 1u << 15;
+        const uint32_t afull0 = bar0 + 8u * (2 * S), aempty0 = bar0 + 8u * (2 * S + kUG * kNBuf);
         uint32_t dcol = tmem;
-        int xs = 0;                                           // x~ slot of cell jj, its fill parity
-        uint32_t xph = 0;
-        int g = 0, b = 0;                                     // decoder group / A buffer of cell jj, buffer parity
-        uint32_t aph = 0;
-        auto advance = [&]() {
-            if (++KC == n_kc) KC = 0;
-            if (++ul == Ul && gl + 1 < a.G) {
-                ul = 0;
-                ++gl;
-                KC = 0;
-            }
-            if (++xs == XS) { xs = 0; xph ^= 1u; }
-            if (++g == kUG) {
-                g = 0;
-                if (++b == kNBuf) { b = 0; aph ^= 1u; }
-            }
-        };
-        // Two cells per iteration when the second continues the first's segment (row block): one round
-        // of bookkeeping for 16 MMAs (the loop's instruction count, not the tensor core, set the rate).
         for (int jj = 0; jj < ncell;) {
-            const bool first = jj == 0 || KC == 0;            // a new segment (row block) starts
+            const uint2 r0 = rec[jj];
+            const uint2 r1 = jj + 1 < ncell ? rec[jj + 1] : make_uint2(0u, kFirst);
+            const bool pair = !(r1.y & kFirst);
+            const bool first = (r0.y & kFirst) != 0;
             if (first) {
-                const int d = seg & 1;
-                if (seg >= 2) ptx::mbar_wait_sleep(dempty(d), (uint32_t)(((seg >> 1) - 1) & 1));
+                const uint32_t d = (r0.y >> 14) & 1u;
+                if (r0.y & kDWait) ptx::mbar_wait_sleep(dempty(d), (r0.y >> 16) & 1u);
                 ptx::tc_fence_after();
-                dcol = tmem + (uint32_t)d * kD1;
+                dcol = tmem + d * kD1;
             }
-            const bool pair = jj + 1 < ncell && KC + 1 < n_kc && !(ul + 1 == Ul && gl + 1 < a.G);
-            const int xs1 = xs + 1 == XS ? 0 : xs + 1;
-            const uint32_t xph1 = xs + 1 == XS ? xph ^ 1u : xph;
-            const int g1 = g + 1 == kUG ? 0 : g + 1;
-            const int b1 = g + 1 == kUG ? (b + 1 == kNBuf ? 0 : b + 1) : b;
-            const uint32_t aph1 = (g + 1 == kUG && b + 1 == kNBuf) ? aph ^ 1u : aph;
-            ptx::mbar_wait_sleep(xfull(xs), xph);
-            ptx::mbar_wait_sleep(afull(g, b), aph);
+            const uint32_t xs0 = r0.y & 63u, ab0 = (r0.y >> 6) & 7u, xs1 = r1.y & 63u, ab1 = (r1.y >> 6) & 7u;
+            ptx::mbar_wait_sleep(xfull(xs0), (r0.y >> 9) & 1u);
+            ptx::mbar_wait_sleep(afull0 + 8u * ab0, (r0.y >> 10) & 1u);
             if (pair) {
-                ptx::mbar_wait_sleep(xfull(xs1), xph1);
-                ptx::mbar_wait_sleep(afull(g1, b1), aph1);
+                ptx::mbar_wait_sleep(xfull(xs1), (r1.y >> 9) & 1u);
+                ptx::mbar_wait_sleep(afull0 + 8u * ab1, (r1.y >> 10) & 1u);
             }
             if (tr && lane == 0) {
                 if (jj == 0) utrace(7, 1);
                 utrace(4, jj);
             }
             ptx::tc_fence_after();
-            const int ncl = pair ? 2 : 1;
-            const bool seg_end = jj + ncl == ncell || KC + ncl == n_kc || (pair ? (ul + 2 == Ul) : (ul + 1 == Ul));
+            const bool seg_end = ((pair ? r1.y : r0.y) & kSegEnd) != 0;
             if (ptx::elect_one()) {
-                const uint64_t cd0 = cdesc0 + cslot * (uint64_t)xs;
-                const uint32_t ac0 = tmem + kA0 + (uint32_t)(g * kNBuf + b) * kACols;
+                const uint64_t cd0 = cdesc0 + cslot * xs0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    ptx::umma_f16_ts(dcol, ac0 + 8u * (uint32_t)i, cd0 + (uint64_t)(dstep * (uint32_t)i), idesc,
+                    ptx::umma_f16_ts(dcol, r0.x + 8u * (uint32_t)i, cd0 + (uint64_t)(dstep * (uint32_t)i), idesc,
                                      (first && i == 0) ? 0u : 1u);
-                ptx::umma_commit(aempty(g, b));
-                if (jj + XS < ncell) ptx::umma_commit(xempty(xs));
+                ptx::umma_commit(aempty0 + 8u * ab0);
+                if (r0.y & kCommitX) ptx::umma_commit(xempty(xs0));
                 if (pair) {
-                    const uint64_t cd1 = cdesc0 + cslot * (uint64_t)xs1;
-                    const uint32_t ac1 = tmem + kA0 + (uint32_t)(g1 * kNBuf + b1) * kACols;
+                    const uint64_t cd1 = cdesc0 + cslot * xs1;
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
-                        ptx::umma_f16_ts(dcol, ac1 + 8u * (uint32_t)i, cd1 + (uint64_t)(dstep * (uint32_t)i), idesc, 1u);
-                    ptx::umma_commit(aempty(g1, b1));
-                    if (jj + 1 + XS < ncell) ptx::umma_commit(xempty(xs1));
+                        ptx::umma_f16_ts(dcol, r1.x + 8u * (uint32_t)i, cd1 + (uint64_t)(dstep * (uint32_t)i), idesc, 1u);
+                    ptx::umma_commit(aempty0 + 8u * ab1);
+                    if (r1.y & kCommitX) ptx::umma_commit(xempty(xs1));
                 }
-                if (seg_end) ptx::umma_commit(dfull(seg & 1));
+                if (seg_end) ptx::umma_commit(dfull((r0.y >> 14) & 1u));
             }
             __syncwarp();
             if (tr && lane == 0) utrace(5, jj);
-            if (seg_end) ++seg;
-            advance();
-            if (pair) advance();
-            jj += ncl;
+            jj += pair ? 2 : 1;
         }
     } else if (warp < 6) {
         // ================= epilogue warpgroup (warps 2-5: the four TMEM lane quadrants): D (thread =
@@ -474,7 +465,7 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
 struct UmmaPlan {
     int S, BP, N, XS;
     int64_t P, W, U;
-    uint32_t xcol, off_ring, off_x;
+    uint32_t xcol, off_ring, off_x, off_rec;
     size_t smem;
 };
 
@@ -492,14 +483,16 @@ bool umma_plan(const Layout& lay, int code, int64_t B, int G, int64_t nrb, UmmaP
     const int S = umma_stages(lay.k, code);
     pl->S = S;
     const size_t pad = 512;                                           // the last slab's overlapping core-matrix rows
-    const size_t fixed = kHdr + lutb + (size_t)S * cell + pad;
+    const size_t recb = (size_t)(((pl->U + pl->P - 1) / pl->P + 1) * 8 + 15) & ~(size_t)15;   // MMA cell records
+    const size_t fixed = kHdr + lutb + (size_t)S * cell + pad + recb;
     if (fixed >= max_smem) return false;
     const int64_t fit = (int64_t)((max_smem - fixed) / pl->xcol);
     pl->XS = (int)std::min<int64_t>(fit, kMaxXS);
     if (pl->XS < 2) return false;
     pl->off_ring = (uint32_t)(kHdr + lutb);
     pl->off_x = (uint32_t)(kHdr + lutb + (size_t)S * cell);
-    pl->smem = pl->off_x + (size_t)pl->XS * pl->xcol + pad;
+    pl->off_rec = (uint32_t)(pl->off_x + (size_t)pl->XS * pl->xcol + pad);
+    pl->smem = pl->off_rec + recb;
     if ((uint64_t)pl->U * (uint64_t)(pl->W + 1) >= (1ull << 31)) return false;   // 32-bit index math in the kernel
     return pl->smem <= max_smem;
 }
@@ -567,6 +560,7 @@ cudaError_t launch_umma(const Layout& lay, int code, const CodeArgs& ca, int G, 
     a.code_factor = cf;
     a.off_ring = pl.off_ring;
     a.off_x = pl.off_x;
+    a.off_rec = pl.off_rec;
     a.xcol_bytes = pl.xcol;
     a.XS = pl.XS;
     a.lbo = 16u * (uint32_t)pl.BP;
