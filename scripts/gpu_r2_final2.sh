@@ -19,8 +19,4 @@ for B in 1 16; do timeout 300 python scripts/stage_flags.py hyb 4 $B 0 > $O/flag
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-70b > $O/launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemv|layer_kernel|umma" -s 700 -c 4 -o $O/prof_gemv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-70b > $O/prof_gemv.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"umma" -s 40 -c 2 -o $O/prof_umma_hyb4 python bench.py --code hyb --k 4 --steps 1 --warmup 3 --no-cpu-baseline --no-70b > $O/prof_umma.log 2>&1
-T="tests/test_gpu_parity.py::test_matvec_small[1-3inst-2-7] tests/test_gpu_parity.py::test_matvec_small[16-hyb-4-7] tests/test_gpu_parity.py::test_matvec_small[4-hyb-3-7] tests/test_gpu_parity.py::test_rht_matches_oracle[16-11008] tests/test_gpu_parity.py::test_rht_matches_oracle[16-28672] tests/test_gpu_parity.py::test_grouped_matvec_against_oracle"
-timeout 900 compute-sanitizer --tool memcheck python -m pytest $T -q -x > $O/sanitizer_memcheck.txt 2>&1
-timeout 900 compute-sanitizer --tool racecheck python -m pytest $T -q -x > $O/sanitizer_racecheck.txt 2>&1
-timeout 900 compute-sanitizer --tool synccheck python -m pytest $T -q -x > $O/sanitizer_synccheck.txt 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv >> $O/gpu.txt 2>&1
