@@ -96,6 +96,7 @@ struct UmmaArgs {
 // Debug timeline of CTA 0 (qtip_internal_set_umma_trace; null in normal operation): u64 clock64
 // stamps at [kind * 64 + index].  The pointer is read once per thread at kernel start.
 __device__ unsigned long long* g_umma_trace = nullptr;
+__device__ int g_umma_trace_cta = 0;                 // the traced CTA
 __device__ __forceinline__ void utrace_at(unsigned long long* t, int kind, int64_t idx) {
     if (t != nullptr && idx < 64) t[kind * 64 + idx] = clock64();
 }
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    unsigned long long* const trc = blockIdx.x == 0 ? g_umma_trace : nullptr;
+    unsigned long long* const trc = (int)blockIdx.x == g_umma_trace_cta ? g_umma_trace : nullptr;
     const uint32_t bar0 = ptx::smem_u32(smem);
     auto full = [&](int s) { return bar0 + 8u * s; };
     auto empty = [&](int s) { return bar0 + 8u * (S + s); };
@@ -588,6 +589,10 @@ cudaError_t launch_umma(const Layout& lay, int code, const CodeArgs& ca, int G, 
 }
 
 }  // namespace qtip
+
+extern "C" int qtip_internal_set_umma_trace_cta(int cta) {
+    return (int)cudaMemcpyToSymbol(qtip::g_umma_trace_cta, &cta, sizeof(cta));
+}
 
 extern "C" int qtip_internal_set_umma_trace(void* dptr) {
     unsigned long long* p = (unsigned long long*)dptr;

@@ -28,6 +28,7 @@ for _ in range(3):
     lay(x)
 torch.cuda.synchronize()
 lib.qtip_internal_set_umma_trace.argtypes = [ctypes.c_void_p]
+lib.qtip_internal_set_umma_trace_cta(int(os.environ.get("TRACE_CTA", "0")))
 lib.qtip_internal_set_umma_trace(ctypes.c_void_p(buf.data_ptr()))
 lay(x)
 torch.cuda.synchronize()
