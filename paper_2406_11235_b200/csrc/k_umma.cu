@@ -406,19 +406,26 @@ __global__ void __launch_bounds__(kUThreads, 1) umma_gemv_kernel(const __grid_co
                 if (s_last) {
                     __threadfence();
                     const int cnt = (int)(w1 - w0 + 1);
+                    // four batch columns at a time with all their segment loads in flight: one L2 round
+                    // trip per 4 columns (per column, it was 16 dependent round trips at B = 16: ncu had
+                    // the batch-16 launch at 37 vs 22 us, warps parked at the exit barrier behind it)
+                    for (int cb = 0; cb < a.B; cb += 4) {
+                        float t[8][4];
 #pragma unroll
-                    for (int bb = 0; bb < N; ++bb) {
-                        if (bb >= a.B) break;
-                        const float* sp = segp + bb * 128;
-                        float t[8];
+                        for (int j = 0; j < 8; ++j)
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) t[j] = j < cnt ? __ldcg(sp + (int64_t)j * a.BP * 128) : 0.0f;
-                        float acc = t[0];
+                            for (int i = 0; i < 4; ++i)
+                                t[j][i] = (j < cnt && cb + i < a.B) ? __ldcg(segp + (int64_t)j * a.BP * 128 + (cb + i) * 128) : 0.0f;
 #pragma unroll
-                        for (int j = 1; j < 8; ++j)
-                            if (j < cnt) acc += t[j];
-                        for (int j = 8; j < cnt; ++j) acc += __ldcg(sp + (int64_t)j * a.BP * 128);
-                        if (live) yo[bb * a.ys] = acc * sc;
+                        for (int i = 0; i < 4; ++i) {
+                            if (cb + i >= a.B) break;
+                            float acc = t[0][i];                     // range order: a fixed association
+#pragma unroll
+                            for (int j = 1; j < 8; ++j)
+                                if (j < cnt) acc += t[j][i];
+                            for (int j = 8; j < cnt; ++j) acc += __ldcg(segp + (int64_t)j * a.BP * 128 + (cb + i) * 128);
+                            if (live) yo[(cb + i) * a.ys] = acc * sc;
+                        }
                     }
                 }
             }
